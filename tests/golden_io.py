@@ -1,0 +1,44 @@
+"""Loader for the committed golden vectors (tests/golden/golden_s5.npz)."""
+
+from __future__ import annotations
+
+import json
+from functools import lru_cache
+from pathlib import Path
+
+import numpy as np
+
+PATH = Path(__file__).resolve().parent / "golden" / "golden_s5.npz"
+
+
+@lru_cache(maxsize=1)
+def load():
+    z = np.load(PATH)
+    arrays = {k: z[k] for k in z.files}
+    meta = json.loads(arrays.pop("meta").tobytes().decode())
+    return arrays, meta
+
+
+def cases():
+    return sorted(load()[1]["cases"])
+
+
+def case(name):
+    arrays, meta = load()
+    pre = name + "/"
+    out = {k[len(pre):]: v for k, v in arrays.items() if k.startswith(pre)}
+    out.update(meta["cases"][name])
+    out["buffer_bytes"] = out["buffer"].tobytes()
+    return out
+
+
+def kats():
+    return sorted(load()[1]["kat"])
+
+
+def kat(name):
+    arrays, meta = load()
+    pre = name + "/"
+    out = {k[len(pre):]: v for k, v in arrays.items() if k.startswith(pre)}
+    out.update(meta["kat"][name])
+    return out
