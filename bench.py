@@ -1,0 +1,334 @@
+#!/usr/bin/env python
+"""Benchmark: GPU S^5 string sort with LCP array (BASELINE.json metric).
+
+One "step" = one full sort (handles + LCP array) of the workload, inputs
+resident in HBM.  Default workload: BASELINE.json configs[1] (C2, 2^24 DNA
+reads of length 100, seed 1).  Prints ONE JSON line on rank 0.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2_dna]
+  python bench.py --impl reference ...   # CPU S^5 (oracle port), all host cores
+
+The arena (1.69 GB at C2) is larger than the 126 MB L2, so no explicit L2
+flush is needed between timed steps.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "strings/sec (+ D-bytes/sec) of S^5 sort with LCP array"
+UNIT = "strings/s"
+PEAKS = ROOT / "MEASURED_PEAKS.json"
+FALLBACK_HBM = 6650.0  # GB/s, B200_PROFILING.md fallback
+
+
+def hbm_peak():
+    try:
+        d = json.loads(PEAKS.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return FALLBACK_HBM, "fallback (B200_PROFILING.md)"
+
+
+def b_alg(n: int, D: int) -> int:
+    """Algorithmic bytes of a sort: 24*(floor(D/8) + n) + 8n."""
+    return 24 * (D // 8 + n) + 8 * n
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200", "-f", self.path],
+                stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+            time.sleep(0.3)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        try:
+            for line in open(self.path):
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) >= 9:
+                    rows.append(parts)
+        except OSError:
+            pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i] == "Active"})
+        busy = [s for s in sm if mx and s > 0.3 * max(mx)] or sm
+        return {"sm_mhz": statistics.median(busy) if busy else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(rows)}
+
+
+def cpu_reference(buf, hnd, sample_n: int, reps: int, threads: int):
+    """The reference's CPU S^5 (oracle port of parallel_s5, parallel.py:468-492)
+    on a bounded prefix sample.  Returns (strings/s, seconds list)."""
+    import oracle
+
+    if sample_n < len(hnd):
+        end = int(hnd[sample_n])  # packed configs: the prefix is a self-contained set
+        sbuf, shnd = buf[:end], hnd[:sample_n]
+    else:
+        sbuf, shnd = buf, hnd
+    times = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        oracle.parallel_s5(sbuf, shnd, p=threads, want_lcps=True)
+        times.append(time.perf_counter() - t0)
+    return len(shnd) / statistics.median(times), times
+
+
+def load_config(name: str, scale: float):
+    from paper_1403_2056_b200 import corpora
+
+    return corpora.CONFIGS[name](scale)
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    threads = os.cpu_count() or 1
+    buf, hnd = load_config(args.config, args.scale)
+    n = len(hnd)
+    sample = min(n, args.cpu_sample)
+    for _ in range(args.warmup):
+        cpu_reference(buf, hnd, sample, 1, threads)
+    rate, times = cpu_reference(buf, hnd, sample, args.steps, threads)
+    total = sum(times)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1000 * total / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "config": {"workload": args.config, "n": n, "scale": args.scale,
+                   "sample_strings": sample, "parallelism": f"cpu{threads}"},
+        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"first {sample} strings of {args.config} "
+                                   f"(oracle/s5_oracle.c parallel_s5, {threads} OpenMP threads, "
+                                   f"{cpu_model()})"},
+        "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def dist_stats_device(ds, out_h, lcps):
+    """(D, L) of the sorted set on the GPU (strset.py:290-309 convention)."""
+    import torch
+
+    n = out_h.numel()
+    zeros = torch.nonzero(ds.arena[: ds.arena_len] == 0).squeeze(1)
+    ends = zeros[torch.searchsorted(zeros, out_h)]
+    lens = ends - out_h
+    h = torch.zeros(n + 1, dtype=torch.int64, device=out_h.device)
+    h[1:n] = lcps[1:]
+    neighbor = torch.maximum(h[:n], h[1:])
+    D = int(torch.minimum(lens + 1, neighbor + 1).sum())
+    L = int(lcps[1:].sum())
+    return D, L
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1403_2056_b200 import _lib
+    from paper_1403_2056_b200 import device as DV
+
+    rank, world, local = dist_env()
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    dev = torch.device("cuda", torch.cuda.current_device())
+    buf, hnd = load_config(args.config, args.scale)
+    n = len(hnd)
+    threads = os.cpu_count() or 1
+
+    cpu_line = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        sample = min(n, args.cpu_sample)
+        rate, times = cpu_reference(buf, hnd, sample, 1, threads)
+        cpu_line = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
+                    "sample": f"first {sample} strings of {args.config}, 1 rep, "
+                              f"{times[0]:.2f} s (oracle/s5_oracle.c parallel_s5, "
+                              f"{threads} OpenMP threads, {cpu_model()})"}
+
+    ds = DV.upload(buf, hnd, dev)
+    ws = torch.empty(DV.workspace_bytes(n, 1 << 20), dtype=torch.uint8, device=dev)
+    out = (torch.empty(n, dtype=torch.int64, device=dev),
+           torch.empty(n, dtype=torch.int64, device=dev))
+
+    def step():
+        return DV.sort(ds, want_lcps=True, out=out, workspace=ws)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    D, L = dist_stats_device(ds, out[0], out[1])
+
+    stream = torch.cuda.current_stream()
+    _lib.profile(enable=True, reset=True)
+    l0 = _lib.launch_count()
+    with ClockSampler(dev.index) as clk:
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    launches = _lib.launch_count() - l0
+    prof = _lib.profile(enable=False)
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    total_strings = n * world
+    value = total_strings / (ms_step / 1000.0)
+
+    # end to end through the public C ABI on pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        pin_buf = torch.empty(len(buf), dtype=torch.uint8, pin_memory=True)
+        pin_buf.numpy()[:] = buf
+        pin_h = torch.empty(n, dtype=torch.int64, pin_memory=True)
+        pin_h.numpy()[:] = hnd
+        pin_oh = torch.empty(n, dtype=torch.int64, pin_memory=True).numpy()
+        pin_ol = torch.empty(n, dtype=torch.int64, pin_memory=True).numpy()
+        bnp, hnp = pin_buf.numpy(), pin_h.numpy()
+        DV.sort_host(bnp, hnp, out_handles=pin_oh, out_lcps=pin_ol)  # warm-up
+        ts = []
+        for _ in range(max(1, min(args.steps, 3))):
+            t0 = time.perf_counter()
+            DV.sort_host(bnp, hnp, out_handles=pin_oh, out_lcps=pin_ol)
+            ts.append(time.perf_counter() - t0)
+        assert np.array_equal(pin_oh, out[0].cpu().numpy())
+        e2e = {"value": n / statistics.median(ts), "unit": UNIT,
+               "h2d_bytes_per_step": int(len(buf) + 8 * n),
+               "d2h_bytes_per_step": int(16 * n), "ms_per_step": 1000 * statistics.median(ts)}
+
+    peak, peak_src = hbm_peak()
+    kernels = {k: v for k, v in prof.items() if v["launches"]}
+    top = max(kernels, key=lambda k: kernels[k]["ms"])
+    kt = kernels[top]
+    ach = kt["bytes"] / (kt["ms"] / 1000.0) / 1e9 if kt["ms"] > 0 else 0.0
+    sort_gbs = b_alg(n, D) / (ms_step / 1000.0) / 1e9
+    step_ms_sum = sum(v["ms"] for v in kernels.values()) / args.steps
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "config": {"workload": args.config, "n": n, "N_bytes": int(len(buf)), "scale": args.scale,
+                   "D": D, "L": L, "parallelism": f"dp{world}" if world > 1 else "1gpu",
+                   "l2": "inputs larger than L2 (arena > 126 MB), no flush"},
+        "d_bytes_per_s": D * world / (ms_step / 1000.0),
+        "roofline": {"bound": "hbm", "kernel": top, "achieved": ach, "peak": peak,
+                     "unit": "GB/s", "frac": ach / peak, "traffic": None,
+                     "peak_source": peak_src,
+                     "share_of_step": kt["ms"] / args.steps / ms_step},
+        "sort_roofline": {"b_alg_bytes": b_alg(n, D), "achieved": sort_gbs,
+                          "frac": sort_gbs / peak, "unit": "GB/s"},
+        "kernels": {k: {"ms_per_step": v["ms"] / args.steps,
+                        "launches_per_step": v["launches"] / args.steps,
+                        "GBps": v["bytes"] / (v["ms"] / 1000) / 1e9 if v["ms"] else None}
+                    for k, v in kernels.items()},
+        "kernel_ms_per_step": step_ms_sum,
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+        "cpu_baseline": cpu_line,
+        "e2e": e2e,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="c2_dna")
+    ap.add_argument("--scale", type=float, default=1.0)
+    ap.add_argument("--cpu-sample", type=int, default=1 << 22)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args(argv)
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,145 @@
+/*
+ * s5g.h -- C ABI of the B200-native S^5 string sorter (libs5gpu.so).
+ *
+ * Drop-in boundary for the reference's sort entry points
+ *   strsort.ssss.s5_sort        /root/reference/pkg/src/strsort/ssss.py:361-387
+ *   strsort.parallel.parallel_s5 /root/reference/pkg/src/strsort/parallel.py:468-492
+ * and the return convention SortedWithLcp (basecase.py:21-33): the stable
+ * content order of the input handles plus an int64 LCP array with
+ * lcps[0] = LCP_UNDEF = -1 (strset.py:31).
+ *
+ * Conventions
+ *  - Plain pointers and sizes only.  "device" pointers are CUDA device
+ *    memory of the current device; "host" pointers are host memory.
+ *  - Return 0 on success, a negative S5G_E* code on failure; the message is
+ *    in s5g_last_error() (thread-local).
+ *  - Calls are synchronous: all work is complete when they return.
+ *  - Arena: 0-terminated strings back to back; every handle h satisfies
+ *    0 <= h < arena_len and the string at h ends at a 0 byte.  The arena
+ *    pointer must be 8-byte aligned and readable for S5G_ARENA_PAD bytes
+ *    past arena_len (bytes there are never interpreted as characters).
+ */
+#ifndef S5G_H
+#define S5G_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define S5G_VERSION 1
+#define S5G_ARENA_PAD 16
+
+#define S5G_OK 0
+#define S5G_E_INVALID (-1)      /* bad argument (ValueError) */
+#define S5G_E_VARIANT (-2)      /* unknown classify variant (ValueError) */
+#define S5G_E_CUDA (-3)         /* CUDA runtime error */
+#define S5G_E_WORKSPACE (-4)    /* workspace too small */
+#define S5G_E_NCCL (-5)         /* reserved for the multi-GPU exchange */
+
+#define S5G_VARIANT_UNROLL 0    /* ssss.py:160-169 */
+#define S5G_VARIANT_EQUAL 1     /* ssss.py:170-180 */
+
+/* Mirror of strsort.counters.SortStats (counters.py:13-36). */
+typedef struct s5g_stats {
+    int64_t char_cmps;
+    int64_t word_fetches;      /* 8-byte arena word loads actually issued */
+    int64_t merge_buffer_cmps;
+    int64_t scratch_words;
+    int64_t jobs_enqueued;     /* segments queued (S^5 steps + CTA segments) */
+    int64_t jobs_executed;
+    int64_t share_events;
+} s5g_stats;
+
+/* Step hook, the analogue of step_hook(StepRecord) (ssss.py:215-224,
+ * 340-341): called on the host after every device-wide S^5 step with the
+ * bucket bounds (2v+2 entries, relative to lo) and the v in-order splitters. */
+typedef void (*s5g_step_cb)(void *ctx, int64_t lo, int64_t hi, int64_t depth, int64_t v,
+                            const int64_t *bounds, const uint64_t *inorder);
+
+typedef struct s5g_sort_args {
+    const uint8_t *arena;      /* device */
+    int64_t arena_len;
+    const int64_t *handles;    /* device, n; never modified */
+    int64_t n;
+    int64_t depth;             /* common prefix length of all strings */
+    int64_t *out_handles;      /* device, n */
+    int64_t *out_lcps;         /* device, n, or NULL */
+    uint8_t *out_dchar;        /* device, n, or NULL (needs out_lcps) */
+    void *workspace;           /* device, s5g_workspace_bytes() bytes */
+    size_t workspace_bytes;
+    void *stream;              /* cudaStream_t (NULL = default stream) */
+    int32_t variant;           /* S5G_VARIANT_* */
+    int32_t v;                 /* splitter cap (tuning only; clamped to 8191) */
+    uint64_t seed;             /* sampling seed (tuning only) */
+    int64_t t_medium;          /* segments below this may finish in one CTA */
+    s5g_stats *stats;          /* host, accumulated into; may be NULL */
+    s5g_step_cb step_cb;       /* may be NULL */
+    void *step_ctx;
+} s5g_sort_args;
+
+/* Sort on device buffers.  Replaces s5_sort (ssss.py:361). */
+int s5g_sort(const s5g_sort_args *args);
+
+/* Device workspace needed by s5g_sort for n strings and this t_medium. */
+size_t s5g_workspace_bytes(int64_t n, int64_t t_medium);
+
+/* Sort on HOST buffers (copies in, sorts, copies out; device memory is
+ * managed internally).  This is the reference-facing end-to-end call:
+ * s5_sort(sset, want_lcps=...) with sset.buffer/handles in host memory.
+ * out_lcps / out_dchar may be NULL. */
+int s5g_sort_host(const uint8_t *arena, int64_t arena_len, const int64_t *handles, int64_t n,
+                  int64_t depth, int64_t *out_handles, int64_t *out_lcps, uint8_t *out_dchar,
+                  int32_t variant, int32_t v, uint64_t seed, int64_t t_medium,
+                  s5g_stats *stats);
+
+/* --- kernel-level entry points (parity tests of single rows of the path) --- */
+
+/* extract_keys (strset.py:152-170), exact semantics for any depth. */
+int s5g_extract_keys(const uint8_t *arena, int64_t arena_len, const int64_t *handles, int64_t n,
+                     int64_t depth, uint64_t *out_keys, void *stream);
+
+/* select_splitters (ssss.py:85-146) on a sorted device sample of `count`
+ * keys: level-order tree[v+1], inorder[v], term_pos[v] (uint8),
+ * eq_bucket[v+1] (uint16, 2*eq_leftmost[node_to_inorder[node]]+1). */
+int s5g_select_splitters(const uint64_t *sample, int64_t count, int64_t v, uint64_t *tree,
+                         uint64_t *inorder, uint8_t *term_pos, uint16_t *eq_bucket,
+                         void *stream);
+
+/* classify_keys (ssss.py:149-181) against a level-order tree (v+1 entries,
+ * index 0 unused) and eq_bucket table (v+1, used by the equal variant). */
+int s5g_classify(const uint64_t *keys, int64_t n, const uint64_t *tree,
+                 const uint16_t *eq_bucket, int64_t v, int32_t variant, uint16_t *out_bucket,
+                 void *stream);
+
+/* fill_dchar (basecase.py:36-42). */
+int s5g_fill_dchar(const uint8_t *arena, const int64_t *handles, const int64_t *lcps, int64_t n,
+                   uint8_t *out_dchar, void *stream);
+
+/* --- instrumentation ------------------------------------------------------ */
+
+/* Per-kernel-class device time, recorded with CUDA events on the launching
+ * stream around every launch of s5g_sort while enabled. */
+typedef struct s5g_kernel_profile {
+    char name[32];
+    int64_t launches;
+    int64_t units;     /* elements (or segments / records) the launches covered */
+    double ms;         /* summed event-timed duration */
+    int64_t bytes;     /* summed algorithmic bytes (DESIGN.md kernel models) */
+} s5g_kernel_profile;
+
+void s5g_profile_enable(int on);
+void s5g_profile_reset(void);
+int s5g_profile_read(s5g_kernel_profile *out, int max_entries);
+/* Monotonic count of kernels this library has launched (all entry points). */
+unsigned long long s5g_launch_count(void);
+
+const char *s5g_last_error(void);
+int s5g_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* S5G_H */

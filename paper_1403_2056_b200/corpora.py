@@ -1,0 +1,203 @@
+"""Seeded synthetic corpora for the five BASELINE.json configurations.
+
+The paper's data sets (URL crawl, GOV2, Wikipedia, Sinha's DNA / NoDup) are
+not available; these frozen generators stand in for them with the shapes,
+sizes and value distributions BASELINE.json names:
+
+  C1  random   : exactly strsort.bench.gen_random(n, seed) (bench.py:31-46):
+                 lengths U[0,20), bytes U[33,127)
+  C2  dna      : n = 2^24 reads of length 100 over ACGT with p = .3/.2/.2/.3
+  C3  urls     : n = 2^23 'http://' + Zipf(1.1) host from 10,000 seeded hosts
+                 + 1-4 '/'-segments from a finite per-host pool (duplicates)
+  C4  suffixes : all 2^24 suffixes of an order-2 Markov text over a-z with
+                 5% of the text overwritten by copies of earlier 1-4 KB blocks
+  C5  nodup    : n = 2^28, lengths U[32,200]: 16-char prefix from a 2^16-word
+                 vocabulary + lowercase filler + unique 6-char base-36 counter
+
+Every generator returns (buffer: np.ndarray[uint8], handles: np.ndarray[int64]).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+ALPHA = np.frombuffer(b"abcdefghijklmnopqrstuvwxyz", dtype=np.uint8)
+B36 = np.frombuffer(b"0123456789abcdefghijklmnopqrstuvwxyz", dtype=np.uint8)
+
+
+def _pack_lengths(lens: np.ndarray, fill) -> tuple[np.ndarray, np.ndarray]:
+    """Buffer of zero-terminated strings with the given lengths; fill(total)
+    returns the characters in order."""
+    n = len(lens)
+    total = int(lens.sum())
+    offsets = np.zeros(n, dtype=np.int64)
+    if n:
+        np.cumsum(lens[:-1] + 1, out=offsets[1:])
+    buf = np.zeros(total + n, dtype=np.uint8)
+    chars = fill(total)
+    mask = np.ones(total + n, dtype=bool)
+    mask[offsets + lens] = False
+    buf[mask] = chars
+    return buf, offsets
+
+
+def gen_random(n: int = 1_000_000, seed: int = 0):
+    """C1: identical bytes to strsort.bench.gen_random(n, seed)."""
+    rng = np.random.default_rng(seed)
+    lens = rng.integers(0, 20, size=n, dtype=np.int64)
+    total = int(lens.sum())
+    chars = rng.integers(33, 127, size=total, dtype=np.uint8).astype(np.uint8)
+    return _pack_lengths(lens, lambda t: chars)
+
+
+def gen_dna(n: int = 1 << 24, length: int = 100, seed: int = 1):
+    """C2: fixed-length reads, i.i.d. A/C/G/T with probabilities .3/.2/.2/.3."""
+    rng = np.random.default_rng(seed)
+    table = np.frombuffer(b"AAACCGGTTT", dtype=np.uint8)
+    buf = np.zeros((n, length + 1), dtype=np.uint8)
+    step = max(1, (1 << 26) // (length + 1))
+    for lo in range(0, n, step):
+        hi = min(n, lo + step)
+        buf[lo:hi, :length] = table[rng.integers(0, 10, size=(hi - lo, length), dtype=np.uint8)]
+    return buf.reshape(-1), np.arange(n, dtype=np.int64) * (length + 1)
+
+
+def _expand(pieces: np.ndarray, piece_off: np.ndarray, piece_len: np.ndarray,
+            seq: np.ndarray, per_string: np.ndarray):
+    """Concatenate piece ids `seq` (grouped per string by `per_string`
+    counts) into a zero-terminated buffer."""
+    plen = piece_len[seq]
+    slen = np.add.reduceat(plen, np.r_[0, np.cumsum(per_string)[:-1]]) if len(seq) else plen
+    n = len(per_string)
+    str_off = np.zeros(n, dtype=np.int64)
+    np.cumsum(slen[:-1] + 1, out=str_off[1:])
+    # output offset of every piece occurrence
+    first_piece = np.r_[0, np.cumsum(per_string)[:-1]]
+    within = np.arange(len(seq), dtype=np.int64) - np.repeat(first_piece, per_string)
+    pcum = np.cumsum(plen) - plen  # global exclusive prefix of piece lengths
+    str_piece_base = pcum[first_piece]
+    piece_out = np.repeat(str_off, per_string) + (pcum - np.repeat(str_piece_base, per_string))
+    del within
+    total = int(str_off[-1] + slen[-1] + 1)
+    buf = np.zeros(total, dtype=np.uint8)
+    # byte-level gather, in chunks to bound memory
+    CH = 1 << 22
+    for lo in range(0, len(seq), CH):
+        hi = min(len(seq), lo + CH)
+        pl = plen[lo:hi]
+        src = np.repeat(piece_off[seq[lo:hi]], pl)
+        dst = np.repeat(piece_out[lo:hi], pl)
+        k = np.arange(len(src), dtype=np.int64) - np.repeat(np.cumsum(pl) - pl, pl)
+        buf[dst + k] = pieces[src + k]
+    return buf, str_off
+
+
+def gen_urls(n: int = 1 << 23, seed: int = 2, hosts: int = 10_000, pool: int = 48,
+             zipf_s: float = 1.1):
+    """C3: URL-like strings with Zipf host popularity and duplicate paths."""
+    rng = np.random.default_rng(seed)
+    # piece table: [0] 'http://', hosts, then per-host '/'+segment pools
+    texts: list[bytes] = [b"http://"]
+    hlen = rng.integers(8, 21, size=hosts)
+    for L in hlen:
+        texts.append(bytes(ALPHA[rng.integers(0, 26, size=int(L))]) + b".com")
+    seg_base = len(texts)
+    slen = rng.integers(3, 13, size=hosts * pool)
+    for L in slen:
+        texts.append(b"/" + bytes(ALPHA[rng.integers(0, 26, size=int(L))]))
+    piece_len = np.array([len(t) for t in texts], dtype=np.int64)
+    piece_off = np.r_[0, np.cumsum(piece_len)[:-1]].astype(np.int64)
+    pieces = np.frombuffer(b"".join(texts), dtype=np.uint8)
+    ranks = np.arange(1, hosts + 1, dtype=np.float64)
+    p = ranks ** -zipf_s
+    p /= p.sum()
+    host = rng.choice(hosts, size=n, p=p)
+    nseg = rng.integers(1, 5, size=n)
+    per = 2 + nseg
+    seq = np.empty(int(per.sum()), dtype=np.int64)
+    start = np.r_[0, np.cumsum(per)[:-1]]
+    seq[start] = 0
+    seq[start + 1] = 1 + host
+    for j in range(4):
+        has = nseg > j
+        seg = rng.integers(0, pool, size=int(has.sum()))
+        seq[start[has] + 2 + j] = seg_base + host[has] * pool + seg
+    return _expand(pieces, piece_off, piece_len, seq, per)
+
+
+def gen_suffix_markov(n: int = 1 << 24, seed: int = 3, copy_frac: float = 0.05,
+                      chains: int = 1024):
+    """C4: suffixes of an order-2 Markov text with copied 1-4 KB blocks.
+
+    The text is generated as `chains` independent order-2 chains (seeded
+    transition table, Dirichlet(0.3) rows) laid end to end, then 5% of it is
+    overwritten, left to right, by copies of earlier 1024-4096-byte blocks."""
+    rng = np.random.default_rng(seed)
+    trans = rng.dirichlet(np.full(26, 0.3), size=26 * 26)
+    cdf = np.cumsum(trans, axis=1)
+    cdf[:, -1] = 1.0
+    per = (n + chains - 1) // chains
+    text = np.zeros((chains, per), dtype=np.uint8)
+    a = rng.integers(0, 26, size=chains)
+    b = rng.integers(0, 26, size=chains)
+    u = rng.random(size=(per, chains))
+    for t in range(per):
+        row = cdf[a * 26 + b]
+        c = (row < u[t][:, None]).sum(axis=1)
+        c = np.minimum(c, 25)
+        text[:, t] = c
+        a, b = b, c
+    text = text.reshape(-1)[:n]
+    copied = 0
+    target = int(copy_frac * n)
+    while copied < target:
+        L = int(rng.integers(1024, 4097))
+        p = int(rng.integers(L + 1, n - L))
+        q = int(rng.integers(0, p - L))
+        text[p:p + L] = text[q:q + L]
+        copied += L
+    buf = np.empty(n + 1, dtype=np.uint8)
+    buf[:n] = ALPHA[text]
+    buf[n] = 0
+    return buf, np.arange(n, dtype=np.int64)
+
+
+def gen_nodup(n: int = 1 << 28, seed: int = 4, vocab: int = 1 << 16):
+    """C5: unique strings, lengths U[32,200]: 16-char vocabulary prefix,
+    lowercase filler, 6-char base-36 counter (36^6 > 2^28 keeps them unique)."""
+    rng = np.random.default_rng(seed)
+    words = ALPHA[rng.integers(0, 26, size=(vocab, 16))]
+    lens = rng.integers(32, 201, size=n).astype(np.int64)
+    offsets = np.zeros(n, dtype=np.int64)
+    np.cumsum(lens[:-1] + 1, out=offsets[1:])
+    buf = np.zeros(int(lens.sum()) + n, dtype=np.uint8)
+    CH = 1 << 20
+    for lo in range(0, n, CH):
+        hi = min(n, lo + CH)
+        m = hi - lo
+        L = lens[lo:hi]
+        off = offsets[lo:hi] - offsets[lo]
+        seg = np.zeros(int(L.sum()) + m, dtype=np.uint8)
+        fill = ALPHA[rng.integers(0, 26, size=len(seg), dtype=np.uint8)]
+        mask = np.ones(len(seg), dtype=bool)
+        mask[off + L] = False
+        seg[mask] = fill[mask]
+        w = words[rng.integers(0, vocab, size=m)]
+        seg[(off[:, None] + np.arange(16)).reshape(-1)] = w.reshape(-1)
+        cnt = np.arange(lo, hi, dtype=np.int64)
+        digits = np.empty((m, 6), dtype=np.uint8)
+        for j in range(5, -1, -1):
+            digits[:, j] = B36[cnt % 36]
+            cnt //= 36
+        seg[(off[:, None] + (L - 6)[:, None] + np.arange(6)).reshape(-1)] = digits.reshape(-1)
+        buf[offsets[lo]: offsets[lo] + len(seg)] = seg
+    return buf, offsets
+
+
+CONFIGS = {
+    "c1_random": lambda scale=1.0: gen_random(int(1_000_000 * scale), 0),
+    "c2_dna": lambda scale=1.0: gen_dna(int((1 << 24) * scale), 100, 1),
+    "c3_urls": lambda scale=1.0: gen_urls(int((1 << 23) * scale), 2),
+    "c4_suffixes": lambda scale=1.0: gen_suffix_markov(int((1 << 24) * scale), 3),
+    "c5_nodup": lambda scale=1.0: gen_nodup(int((1 << 28) * scale), 4),
+}

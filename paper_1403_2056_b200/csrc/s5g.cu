@@ -1,0 +1,1083 @@
+// s5g.cu -- kernels, host driver and C ABI of the B200 S^5 sorter.
+//
+// Host driver = the GPU form of s5_sort_items (ssss.py:310-358) /
+// _ParallelS5Run.execute (parallel.py:400-445): rounds of batched
+// device-wide S^5 steps over "large" segments, then one launch that finishes
+// every small segment in a CTA, then the boundary-LCP fix-up.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "s5g.h"
+#include "s5g_kernels.cuh"
+
+namespace s5g {
+
+// ---------------------------------------------------------------------------
+// kernels
+
+__device__ __forceinline__ uint64_t exact_key(const uint8_t* arena, int64_t alen, int64_t h,
+                                              int64_t d) {
+    for (int64_t p = h; p < h + d; p++)
+        if (p >= alen || arena[p] == 0) return 0;
+    return load_key(arena, alen, h, d);
+}
+
+__global__ void k_extract_keys(const uint8_t* __restrict__ arena, int64_t alen,
+                               const int64_t* __restrict__ handles, int64_t n, int64_t depth,
+                               uint64_t* __restrict__ out) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) out[i] = exact_key(arena, alen, handles[i], depth);
+}
+
+// Copy handles into the work array and cache each string's first key.
+__global__ void k_init(const uint8_t* __restrict__ arena, int64_t alen,
+                       const int64_t* __restrict__ handles, int64_t n, int64_t depth,
+                       int64_t* __restrict__ hA, uint64_t* __restrict__ kA) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) {
+        int64_t h = handles[i];
+        hA[i] = h;
+        kA[i] = load_key(arena, alen, h, depth);
+    }
+}
+
+__global__ void __launch_bounds__(SAMPLE_NT) k_sample_tree(
+    const StepDev* __restrict__ steps, const uint8_t* __restrict__ arena, int64_t alen,
+    const int64_t* __restrict__ hX, const uint64_t* __restrict__ kX, uint64_t seed,
+    uint64_t* __restrict__ tree_g, uint64_t* __restrict__ inorder_g, uint8_t* __restrict__ tpos_g,
+    uint16_t* __restrict__ eqb_g) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    const StepDev sd = steps[blockIdx.x];
+    const int v = sd.v, count = OVERSAMPLE * v + OVERSAMPLE - 1, P = 2 * (v + 1);
+    uint64_t* s = reinterpret_cast<uint64_t*>(smem);
+    int16_t* sa = reinterpret_cast<int16_t*>(s + P);
+    int16_t* sb = sa + (v + 1);
+    int16_t* sp = sb + (v + 1);
+    // draw_sample (ssss.py:76-82): uniform positions from a counter-based
+    // stream keyed by (seed, lo, hi, depth) -- the tuple the reference seeds
+    // default_rng with; the picks never influence the output.
+    const uint64_t key0 = splitmix64(seed ^ splitmix64(sd.lo ^ splitmix64(sd.n ^ splitmix64(sd.depth))));
+    for (int j = threadIdx.x; j < P; j += SAMPLE_NT) {
+        uint64_t x = ~0ull;
+        if (j < count) {
+            int64_t idx = (int64_t)(splitmix64(key0 + j) % (uint64_t)sd.n);
+            x = sd.keys_valid ? kX[sd.lo + idx] : load_key(arena, alen, hX[sd.lo + idx], sd.depth);
+        }
+        s[j] = x;
+    }
+    __syncthreads();
+    bitonic_u64<SAMPLE_NT>(s, P);
+    select_tree<SAMPLE_NT>(s, count, v, sd.levels, sa, sb, sp, tree_g + sd.tree_off,
+                           inorder_g + sd.tree_off, tpos_g + sd.tree_off, eqb_g + sd.tree_off);
+}
+
+// Test entry: select_splitters on a given sorted sample.
+__global__ void __launch_bounds__(SAMPLE_NT) k_select_only(const uint64_t* sample, int count, int v,
+                                                           int L, uint64_t* tree, uint64_t* inorder,
+                                                           uint8_t* tpos, uint16_t* eqb) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    uint64_t* s = reinterpret_cast<uint64_t*>(smem);
+    int16_t* sa = reinterpret_cast<int16_t*>(s + count);
+    int16_t* sb = sa + (v + 1);
+    int16_t* sp = sb + (v + 1);
+    for (int j = threadIdx.x; j < count; j += SAMPLE_NT) s[j] = sample[j];
+    __syncthreads();
+    select_tree<SAMPLE_NT>(s, count, v, L, sa, sb, sp, tree, inorder, tpos, eqb);
+}
+
+// classify_keys (ssss.py:149-181).  Unroll: branch-free descent, tracking
+// the last splitter the key went left at (= inorder[leaf], the smallest
+// splitter >= key) for the single equality test.  Equal: early exit on a hit.
+template <int VARIANT>
+__device__ __forceinline__ uint32_t classify_one(uint64_t key, const uint64_t* tree,
+                                                 const uint16_t* eqb, int v, int L) {
+    int idx = 1;
+    if (VARIANT == S5G_VARIANT_UNROLL) {
+        uint64_t succ = 0;
+        for (int l = 0; l < L; l++) {
+            uint64_t t = tree[idx];
+            bool r = key > t;
+            succ = r ? succ : t;
+            idx = 2 * idx + r;
+        }
+        int leaf = idx - (v + 1);
+        return 2 * leaf + ((leaf < v) && key == succ);
+    } else {
+        for (int l = 0; l < L; l++) {
+            uint64_t t = tree[idx];
+            if (key == t) return eqb[idx];
+            idx = 2 * idx + (key > t);
+        }
+        return 2 * (idx - (v + 1));
+    }
+}
+
+template <int VARIANT>
+__global__ void __launch_bounds__(CLS_NT) k_classify(
+    const StepDev* __restrict__ steps, const int32_t* __restrict__ tile_step,
+    const uint8_t* __restrict__ arena, int64_t alen, const int64_t* __restrict__ hX,
+    uint64_t* __restrict__ kX, uint16_t* __restrict__ bid, uint32_t* __restrict__ cnt,
+    const uint64_t* __restrict__ tree_g, const uint16_t* __restrict__ eqb_g,
+    Counters* __restrict__ ctr) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    __shared__ __align__(8) uint64_t bar;
+    __shared__ unsigned fetched;
+    uint64_t* tree = reinterpret_cast<uint64_t*>(smem);            // VMAX+1
+    uint32_t* hist = reinterpret_cast<uint32_t*>(tree + VMAX + 1);  // NBMAX+1
+    uint16_t* eqb = reinterpret_cast<uint16_t*>(hist + NBMAX + 1);  // VMAX+1 (equal only)
+    const int t = blockIdx.x;
+    const StepDev sd = steps[tile_step[t]];
+    const int ti = t - (int)sd.tile0;
+    const int64_t beg = sd.lo + (int64_t)ti * TILE;
+    const int64_t end = min(beg + TILE, sd.lo + sd.n);
+    const int v = sd.v, L = sd.levels, nb = sd.nb;
+    const uint32_t tree_bytes = (uint32_t)(v + 1) * 8u;
+    if (threadIdx.x == 0) {
+        fetched = 0;
+        mbar_init(&bar, 1);
+        fence_mbar_init();
+        mbar_expect_tx(&bar, tree_bytes);
+        const uint8_t* src = reinterpret_cast<const uint8_t*>(tree_g + sd.tree_off);
+        for (uint32_t off = 0; off < tree_bytes; off += 32768u)
+            bulk_g2s(reinterpret_cast<uint8_t*>(tree) + off, src + off,
+                     min(32768u, tree_bytes - off), &bar);
+    }
+    for (int b = threadIdx.x; b < nb; b += CLS_NT) hist[b] = 0;
+    if (VARIANT == S5G_VARIANT_EQUAL)
+        for (int i = threadIdx.x; i <= v; i += CLS_NT) eqb[i] = eqb_g[sd.tree_off + i];
+    __syncthreads();
+    mbar_wait(&bar, 0);
+    const int lane = threadIdx.x & 31;
+    unsigned my_fetch = 0;
+    constexpr int U = 4;
+    for (int64_t base = beg; base < end; base += (int64_t)CLS_NT * U) {
+        uint64_t key[U];
+        bool ok[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            int64_t i = base + u * CLS_NT + threadIdx.x;
+            ok[u] = i < end;
+            key[u] = 0;
+            if (ok[u]) {
+                if (sd.keys_valid) {
+                    key[u] = kX[i];
+                } else {
+                    key[u] = load_key(arena, alen, hX[i], sd.depth);
+                    kX[i] = key[u];
+                    my_fetch++;
+                }
+            }
+        }
+        uint32_t b[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) b[u] = classify_one<VARIANT>(key[u], tree, eqb, v, L);
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            int64_t i = base + u * CLS_NT + threadIdx.x;
+            uint32_t mask = __ballot_sync(0xffffffffu, ok[u]);
+            if (ok[u]) {
+                bid[i] = (uint16_t)b[u];
+                uint32_t peers = __match_any_sync(mask, b[u]);
+                if (lane == __ffs(peers) - 1) atomicAdd(&hist[b[u]], (uint32_t)__popc(peers));
+            }
+        }
+    }
+    if (my_fetch) atomicAdd(&fetched, my_fetch);
+    __syncthreads();
+    uint32_t* row = cnt + sd.cnt_off + (int64_t)ti * nb;
+    for (int b = threadIdx.x; b < nb; b += CLS_NT) row[b] = hist[b];
+    if (threadIdx.x == 0 && fetched) atomicAdd(&ctr->fetches, (unsigned long long)fetched);
+}
+
+// Test entry: classify given keys against a given tree.
+template <int VARIANT>
+__global__ void k_classify_only(const uint64_t* __restrict__ keys, int64_t n,
+                                const uint64_t* __restrict__ tree_g,
+                                const uint16_t* __restrict__ eqb_g, int v, int L,
+                                uint16_t* __restrict__ out) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    uint64_t* tree = reinterpret_cast<uint64_t*>(smem);
+    uint16_t* eqb = reinterpret_cast<uint16_t*>(tree + v + 1);
+    for (int i = threadIdx.x; i <= v; i += blockDim.x) {
+        tree[i] = tree_g[i];
+        eqb[i] = eqb_g ? eqb_g[i] : 0;
+    }
+    __syncthreads();
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) out[i] = (uint16_t)classify_one<VARIANT>(keys[i], tree, eqb, v, L);
+}
+
+// Tile-minor running prefix per bucket column; bucket totals.
+__global__ void k_scan_cols(const StepDev* __restrict__ steps, uint32_t* __restrict__ cnt,
+                            uint32_t* __restrict__ tot) {
+    const StepDev sd = steps[blockIdx.y];
+    int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= sd.nb) return;
+    uint32_t run = 0;
+    uint32_t* col = cnt + sd.cnt_off + b;
+    for (int t = 0; t < sd.ntiles; t++) {
+        uint32_t c = col[(int64_t)t * sd.nb];
+        col[(int64_t)t * sd.nb] = run;
+        run += c;
+    }
+    tot[sd.bk_off + b] = run;
+}
+
+// Bucket-major exclusive scan (bounds), child segments, boundary records.
+__global__ void __launch_bounds__(1024) k_scan_buckets(
+    const StepDev* __restrict__ steps, const uint32_t* __restrict__ tot,
+    uint32_t* __restrict__ bstart, const uint8_t* __restrict__ tpos_g, int dst_in_b,
+    int64_t small_max, SegDev* __restrict__ large_out, SegDev* __restrict__ small_out,
+    int64_t* __restrict__ blist, int64_t* __restrict__ lcps, Counters* __restrict__ ctr) {
+    __shared__ uint32_t wsum[32];
+    const StepDev sd = steps[blockIdx.x];
+    const int nb = sd.nb;
+    constexpr int NT = 1024;
+    const int per = (nb + NT - 1) / NT;
+    const int beg = threadIdx.x * per, end = min(beg + per, nb);
+    uint32_t s = 0;
+    for (int b = beg; b < end; b++) s += tot[sd.bk_off + b];
+    uint32_t run = block_excl_sum<NT>(s, wsum, nullptr);
+    for (int b = beg; b < end; b++) {
+        uint32_t size = tot[sd.bk_off + b];
+        bstart[sd.bk_off + b] = run;
+        if (size) {
+            if (lcps && run > 0) {  // boundary to the previous non-empty bucket
+                int64_t pos = sd.lo + run;
+                lcps[pos] = sd.depth;  // resolved by k_boundary
+                blist[atomicAdd(&ctr->n_bound, 1ull)] = pos;
+            }
+            bool odd = b & 1;
+            int tp = odd ? tpos_g[sd.tree_off + (b >> 1)] : WORD;
+            bool final_bucket = size == 1 || (odd && tp < WORD);
+            if (!final_bucket) {
+                SegDev c;
+                c.lo = sd.lo + run;
+                c.depth = sd.depth + (odd ? WORD : 0);
+                c.n = (int32_t)size;
+                c.flags = (odd ? 0 : SEG_KEYS_VALID) | (dst_in_b ? SEG_IN_B : 0);
+                if ((int64_t)size <= small_max)
+                    small_out[atomicAdd(&ctr->n_small, 1ull)] = c;
+                else
+                    large_out[atomicAdd(&ctr->n_large, 1ull)] = c;
+            }
+        }
+        run += size;
+    }
+}
+
+// Stable scatter of (handle, key) into bucket order.  Singleton and
+// terminator-covering equality buckets are final: their handles go straight
+// to the output and the equality bucket's interior LCPs are written
+// (ssss.py:345-357).
+__global__ void __launch_bounds__(SC_NT) k_scatter(
+    const StepDev* __restrict__ steps, const int32_t* __restrict__ tile_step,
+    const int64_t* __restrict__ hX, const uint64_t* __restrict__ kX,
+    const uint16_t* __restrict__ bid, const uint32_t* __restrict__ cnt,
+    const uint32_t* __restrict__ tot, const uint32_t* __restrict__ bstart,
+    const uint8_t* __restrict__ tpos_g, int64_t* __restrict__ hY, uint64_t* __restrict__ kY,
+    int64_t* __restrict__ out_h, int64_t* __restrict__ lcps) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    __shared__ uint32_t wsum[32];
+    uint32_t* run_off = reinterpret_cast<uint32_t*>(smem);                 // NBMAX+1
+    uint32_t* rcnt = run_off + (NBMAX + 1);                                // SC_R*32
+    uint16_t* first_q = reinterpret_cast<uint16_t*>(rcnt + SC_R * 32);     // NBMAX+1
+    uint16_t* kA = first_q + (NBMAX + 1);
+    uint16_t* vA = kA + SC_SUB;
+    uint16_t* kB = vA + SC_SUB;
+    uint16_t* vB = kB + SC_SUB;
+    uint8_t* tp = reinterpret_cast<uint8_t*>(vB + SC_SUB);                 // VMAX
+    const int t = blockIdx.x;
+    const StepDev sd = steps[tile_step[t]];
+    const int ti = t - (int)sd.tile0;
+    const int64_t beg = sd.lo + (int64_t)ti * TILE;
+    const int64_t end = min(beg + TILE, sd.lo + sd.n);
+    const int nb = sd.nb;
+    const uint32_t* row = cnt + sd.cnt_off + (int64_t)ti * nb;
+    for (int b = threadIdx.x; b < nb; b += SC_NT) run_off[b] = bstart[sd.bk_off + b] + row[b];
+    for (int i = threadIdx.x; i < sd.v; i += SC_NT) tp[i] = tpos_g[sd.tree_off + i];
+    __syncthreads();
+    for (int64_t sub = beg; sub < end; sub += SC_SUB) {
+        const int m = (int)min((int64_t)SC_SUB, end - sub);
+        for (int e = threadIdx.x; e < SC_SUB; e += SC_NT) {
+            kA[e] = e < m ? bid[sub + e] : BID_SENTINEL;
+            vA[e] = (uint16_t)e;
+        }
+        __syncthreads();
+        rank_pass(kA, vA, kB, vB, 0, rcnt, wsum);
+        rank_pass(kB, vB, kA, vA, SC_RB, rcnt, wsum);
+        for (int q = threadIdx.x; q < m; q += SC_NT) {
+            uint16_t b = kA[q];
+            if (q == 0 || kA[q - 1] != b) first_q[b] = (uint16_t)q;
+        }
+        __syncthreads();
+        for (int q = threadIdx.x; q < m; q += SC_NT) {
+            const uint32_t b = kA[q];
+            const int64_t e = sub + vA[q];
+            const uint32_t rel = run_off[b] + (q - first_q[b]);
+            const int64_t pos = sd.lo + rel;
+            const int64_t h = hX[e];
+            const uint32_t size = tot[sd.bk_off + b];
+            const bool odd = b & 1;
+            const int tpv = odd ? tp[b >> 1] : WORD;
+            if (size == 1 || (odd && tpv < WORD)) {
+                out_h[pos] = h;
+                if (lcps && size > 1 && rel != bstart[sd.bk_off + b]) lcps[pos] = sd.depth + tpv;
+            } else {
+                hY[pos] = h;
+                kY[pos] = kX[e];
+            }
+        }
+        __syncthreads();
+        for (int q = threadIdx.x; q < m; q += SC_NT) {
+            uint16_t b = kA[q];
+            if (q == m - 1 || kA[q + 1] != b) run_off[b] += q - first_q[b] + 1;
+        }
+        __syncthreads();
+    }
+}
+
+// Finish one small segment per CTA: stable sort by the cached word, LCPs
+// from word-parallel XOR/clz at every key change, and re-keying of
+// non-terminated equal runs one word deeper until every run is a singleton
+// or terminator-equal (the multikey refinement of mkqs.py:221-251).
+__global__ void __launch_bounds__(SEG_NT) k_seg_sort(
+    const SegDev* __restrict__ segs, const int64_t* __restrict__ hA,
+    const uint64_t* __restrict__ kA, const int64_t* __restrict__ hB,
+    const uint64_t* __restrict__ kB, const uint8_t* __restrict__ arena, int64_t alen,
+    int64_t* __restrict__ out_h, int64_t* __restrict__ lcps, Counters* __restrict__ ctr) {
+    constexpr int M = SEG_M, NT = SEG_NT;
+    extern __shared__ __align__(16) uint8_t smem[];
+    uint64_t* key = reinterpret_cast<uint64_t*>(smem);
+    uint64_t* akey = key + M;
+    uint32_t* ameta = reinterpret_cast<uint32_t*>(akey + M);
+    uint32_t* xchg = ameta + M;
+    uint16_t* act0 = reinterpret_cast<uint16_t*>(xchg + NT);
+    uint16_t* act1 = act0 + M;
+    uint16_t* tag = act1 + M;
+    uint16_t* grp = tag + M;
+    uint8_t* brk = reinterpret_cast<uint8_t*>(grp + M);
+    __shared__ uint32_t wsum[32];
+    const SegDev sg = segs[blockIdx.x];
+    const int m = sg.n;
+    const int64_t lo = sg.lo;
+    const int64_t* sh = (sg.flags & SEG_IN_B) ? hB : hA;
+    const uint64_t* sk = (sg.flags & SEG_IN_B) ? kB : kA;
+    const bool valid = sg.flags & SEG_KEYS_VALID;
+    int64_t depth = sg.depth;
+    unsigned fetches = 0;
+    for (int i = threadIdx.x; i < m; i += NT) {
+        if (valid) {
+            key[i] = sk[lo + i];
+        } else {
+            key[i] = load_key(arena, alen, sh[lo + i], depth);
+            fetches++;
+        }
+        tag[i] = (uint16_t)i;
+        grp[i] = 0;
+        act0[i] = (uint16_t)i;
+    }
+    uint16_t* act = act0;
+    uint16_t* nact = act1;
+    int na = m;
+    __syncthreads();
+    for (;;) {
+        int P = 1;
+        while (P < na) P <<= 1;
+        for (int k = threadIdx.x; k < P; k += NT) {
+            if (k < na) {
+                int p = act[k];
+                akey[k] = key[p];
+                ameta[k] = ((uint32_t)grp[p] << 16) | tag[p];
+            } else {
+                akey[k] = ~0ull;
+                ameta[k] = 0xffffffffu;
+            }
+        }
+        __syncthreads();
+        bitonic_pairs<NT>(akey, ameta, P);
+        for (int k = threadIdx.x; k < na; k += NT) {
+            int p = act[k];
+            key[p] = akey[k];
+            tag[p] = (uint16_t)(ameta[k] & 0xffff);
+        }
+        __syncthreads();
+        for (int k = threadIdx.x; k < na; k += NT) {
+            int p = act[k];
+            if (p == grp[p]) {
+                brk[p] = 1;
+            } else {
+                uint64_t a = key[p - 1], b = key[p];
+                if (a != b) {
+                    brk[p] = 1;
+                    if (lcps) lcps[lo + p] = depth + (__clzll(a ^ b) >> 3);
+                } else {
+                    brk[p] = 0;
+                    int tpv = term_pos(b);
+                    if (lcps && tpv < WORD) lcps[lo + p] = depth + tpv;
+                }
+            }
+        }
+        __syncthreads();
+        // keep = member of a >= 2 run of equal, non-terminated keys; new
+        // group id = run start (max-scan of break positions)
+        const int per = (na + NT - 1) / NT;
+        const int kb = threadIdx.x * per, ke = min(kb + per, na);
+        uint32_t kc = 0, mx = 0;
+        for (int k = kb; k < ke; k++) {
+            int p = act[k];
+            bool same_prev = !brk[p];
+            bool same_next = k + 1 < na && !brk[act[k + 1]];
+            kc += (same_prev || same_next) && term_pos(key[p]) == WORD;
+            if (brk[p]) mx = max(mx, (uint32_t)p + 1);
+        }
+        uint32_t total;
+        uint32_t idx = block_excl_sum<NT>(kc, wsum, &total);
+        uint32_t incl = block_incl_max<NT>(mx, wsum);
+        xchg[threadIdx.x] = incl;
+        __syncthreads();
+        uint32_t run = threadIdx.x ? xchg[threadIdx.x - 1] : 0;
+        for (int k = kb; k < ke; k++) {
+            int p = act[k];
+            if (brk[p]) run = p + 1;
+            bool same_prev = !brk[p];
+            bool same_next = k + 1 < na && !brk[act[k + 1]];
+            if ((same_prev || same_next) && term_pos(key[p]) == WORD) {
+                nact[idx++] = (uint16_t)p;
+                grp[p] = (uint16_t)(run - 1);
+            }
+        }
+        __syncthreads();
+        na = (int)total;
+        if (na == 0 || depth > alen) break;  // depth > alen: corrupt input guard
+        uint16_t* tmp = act; act = nact; nact = tmp;
+        depth += WORD;
+        for (int k = threadIdx.x; k < na; k += NT) {
+            int p = act[k];
+            key[p] = load_key(arena, alen, sh[lo + tag[p]], depth);
+            fetches++;
+        }
+        __syncthreads();
+    }
+    for (int i = threadIdx.x; i < m; i += NT) out_h[lo + i] = sh[lo + tag[i]];
+    if (fetches) atomicAdd(&ctr->seg_fetches, (unsigned long long)fetches);
+    if (threadIdx.x == 0) atomicAdd(&ctr->small_elems, (unsigned long long)m);
+}
+
+// LCP at a bucket boundary of a device-wide step at depth d: both strings
+// share d characters and their d-words differ (ssss.py:242-263).
+__global__ void k_boundary(const int64_t* __restrict__ blist, int64_t nbound,
+                           const int64_t* __restrict__ out_h, int64_t* __restrict__ lcps,
+                           const uint8_t* __restrict__ arena, int64_t alen) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= nbound) return;
+    int64_t p = blist[i];
+    int64_t d = lcps[p];
+    uint64_t a = load_key(arena, alen, out_h[p - 1], d);
+    uint64_t b = load_key(arena, alen, out_h[p], d);
+    lcps[p] = d + shared_chars(a, b);
+}
+
+__global__ void k_dchar(const uint8_t* __restrict__ arena, const int64_t* __restrict__ h,
+                        const int64_t* __restrict__ lcps, int64_t n, uint8_t* __restrict__ out) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) {
+        int64_t l = lcps[i];
+        out[i] = arena[h[i] + (l < 0 ? 0 : l)];
+    }
+}
+
+__global__ void k_single(const int64_t* __restrict__ handles, int64_t* __restrict__ out_h) {
+    out_h[0] = handles[0];
+}
+
+// ---------------------------------------------------------------------------
+// host side
+
+static thread_local std::string g_err;
+
+// ---- live per-kernel timing (CUDA events on the launching stream) --------
+enum KernelId { K_INIT, K_SAMPLE, K_CLASSIFY, K_SCAN_COLS, K_SCAN_BUCKETS, K_SCATTER, K_SEG_SORT,
+                K_BOUNDARY, K_DCHAR, K_COUNT };
+static const char* kKernelNames[K_COUNT] = {"k_init", "k_sample_tree", "k_classify",
+                                            "k_scan_cols", "k_scan_buckets", "k_scatter",
+                                            "k_seg_sort", "k_boundary", "k_dchar"};
+struct ProfEntry {
+    long long launches = 0, units = 0, bytes = 0;
+    double ms = 0;
+};
+static bool g_prof = false;
+static ProfEntry g_prof_tab[K_COUNT];
+static unsigned long long g_launches = 0;
+
+struct Profiler {
+    cudaStream_t st;
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev;
+    std::vector<long long> units, bytes;
+    explicit Profiler(cudaStream_t s) : st(s) {}
+    int begin() {
+        g_launches++;
+        if (!g_prof) return -1;
+        cudaEvent_t a, b;
+        cudaEventCreate(&a);
+        cudaEventCreate(&b);
+        cudaEventRecord(a, st);
+        ev.push_back({-1, {a, b}});
+        units.push_back(0);
+        bytes.push_back(0);
+        return (int)ev.size() - 1;
+    }
+    void end(int slot, int kid, long long u, long long by) {
+        if (slot < 0) return;
+        ev[slot].first = kid;
+        units[slot] = u;
+        bytes[slot] = by;
+        cudaEventRecord(ev[slot].second.second, st);
+    }
+    void set_bytes(int kid, long long by) {
+        for (size_t i = 0; i < ev.size(); i++)
+            if (ev[i].first == kid) bytes[i] = by;
+    }
+    // call after the stream is synchronized
+    void flush() {
+        for (size_t i = 0; i < ev.size(); i++) {
+            float ms = 0;
+            cudaEventElapsedTime(&ms, ev[i].second.first, ev[i].second.second);
+            if (ev[i].first >= 0) {
+                g_prof_tab[ev[i].first].launches++;
+                g_prof_tab[ev[i].first].ms += ms;
+                g_prof_tab[ev[i].first].units += units[i];
+                g_prof_tab[ev[i].first].bytes += bytes[i];
+            }
+            cudaEventDestroy(ev[i].second.first);
+            cudaEventDestroy(ev[i].second.second);
+        }
+        ev.clear();
+        units.clear();
+        bytes.clear();
+    }
+    ~Profiler() { flush(); }
+};
+// Algorithmic bytes per launch: what the kernel must read and write at
+// minimum, not what it happens to move.
+#define PROF(kid, units_, bytes_, launch)          \
+    do {                                           \
+        int slot_ = prof.begin();                  \
+        launch;                                    \
+        prof.end(slot_, kid, (units_), (bytes_));  \
+    } while (0)
+
+static int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define CK(call)                                                                        \
+    do {                                                                                \
+        cudaError_t e_ = (call);                                                        \
+        if (e_ != cudaSuccess)                                                          \
+            return fail(S5G_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+static int levels_of(int64_t v) {
+    int l = 0;
+    while ((1LL << l) < v + 1) l++;
+    return l;
+}
+
+// tree_capacity (ssss.py:67-73)
+static int64_t tree_capacity(int64_t n, int64_t v) {
+    int64_t limit = std::min<int64_t>(v, std::max<int64_t>(1, n / 2));
+    int d = 0;
+    while ((1LL << (d + 1)) - 1 <= limit) d++;
+    return std::max<int64_t>(1, (1LL << d) - 1);
+}
+
+static int64_t small_max_of(int64_t t_medium) {
+    // segments of size <= small_max finish in one CTA; the reference
+    // switches to its leaves below t_medium (ssss.py:326)
+    return std::min<int64_t>(SEG_M, std::max<int64_t>(1, t_medium - 1));
+}
+
+struct Workspace {
+    int64_t *hA, *hB;
+    uint64_t *kA, *kB;
+    uint16_t* bid;
+    uint32_t* cnt;
+    uint32_t *tot, *bstart;
+    uint64_t *tree, *inorder;
+    uint8_t* tpos;
+    uint16_t* eqb;
+    StepDev* steps;
+    int32_t* tile_step;
+    SegDev* large[2];
+    SegDev* small;
+    int64_t* blist;
+    Counters* ctr;
+    int64_t steps_cap, tiles_cap, cnt_cap, bk_cap, tree_cap, small_cap;
+};
+
+static size_t carve(Workspace* w, uint8_t* base, int64_t n, int64_t t_medium) {
+    size_t off = 0;
+    auto take = [&](size_t bytes) -> uint8_t* {
+        off = (off + 255) & ~size_t(255);
+        uint8_t* p = base ? base + off : nullptr;
+        off += bytes;
+        return p;
+    };
+    const int64_t nn = std::max<int64_t>(n, 1);
+    const int64_t large_min = small_max_of(t_medium) + 1;
+    w->steps_cap = nn / large_min + 2;
+    w->tiles_cap = nn / TILE + w->steps_cap + 1;
+    w->cnt_cap = nn * ((int64_t)NBMAX / TILE + 2) + w->steps_cap * 2;
+    w->bk_cap = nn + 2 * w->steps_cap;
+    w->tree_cap = nn / 2 + 4 * w->steps_cap + 2;
+    w->small_cap = nn / 2 + 2;
+    w->hA = (int64_t*)take(8 * nn);
+    w->hB = (int64_t*)take(8 * nn);
+    w->kA = (uint64_t*)take(8 * nn);
+    w->kB = (uint64_t*)take(8 * nn);
+    w->bid = (uint16_t*)take(2 * nn);
+    w->cnt = (uint32_t*)take(4 * w->cnt_cap);
+    w->tot = (uint32_t*)take(4 * w->bk_cap);
+    w->bstart = (uint32_t*)take(4 * w->bk_cap);
+    w->tree = (uint64_t*)take(8 * w->tree_cap);
+    w->inorder = (uint64_t*)take(8 * w->tree_cap);
+    w->tpos = (uint8_t*)take(w->tree_cap);
+    w->eqb = (uint16_t*)take(2 * w->tree_cap);
+    w->steps = (StepDev*)take(sizeof(StepDev) * w->steps_cap);
+    w->tile_step = (int32_t*)take(4 * w->tiles_cap);
+    w->large[0] = (SegDev*)take(sizeof(SegDev) * w->steps_cap);
+    w->large[1] = (SegDev*)take(sizeof(SegDev) * w->steps_cap);
+    w->small = (SegDev*)take(sizeof(SegDev) * w->small_cap);
+    w->blist = (int64_t*)take(8 * nn);
+    w->ctr = (Counters*)take(sizeof(Counters));
+    return off + 256;
+}
+
+static constexpr size_t SMEM_SEG = (size_t)SEG_M * (8 + 8 + 4 + 2 * 4 + 1) + (size_t)SEG_NT * 4;
+static size_t smem_sample(int v) { return (size_t)2 * (v + 1) * 8 + (size_t)3 * (v + 1) * 2 + 16; }
+static constexpr size_t SMEM_CLS =
+    (size_t)(VMAX + 1) * 8 + (size_t)(NBMAX + 1) * 4 + (size_t)(VMAX + 1) * 2;
+static constexpr size_t SMEM_SC = (size_t)(NBMAX + 1) * 4 + (size_t)SC_R * 32 * 4 +
+                                  (size_t)(NBMAX + 1) * 2 + (size_t)4 * SC_SUB * 2 + VMAX + 1;
+
+static int set_smem_attrs() {
+    static bool done = false;
+    if (done) return 0;
+    CK(cudaFuncSetAttribute(k_sample_tree, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)smem_sample(VMAX)));
+    CK(cudaFuncSetAttribute(k_select_only, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)smem_sample(VMAX)));
+    CK(cudaFuncSetAttribute(k_classify<S5G_VARIANT_UNROLL>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_CLS));
+    CK(cudaFuncSetAttribute(k_classify<S5G_VARIANT_EQUAL>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_CLS));
+    CK(cudaFuncSetAttribute(k_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_SC));
+    CK(cudaFuncSetAttribute(k_seg_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_SEG));
+    done = true;
+    return 0;
+}
+
+static inline unsigned blocks_for(int64_t n, int nt) { return (unsigned)((n + nt - 1) / nt); }
+
+static int sort_impl(const s5g_sort_args* a) {
+    const int64_t n = a->n;
+    cudaStream_t st = (cudaStream_t)a->stream;
+    if (n < 0 || a->arena_len < 0) return fail(S5G_E_INVALID, "negative size");
+    if (a->variant != S5G_VARIANT_UNROLL && a->variant != S5G_VARIANT_EQUAL)
+        return fail(S5G_E_VARIANT, "unknown classify variant");
+    if (n > INT32_MAX) return fail(S5G_E_INVALID, "n exceeds 2^31-1");
+    if (n == 0) return 0;
+    if (!a->arena || !a->handles || !a->out_handles)
+        return fail(S5G_E_INVALID, "null buffer");
+    if (a->out_dchar && !a->out_lcps) return fail(S5G_E_INVALID, "dchar needs lcps");
+    if (int rc = set_smem_attrs()) return rc;
+    const int64_t t_medium = a->t_medium > 0 ? a->t_medium : (1 << 20);
+    const int64_t vcap = std::max<int64_t>(1, std::min<int64_t>(a->v > 0 ? a->v : VMAX, VMAX));
+    int64_t* lcps = a->out_lcps;
+    if (a->stats) a->stats->scratch_words += n;
+    if (n == 1) {
+        g_launches++;
+        k_single<<<1, 1, 0, st>>>(a->handles, a->out_handles);
+        if (lcps) CK(cudaMemsetAsync(lcps, 0xff, 8, st));
+        if (a->out_dchar) {
+            g_launches++;
+            k_dchar<<<1, 32, 0, st>>>(a->arena, a->out_handles, lcps, 1, a->out_dchar);
+        }
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(st));
+        return 0;
+    }
+    Profiler prof(st);
+    Workspace w;
+    size_t need = carve(&w, nullptr, n, t_medium);
+    if (!a->workspace || a->workspace_bytes < need)
+        return fail(S5G_E_WORKSPACE, "workspace too small: need " + std::to_string(need));
+    carve(&w, (uint8_t*)a->workspace, n, t_medium);
+    const int64_t small_max = small_max_of(t_medium);
+
+    CK(cudaMemsetAsync(w.ctr, 0, sizeof(Counters), st));
+    PROF(K_INIT, n, 32LL * n, (k_init<<<blocks_for(n, 256), 256, 0, st>>>(a->arena, a->arena_len,
+                                                                 a->handles, n, a->depth, w.hA,
+                                                                 w.kA)));
+    CK(cudaGetLastError());
+    Counters hc{};
+    hc.fetches = 0;
+    int64_t n_jobs = 0;
+    std::vector<SegDev> large;
+    SegDev root{0, a->depth, (int32_t)n, SEG_KEYS_VALID};
+    if (n <= small_max) {
+        CK(cudaMemcpyAsync(w.small, &root, sizeof(SegDev), cudaMemcpyHostToDevice, st));
+        hc.n_small = 1;
+        CK(cudaMemcpyAsync(&w.ctr->n_small, &hc.n_small, 8, cudaMemcpyHostToDevice, st));
+    } else {
+        large.push_back(root);
+    }
+    int in_b = 0;  // data of this round's segments lives in buffer B
+    int round = 0;
+    std::vector<StepDev> steps;
+    std::vector<int32_t> tile_step;
+    std::vector<uint32_t> h_tot, h_bstart;
+    std::vector<uint64_t> h_inorder;
+    std::vector<int64_t> h_bounds;
+    while (!large.empty()) {
+        // ---- plan the round's steps (host) -------------------------------
+        steps.clear();
+        tile_step.clear();
+        int64_t cnt_off = 0, bk_off = 0, tree_off = 0, tile0 = 0;
+        size_t i0 = 0;
+        // a round may be split into batches when it exceeds the capacities
+        while (i0 < large.size()) {
+            steps.clear();
+            tile_step.clear();
+            cnt_off = bk_off = tree_off = tile0 = 0;
+            size_t i = i0;
+            for (; i < large.size(); i++) {
+                const SegDev& s = large[i];
+                StepDev d{};
+                d.lo = s.lo;
+                d.n = s.n;
+                d.depth = s.depth;
+                d.v = (int32_t)tree_capacity(s.n, vcap);
+                d.levels = levels_of(d.v);
+                d.nb = 2 * d.v + 1;
+                d.keys_valid = (s.flags & SEG_KEYS_VALID) ? 1 : 0;
+                d.ntiles = (int32_t)((s.n + TILE - 1) / TILE);
+                int64_t need_cnt = (int64_t)d.ntiles * d.nb;
+                if ((int64_t)steps.size() + 1 > w.steps_cap || tile0 + d.ntiles > w.tiles_cap ||
+                    cnt_off + need_cnt > w.cnt_cap || bk_off + d.nb > w.bk_cap ||
+                    tree_off + d.v + 2 > w.tree_cap) {
+                    if (steps.empty()) return fail(S5G_E_WORKSPACE, "step exceeds capacity");
+                    break;
+                }
+                d.tile0 = tile0;
+                d.cnt_off = cnt_off;
+                d.bk_off = bk_off;
+                d.tree_off = tree_off;
+                for (int t = 0; t < d.ntiles; t++) tile_step.push_back((int32_t)steps.size());
+                tile0 += d.ntiles;
+                cnt_off += need_cnt;
+                bk_off += d.nb;
+                tree_off += (d.v + 1 + 1) & ~int64_t(1);
+                steps.push_back(d);
+            }
+            i0 = i;
+            const int nsteps = (int)steps.size();
+            n_jobs += nsteps;
+            CK(cudaMemcpyAsync(w.steps, steps.data(), sizeof(StepDev) * nsteps,
+                               cudaMemcpyHostToDevice, st));
+            CK(cudaMemcpyAsync(w.tile_step, tile_step.data(), 4 * tile_step.size(),
+                               cudaMemcpyHostToDevice, st));
+            const int64_t* hX = in_b ? w.hB : w.hA;
+            uint64_t* kX = in_b ? w.kB : w.kA;
+            int64_t* hY = in_b ? w.hA : w.hB;
+            uint64_t* kY = in_b ? w.kA : w.kB;
+            int maxv = 1;
+            long long sample_bytes = 0;
+            for (auto& d : steps) {
+                maxv = std::max(maxv, d.v);
+                sample_bytes += (long long)(2 * d.v + 1) * (d.keys_valid ? 8 : 16) + 27LL * d.v;
+            }
+            PROF(K_SAMPLE, nsteps, sample_bytes,
+                 (k_sample_tree<<<nsteps, SAMPLE_NT, smem_sample(maxv), st>>>(
+                     w.steps, a->arena, a->arena_len, hX, kX, a->seed, w.tree, w.inorder, w.tpos,
+                     w.eqb)));
+            CK(cudaGetLastError());
+            const unsigned ntiles = (unsigned)tile0;
+            int64_t round_elems = 0, cls_bytes = 0;
+            for (auto& d : steps) {
+                round_elems += d.n;
+                cls_bytes += (d.keys_valid ? 10LL : 26LL) * d.n;
+            }
+            if (a->variant == S5G_VARIANT_UNROLL)
+                PROF(K_CLASSIFY, round_elems, cls_bytes,
+                     (k_classify<S5G_VARIANT_UNROLL><<<ntiles, CLS_NT, SMEM_CLS, st>>>(
+                         w.steps, w.tile_step, a->arena, a->arena_len, hX, kX, w.bid, w.cnt,
+                         w.tree, w.eqb, w.ctr)));
+            else
+                PROF(K_CLASSIFY, round_elems, cls_bytes,
+                     (k_classify<S5G_VARIANT_EQUAL><<<ntiles, CLS_NT, SMEM_CLS, st>>>(
+                         w.steps, w.tile_step, a->arena, a->arena_len, hX, kX, w.bid, w.cnt,
+                         w.tree, w.eqb, w.ctr)));
+            CK(cudaGetLastError());
+            int maxnb = 2 * maxv + 1;
+            PROF(K_SCAN_COLS, cnt_off, 8LL * cnt_off + 4LL * bk_off,
+                 (k_scan_cols<<<dim3(blocks_for(maxnb, 256), nsteps), 256, 0, st>>>(w.steps, w.cnt,
+                                                                                   w.tot)));
+            CK(cudaGetLastError());
+            PROF(K_SCAN_BUCKETS, bk_off, 8LL * bk_off,
+                 (k_scan_buckets<<<nsteps, 1024, 0, st>>>(w.steps, w.tot, w.bstart, w.tpos, !in_b,
+                                                         small_max, w.large[(round + 1) & 1],
+                                                         w.small, w.blist, lcps, w.ctr)));
+            CK(cudaGetLastError());
+            PROF(K_SCATTER, round_elems, 34LL * round_elems,
+                 (k_scatter<<<ntiles, SC_NT, SMEM_SC, st>>>(w.steps, w.tile_step, hX, kX, w.bid,
+                                                           w.cnt, w.tot, w.bstart, w.tpos, hY, kY,
+                                                           a->out_handles, lcps)));
+            CK(cudaGetLastError());
+            if (a->step_cb) {
+                h_tot.resize(bk_off);
+                h_bstart.resize(bk_off);
+                h_inorder.resize(tree_off);
+                CK(cudaMemcpyAsync(h_tot.data(), w.tot, 4 * bk_off, cudaMemcpyDeviceToHost, st));
+                CK(cudaMemcpyAsync(h_bstart.data(), w.bstart, 4 * bk_off, cudaMemcpyDeviceToHost,
+                                   st));
+                CK(cudaMemcpyAsync(h_inorder.data(), w.inorder, 8 * tree_off,
+                                   cudaMemcpyDeviceToHost, st));
+                CK(cudaStreamSynchronize(st));
+                for (auto& d : steps) {
+                    h_bounds.resize(d.nb + 1);
+                    for (int b = 0; b < d.nb; b++) h_bounds[b] = h_bstart[d.bk_off + b];
+                    h_bounds[d.nb] = d.n;
+                    a->step_cb(a->step_ctx, d.lo, d.lo + d.n, d.depth, d.v, h_bounds.data(),
+                               h_inorder.data() + d.tree_off);
+                }
+            }
+        }
+        // ---- next round's large segments ---------------------------------
+        CK(cudaMemcpyAsync(&hc, w.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        large.resize(hc.n_large);
+        if (hc.n_large) {
+            CK(cudaMemcpyAsync(large.data(), w.large[(round + 1) & 1], sizeof(SegDev) * hc.n_large,
+                               cudaMemcpyDeviceToHost, st));
+            unsigned long long zero = 0;
+            CK(cudaMemcpyAsync(&w.ctr->n_large, &zero, 8, cudaMemcpyHostToDevice, st));
+            CK(cudaStreamSynchronize(st));
+        }
+        in_b ^= 1;
+        round++;
+        if (round > a->arena_len / WORD + 64) return fail(S5G_E_INVALID, "no progress: corrupt input");
+    }
+    if ((int64_t)hc.n_small > w.small_cap) return fail(S5G_E_WORKSPACE, "small list overflow");
+    if (hc.n_small)
+        PROF(K_SEG_SORT, (long long)hc.n_small, 0,
+             (k_seg_sort<<<(unsigned)hc.n_small, SEG_NT, SMEM_SEG, st>>>(
+                 w.small, w.hA, w.kA, w.hB, w.kB, a->arena, a->arena_len, a->out_handles, lcps,
+                 w.ctr)));
+    CK(cudaGetLastError());
+    if (lcps) {
+        if (hc.n_bound)
+            PROF(K_BOUNDARY, (long long)hc.n_bound, 56LL * (long long)hc.n_bound,
+                 (k_boundary<<<blocks_for(hc.n_bound, 256), 256, 0, st>>>(
+                     w.blist, (int64_t)hc.n_bound, a->out_handles, lcps, a->arena,
+                     a->arena_len)));
+        CK(cudaMemsetAsync(lcps, 0xff, 8, st));
+        if (a->out_dchar)
+            PROF(K_DCHAR, n, 17LL * n,
+                 (k_dchar<<<blocks_for(n, 256), 256, 0, st>>>(a->arena, a->out_handles, lcps, n,
+                                                              a->out_dchar)));
+        CK(cudaGetLastError());
+    }
+    CK(cudaMemcpyAsync(&hc, w.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    // k_seg_sort: (h, key) in, (handle, lcp) out per element; (handle, word)
+    // per re-keyed element
+    prof.set_bytes(K_SEG_SORT, 32LL * (long long)hc.small_elems + 16LL * (long long)hc.seg_fetches);
+    if (a->stats) {
+        a->stats->word_fetches += n + (int64_t)hc.fetches + (int64_t)hc.seg_fetches;
+        a->stats->jobs_enqueued += n_jobs + (int64_t)hc.n_small;
+        a->stats->jobs_executed += n_jobs + (int64_t)hc.n_small;
+    }
+    return 0;
+}
+
+}  // namespace s5g
+
+// ---------------------------------------------------------------------------
+// C ABI
+
+using namespace s5g;
+
+extern "C" {
+
+int s5g_version(void) { return S5G_VERSION; }
+
+void s5g_profile_enable(int on) { g_prof = on != 0; }
+
+void s5g_profile_reset(void) {
+    for (auto& e : g_prof_tab) e = ProfEntry();
+}
+
+int s5g_profile_read(s5g_kernel_profile* out, int max_entries) {
+    int k = 0;
+    for (int i = 0; i < K_COUNT && k < max_entries; i++, k++) {
+        std::snprintf(out[k].name, sizeof(out[k].name), "%s", kKernelNames[i]);
+        out[k].launches = g_prof_tab[i].launches;
+        out[k].units = g_prof_tab[i].units;
+        out[k].ms = g_prof_tab[i].ms;
+        out[k].bytes = g_prof_tab[i].bytes;
+    }
+    return k;
+}
+
+unsigned long long s5g_launch_count(void) { return g_launches; }
+
+const char* s5g_last_error(void) { return g_err.c_str(); }
+
+size_t s5g_workspace_bytes(int64_t n, int64_t t_medium) {
+    Workspace w;
+    return carve(&w, nullptr, n, t_medium > 0 ? t_medium : (1 << 20));
+}
+
+int s5g_sort(const s5g_sort_args* args) {
+    if (!args) return fail(S5G_E_INVALID, "null args");
+    return sort_impl(args);
+}
+
+int s5g_sort_host(const uint8_t* arena, int64_t arena_len, const int64_t* handles, int64_t n,
+                  int64_t depth, int64_t* out_handles, int64_t* out_lcps, uint8_t* out_dchar,
+                  int32_t variant, int32_t v, uint64_t seed, int64_t t_medium, s5g_stats* stats) {
+    if (n < 0 || arena_len < 0) return fail(S5G_E_INVALID, "negative size");
+    if (variant != S5G_VARIANT_UNROLL && variant != S5G_VARIANT_EQUAL)
+        return fail(S5G_E_VARIANT, "unknown classify variant");
+    if (n == 0) return 0;
+    static bool pool_set = false;
+    if (!pool_set) {
+        int dev = 0;
+        cudaMemPool_t pool;
+        if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        pool_set = true;
+    }
+    cudaStream_t st;
+    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    const int64_t tm = t_medium > 0 ? t_medium : (1 << 20);
+    size_t ws = s5g_workspace_bytes(n, tm);
+    size_t alen_pad = ((size_t)arena_len + S5G_ARENA_PAD + 15) & ~size_t(15);
+    uint8_t *d_arena = nullptr, *d_ws = nullptr, *d_dchar = nullptr;
+    int64_t *d_h = nullptr, *d_out = nullptr, *d_lcp = nullptr;
+    int rc = 0;
+    auto cleanup = [&]() {
+        cudaFreeAsync(d_arena, st); cudaFreeAsync(d_ws, st); cudaFreeAsync(d_h, st);
+        cudaFreeAsync(d_out, st); cudaFreeAsync(d_lcp, st); cudaFreeAsync(d_dchar, st);
+        cudaStreamSynchronize(st);
+        cudaStreamDestroy(st);
+    };
+#define CKH(call)                                                                        \
+    do {                                                                                 \
+        cudaError_t e_ = (call);                                                         \
+        if (e_ != cudaSuccess) {                                                         \
+            rc = fail(S5G_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));   \
+            cleanup();                                                                   \
+            return rc;                                                                   \
+        }                                                                                \
+    } while (0)
+    CKH(cudaMallocAsync((void**)&d_arena, alen_pad, st));
+    CKH(cudaMallocAsync((void**)&d_ws, ws, st));
+    CKH(cudaMallocAsync((void**)&d_h, 8 * n, st));
+    CKH(cudaMallocAsync((void**)&d_out, 8 * n, st));
+    if (out_lcps || out_dchar) CKH(cudaMallocAsync((void**)&d_lcp, 8 * n, st));
+    if (out_dchar) CKH(cudaMallocAsync((void**)&d_dchar, n, st));
+    CKH(cudaMemsetAsync(d_arena + arena_len, 0, alen_pad - arena_len, st));
+    CKH(cudaMemcpyAsync(d_arena, arena, arena_len, cudaMemcpyHostToDevice, st));
+    CKH(cudaMemcpyAsync(d_h, handles, 8 * n, cudaMemcpyHostToDevice, st));
+    s5g_sort_args a{};
+    a.arena = d_arena; a.arena_len = arena_len; a.handles = d_h; a.n = n; a.depth = depth;
+    a.out_handles = d_out; a.out_lcps = d_lcp; a.out_dchar = d_dchar;
+    a.workspace = d_ws; a.workspace_bytes = ws; a.stream = st;
+    a.variant = variant; a.v = v; a.seed = seed; a.t_medium = tm; a.stats = stats;
+    rc = sort_impl(&a);
+    if (rc) { std::string keep = g_err; cleanup(); g_err = keep; return rc; }
+    CKH(cudaMemcpyAsync(out_handles, d_out, 8 * n, cudaMemcpyDeviceToHost, st));
+    if (out_lcps) CKH(cudaMemcpyAsync(out_lcps, d_lcp, 8 * n, cudaMemcpyDeviceToHost, st));
+    if (out_dchar) CKH(cudaMemcpyAsync(out_dchar, d_dchar, n, cudaMemcpyDeviceToHost, st));
+    CKH(cudaStreamSynchronize(st));
+    cleanup();
+#undef CKH
+    return 0;
+}
+
+int s5g_extract_keys(const uint8_t* arena, int64_t arena_len, const int64_t* handles, int64_t n,
+                     int64_t depth, uint64_t* out_keys, void* stream) {
+    if (n <= 0) return n < 0 ? fail(S5G_E_INVALID, "negative n") : 0;
+    cudaStream_t st = (cudaStream_t)stream;
+    g_launches++;
+    k_extract_keys<<<blocks_for(n, 256), 256, 0, st>>>(arena, arena_len, handles, n, depth,
+                                                       out_keys);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(st));
+    return 0;
+}
+
+int s5g_select_splitters(const uint64_t* sample, int64_t count, int64_t v, uint64_t* tree,
+                         uint64_t* inorder, uint8_t* term_pos, uint16_t* eq_bucket, void* stream) {
+    if (v < 1 || v > VMAX || ((v + 1) & v) != 0 || count < 1 || count > 2 * (VMAX + 1))
+        return fail(S5G_E_INVALID, "v must be 2^d-1 <= 8191 and 1 <= count <= 16384");
+    if (int rc = set_smem_attrs()) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    size_t smem = (size_t)count * 8 + (size_t)3 * (v + 1) * 2 + 16;
+    g_launches++;
+    k_select_only<<<1, SAMPLE_NT, smem, st>>>(sample, (int)count, (int)v, levels_of(v), tree,
+                                              inorder, term_pos, eq_bucket);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(st));
+    return 0;
+}
+
+int s5g_classify(const uint64_t* keys, int64_t n, const uint64_t* tree, const uint16_t* eq_bucket,
+                 int64_t v, int32_t variant, uint16_t* out_bucket, void* stream) {
+    if (variant != S5G_VARIANT_UNROLL && variant != S5G_VARIANT_EQUAL)
+        return fail(S5G_E_VARIANT, "unknown classify variant");
+    if (v < 1 || v > VMAX || ((v + 1) & v) != 0) return fail(S5G_E_INVALID, "bad v");
+    if (n <= 0) return n < 0 ? fail(S5G_E_INVALID, "negative n") : 0;
+    cudaStream_t st = (cudaStream_t)stream;
+    size_t smem = (size_t)(v + 1) * 10;
+    if (smem > 48 * 1024) {
+        CK(cudaFuncSetAttribute(k_classify_only<S5G_VARIANT_UNROLL>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CK(cudaFuncSetAttribute(k_classify_only<S5G_VARIANT_EQUAL>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    }
+    g_launches++;
+    if (variant == S5G_VARIANT_UNROLL)
+        k_classify_only<S5G_VARIANT_UNROLL><<<blocks_for(n, 256), 256, smem, st>>>(
+            keys, n, tree, eq_bucket, (int)v, levels_of(v), out_bucket);
+    else
+        k_classify_only<S5G_VARIANT_EQUAL><<<blocks_for(n, 256), 256, smem, st>>>(
+            keys, n, tree, eq_bucket, (int)v, levels_of(v), out_bucket);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(st));
+    return 0;
+}
+
+int s5g_fill_dchar(const uint8_t* arena, const int64_t* handles, const int64_t* lcps, int64_t n,
+                   uint8_t* out_dchar, void* stream) {
+    if (n <= 0) return n < 0 ? fail(S5G_E_INVALID, "negative n") : 0;
+    cudaStream_t st = (cudaStream_t)stream;
+    g_launches++;
+    k_dchar<<<blocks_for(n, 256), 256, 0, st>>>(arena, handles, lcps, n, out_dchar);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(st));
+    return 0;
+}
+
+}  // extern "C"

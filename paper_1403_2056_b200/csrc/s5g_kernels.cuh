@@ -1,0 +1,214 @@
+// s5g_kernels.cuh -- sm_100a kernels of the S^5 string sorter.
+//
+// Pipeline of one device-wide S^5 step over a batch of "large" segments
+// (the GPU form of s5_step, ssss.py:281-297, and of the fully parallel step
+// _ParallelS5Run._phased_step, parallel.py:359-398):
+//   k_sample_tree  draw_sample + select_splitters (ssss.py:76-146), 1 CTA/step
+//   k_classify     classify_keys + per-tile bincount (ssss.py:149-181, 292)
+//   k_scan_cols    tile-minor prefix per bucket      (parallel.py:379-385)
+//   k_scan_buckets bucket-major exclusive scan, children, boundary records
+//   k_scatter      stable scatter (argsort(kind=stable) + gather, ssss.py:295)
+// Small segments finish in one CTA each (k_seg_sort): the GPU stand-in for
+// the MKQS / insertion leaves (mkqs.py:196-253, basecase.py:67-116) --
+// repeated stable sorts on 8-byte keys with depth advancing by a word.
+#pragma once
+#include "s5g_device.cuh"
+
+namespace s5g {
+
+constexpr int TILE = 32768;     // elements per classify / scatter CTA
+constexpr int CLS_NT = 1024;
+constexpr int SC_NT = 1024;
+constexpr int SC_ITEMS = 4;
+constexpr int SC_SUB = SC_NT * SC_ITEMS;  // 4096-element stable sub-tiles
+constexpr int SC_RB = 7;                  // radix bits per ranking pass
+constexpr int SC_R = 1 << SC_RB;
+constexpr uint16_t BID_SENTINEL = 0x3FFF; // > any bucket id (max 16382)
+constexpr int SAMPLE_NT = 1024;
+constexpr int SEG_M = 2048;     // capacity of a CTA segment
+constexpr int SEG_NT = 256;
+
+enum : int32_t { SEG_KEYS_VALID = 1, SEG_IN_B = 2 };
+
+struct StepDev {
+    int64_t lo, n, depth;
+    int32_t v, levels, nb, keys_valid;
+    int64_t tile0;
+    int32_t ntiles, pad0;
+    int64_t cnt_off;   // first entry in the tile x bucket count matrix
+    int64_t bk_off;    // first entry in tot / bstart
+    int64_t tree_off;  // first entry in tree / inorder / tpos / eqb (even)
+};
+
+struct SegDev {
+    int64_t lo, depth;
+    int32_t n, flags;
+};
+
+struct Counters {
+    unsigned long long n_large, n_small, n_bound, fetches, seg_fetches, small_elems;
+};
+
+// ---------------------------------------------------------------------------
+// shared-memory sorts
+
+template <int NT>
+__device__ void bitonic_u64(uint64_t* s, int P) {
+    for (int k = 2; k <= P; k <<= 1)
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < P / 2; i += NT) {
+                int lo = 2 * i - (i & (j - 1)), hi = lo + j;
+                bool up = (lo & k) == 0;
+                uint64_t a = s[lo], b = s[hi];
+                if ((a > b) == up) { s[lo] = b; s[hi] = a; }
+            }
+            __syncthreads();
+        }
+}
+
+// Sort (meta.group, key, meta.tag) lexicographically; meta = group<<16 | tag.
+template <int NT>
+__device__ void bitonic_pairs(uint64_t* key, uint32_t* meta, int P) {
+    for (int k = 2; k <= P; k <<= 1)
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < P / 2; i += NT) {
+                int lo = 2 * i - (i & (j - 1)), hi = lo + j;
+                bool up = (lo & k) == 0;
+                uint64_t a = key[lo], b = key[hi];
+                uint32_t ma = meta[lo], mb = meta[hi];
+                bool gt = (ma >> 16) != (mb >> 16) ? (ma >> 16) > (mb >> 16)
+                          : a != b               ? a > b
+                                                 : (ma & 0xffff) > (mb & 0xffff);
+                if (gt == up) {
+                    key[lo] = b; key[hi] = a;
+                    meta[lo] = mb; meta[hi] = ma;
+                }
+            }
+            __syncthreads();
+        }
+}
+
+// One stable LSD counting pass over SC_SUB (key, val) uint16 pairs by the
+// SC_RB-bit digit at `shift`.  Warp w owns elements [w*128, w*128+128),
+// item j / lane l is element w*128 + j*32 + l, so (digit, warp, item, lane)
+// order is input order: stability comes from warp-minor digit offsets plus
+// match_any ranks inside each warp.
+__device__ void rank_pass(const uint16_t* kin, const uint16_t* vin, uint16_t* kout,
+                          uint16_t* vout, int shift, uint32_t* cnt, uint32_t* wsum) {
+    constexpr int NW = SC_NT / 32;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int i = threadIdx.x; i < SC_R * NW; i += SC_NT) cnt[i] = 0;
+    __syncthreads();
+    uint16_t kk[SC_ITEMS], vv[SC_ITEMS];
+    uint32_t loc[SC_ITEMS], dg[SC_ITEMS];
+    const uint32_t lt = lanemask_lt();
+#pragma unroll
+    for (int j = 0; j < SC_ITEMS; j++) {
+        int e = w * (32 * SC_ITEMS) + j * 32 + lane;
+        kk[j] = kin[e];
+        vv[j] = vin[e];
+        uint32_t d = (kk[j] >> shift) & (SC_R - 1);
+        uint32_t peers = __match_any_sync(0xffffffffu, d);
+        uint32_t base = cnt[d * NW + w];
+        __syncwarp();
+        if (lane == __ffs(peers) - 1) cnt[d * NW + w] = base + __popc(peers);
+        __syncwarp();
+        loc[j] = base + __popc(peers & lt);
+        dg[j] = d;
+    }
+    __syncthreads();
+    // exclusive scan over (digit-major, warp-minor): SC_R*NW = 4096 entries
+    {
+        constexpr int PER = SC_R * NW / SC_NT;
+        uint32_t v[PER], s = 0;
+#pragma unroll
+        for (int i = 0; i < PER; i++) { v[i] = cnt[threadIdx.x * PER + i]; s += v[i]; }
+        uint32_t run = block_excl_sum<SC_NT>(s, wsum, nullptr);
+#pragma unroll
+        for (int i = 0; i < PER; i++) { cnt[threadIdx.x * PER + i] = run; run += v[i]; }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < SC_ITEMS; j++) {
+        uint32_t pos = cnt[dg[j] * NW + w] + loc[j];
+        kout[pos] = kk[j];
+        vout[pos] = vv[j];
+    }
+    __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// splitter selection, ssss.py:85-146, level-synchronous.
+// The reference recursion fill(slot_lo, slot_hi, a, b) runs here one tree
+// level at a time: node state (a, b, parent-sample-index) lives in shared
+// memory; the "skip samples equal to the pick" loops become lower/upper
+// bound searches.  tree[node] equals inorder[mid_slot(node)], so both are
+// written from the node's own pick.
+
+__device__ __forceinline__ int lower_bound_u64(const uint64_t* s, int a, int b, uint64_t x) {
+    while (a < b) {
+        int m = (a + b) >> 1;
+        if (s[m] < x) a = m + 1; else b = m;
+    }
+    return a;
+}
+__device__ __forceinline__ int upper_bound_u64(const uint64_t* s, int a, int b, uint64_t x) {
+    while (a < b) {
+        int m = (a + b) >> 1;
+        if (s[m] <= x) a = m + 1; else b = m;
+    }
+    return a;
+}
+
+template <int NT>
+__device__ void select_tree(const uint64_t* s, int count, int v, int L, int16_t* sa, int16_t* sb,
+                            int16_t* sp, uint64_t* tree, uint64_t* inorder, uint8_t* tpos,
+                            uint16_t* eqb) {
+    if (threadIdx.x == 0) {
+        sa[1] = 0;
+        sb[1] = (int16_t)count;
+        sp[1] = (int16_t)(count / 2);
+    }
+    __syncthreads();
+    for (int l = 0; l < L; l++) {
+        const int first = 1 << l;
+        for (int p = threadIdx.x; p < first; p += NT) {
+            int node = first + p;
+            int a = sa[node], b = sb[node], par = sp[node];
+            uint64_t val;
+            int la, lb, ra, rb, cp;
+            if (a >= b) {  // exhausted by duplicate skipping: reuse the parent pick
+                val = s[par];
+                la = lb = ra = rb = 0;
+                cp = par;
+            } else {
+                int m = (a + b) >> 1;
+                val = s[m];
+                la = a;
+                lb = lower_bound_u64(s, a, m, val);
+                ra = upper_bound_u64(s, m + 1, b, val);
+                rb = b;
+                cp = m;
+            }
+            tree[node] = val;
+            int slot = p * (1 << (L - l)) + (1 << (L - l - 1)) - 1;
+            inorder[slot] = val;
+            if (l + 1 < L) {
+                sa[2 * node] = (int16_t)la; sb[2 * node] = (int16_t)lb; sp[2 * node] = (int16_t)cp;
+                sa[2 * node + 1] = (int16_t)ra; sb[2 * node + 1] = (int16_t)rb;
+                sp[2 * node + 1] = (int16_t)cp;
+            }
+        }
+        __syncthreads();
+    }
+    // term_pos / eq_final per in-order slot, and the equality bucket each
+    // node maps to: 2*eq_leftmost[node_to_inorder[node]] + 1 (ssss.py:137-143)
+    for (int i = threadIdx.x; i < v; i += NT) tpos[i] = (uint8_t)term_pos(inorder[i]);
+    for (int node = 1 + threadIdx.x; node <= v; node += NT) {
+        int lo = lower_bound_u64(inorder, 0, v, tree[node]);
+        eqb[node] = (uint16_t)(2 * lo + 1);
+    }
+    if (threadIdx.x == 0) { tree[0] = 0; eqb[0] = 0; }
+}
+
+}  // namespace s5g

@@ -1,0 +1,162 @@
+"""Device-side entry: strings resident in HBM, sorted through libs5gpu.so.
+
+PyTorch provides the device buffers and the stream; every byte of sorting
+work happens in the library's sm_100a kernels (csrc/s5g.cu).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import warnings
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import S5G_ARENA_PAD, SortArgs, Stats, check, lib
+
+
+def _require_cuda() -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_1403_2056_b200 needs a CUDA device (B200, sm_100a); "
+                           "there is no CPU fallback")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+@dataclass
+class DeviceStrings:
+    """A string set resident on the device: padded arena + int64 handles."""
+
+    arena: torch.Tensor      # uint8, arena_len + pad bytes, pad zeroed
+    arena_len: int
+    handles: torch.Tensor    # int64[n]
+
+    @property
+    def n(self) -> int:
+        return int(self.handles.numel())
+
+
+def alloc_arena(arena_len: int, device) -> torch.Tensor:
+    cap = (arena_len + S5G_ARENA_PAD + 15) // 16 * 16
+    a = torch.empty(cap, dtype=torch.uint8, device=device)
+    a[arena_len:].zero_()
+    return a
+
+
+def upload(buffer, handles, device=None) -> DeviceStrings:
+    """Copy a host buffer (bytes / uint8 array) and handles into HBM."""
+    device = device or _require_cuda()
+    arr = buffer if isinstance(buffer, np.ndarray) else np.frombuffer(buffer, dtype=np.uint8)
+    alen = int(arr.size)
+    arena = alloc_arena(alen, device)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")  # read-only bytes buffers are only read
+        if alen:
+            arena[:alen].copy_(torch.from_numpy(arr), non_blocking=False)
+        h = torch.from_numpy(np.ascontiguousarray(handles, dtype=np.int64))
+    return DeviceStrings(arena, alen, h.to(device))
+
+
+def workspace_bytes(n: int, t_medium: int) -> int:
+    return int(lib().s5g_workspace_bytes(n, t_medium))
+
+
+def sort(ds: DeviceStrings, depth: int = 0, want_lcps: bool = True, want_dchar: bool = False,
+         variant: str = "unroll", v: int = 8191, seed: int = 1, t_medium: int = 1 << 20,
+         stats: Stats | None = None, step_cb=None, out=None, workspace=None):
+    """Sort device strings; returns (out_handles, lcps | None, dchar | None) tensors."""
+    if variant not in _lib.VARIANTS:
+        raise ValueError(f"unknown classify variant: {variant}")
+    n = ds.n
+    dev = ds.handles.device
+    out_h = out[0] if out is not None else torch.empty(n, dtype=torch.int64, device=dev)
+    lcps = None
+    if want_lcps or want_dchar:
+        lcps = out[1] if out is not None else torch.empty(n, dtype=torch.int64, device=dev)
+    dchar = torch.empty(n, dtype=torch.uint8, device=dev) if want_dchar else None
+    wsb = workspace_bytes(n, t_medium)
+    if workspace is None or workspace.numel() < wsb:
+        workspace = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
+    a = SortArgs()
+    a.arena = ds.arena.data_ptr()
+    a.arena_len = ds.arena_len
+    a.handles = ds.handles.data_ptr()
+    a.n = n
+    a.depth = depth
+    a.out_handles = out_h.data_ptr()
+    a.out_lcps = lcps.data_ptr() if lcps is not None else None
+    a.out_dchar = dchar.data_ptr() if dchar is not None else None
+    a.workspace = workspace.data_ptr()
+    a.workspace_bytes = workspace.numel()
+    a.stream = torch.cuda.current_stream(dev).cuda_stream
+    a.variant = _lib.VARIANTS[variant]
+    a.v = int(max(1, min(v, 8191)))
+    a.seed = int(seed) & ((1 << 64) - 1)
+    a.t_medium = int(t_medium)
+    st = stats if stats is not None else Stats()
+    a.stats = C.pointer(st)
+    a.step_cb = step_cb if step_cb is not None else _lib.STEP_CB()
+    a.step_ctx = None
+    check(lib().s5g_sort(C.byref(a)))
+    return out_h, lcps, dchar
+
+
+def extract_keys(ds: DeviceStrings, depth: int) -> torch.Tensor:
+    out = torch.empty(ds.n, dtype=torch.int64, device=ds.handles.device)
+    check(lib().s5g_extract_keys(ds.arena.data_ptr(), ds.arena_len, ds.handles.data_ptr(),
+                                 ds.n, depth, out.data_ptr(),
+                                 torch.cuda.current_stream().cuda_stream))
+    return out
+
+
+def select_splitters(sample: torch.Tensor, v: int):
+    """Device select_splitters: (tree[v+1], inorder[v], term_pos[v], eq_bucket[v+1])."""
+    dev = sample.device
+    tree = torch.empty(v + 1, dtype=torch.int64, device=dev)
+    inorder = torch.empty(v, dtype=torch.int64, device=dev)
+    tpos = torch.empty(v, dtype=torch.uint8, device=dev)
+    eqb = torch.empty(v + 1, dtype=torch.int16, device=dev)
+    check(lib().s5g_select_splitters(sample.data_ptr(), sample.numel(), v, tree.data_ptr(),
+                                     inorder.data_ptr(), tpos.data_ptr(), eqb.data_ptr(),
+                                     torch.cuda.current_stream().cuda_stream))
+    return tree, inorder, tpos, eqb
+
+
+def classify(keys: torch.Tensor, tree: torch.Tensor, eq_bucket: torch.Tensor, v: int,
+             variant: str = "unroll") -> torch.Tensor:
+    if variant not in _lib.VARIANTS:
+        raise ValueError(f"unknown classify variant: {variant}")
+    out = torch.empty(keys.numel(), dtype=torch.int16, device=keys.device)
+    check(lib().s5g_classify(keys.data_ptr(), keys.numel(), tree.data_ptr(),
+                             eq_bucket.data_ptr(), v, _lib.VARIANTS[variant], out.data_ptr(),
+                             torch.cuda.current_stream().cuda_stream))
+    return out
+
+
+def fill_dchar(ds: DeviceStrings, sorted_handles: torch.Tensor, lcps: torch.Tensor) -> torch.Tensor:
+    out = torch.empty(sorted_handles.numel(), dtype=torch.uint8, device=sorted_handles.device)
+    check(lib().s5g_fill_dchar(ds.arena.data_ptr(), sorted_handles.data_ptr(), lcps.data_ptr(),
+                               sorted_handles.numel(), out.data_ptr(),
+                               torch.cuda.current_stream().cuda_stream))
+    return out
+
+
+def sort_host(buffer, handles, depth: int = 0, want_lcps: bool = True, want_dchar: bool = False,
+              variant: str = "unroll", v: int = 8191, seed: int = 1, t_medium: int = 1 << 20,
+              stats: Stats | None = None, out_handles=None, out_lcps=None):
+    """End-to-end C-ABI call on host buffers (s5g_sort_host)."""
+    if variant not in _lib.VARIANTS:
+        raise ValueError(f"unknown classify variant: {variant}")
+    arr = buffer if isinstance(buffer, np.ndarray) else np.frombuffer(buffer, dtype=np.uint8)
+    h = handles if isinstance(handles, np.ndarray) else np.asarray(handles, dtype=np.int64)
+    n = len(h)
+    oh = out_handles if out_handles is not None else np.empty(n, dtype=np.int64)
+    ol = out_lcps if out_lcps is not None else (np.empty(n, dtype=np.int64) if want_lcps else None)
+    od = np.empty(n, dtype=np.uint8) if want_dchar else None
+    st = stats if stats is not None else Stats()
+    ptr = lambda x: x.ctypes.data if x is not None and x.size else None  # noqa: E731
+    check(lib().s5g_sort_host(ptr(arr), arr.size, ptr(h), n, depth, ptr(oh), ptr(ol), ptr(od),
+                              _lib.VARIANTS[variant], int(min(max(v, 1), 8191)), int(seed),
+                              int(t_medium), C.byref(st)))
+    return oh, ol, od

@@ -1,0 +1,167 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's
+golden vectors and the pinned CPU oracle.  Bit-exact handles, LCPs, dchar."""
+
+import numpy as np
+import pytest
+from hypothesis import given, settings
+from hypothesis import strategies as st
+
+import golden_io as G
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+import paper_1403_2056_b200 as P  # noqa: E402
+from paper_1403_2056_b200 import corpora  # noqa: E402
+from paper_1403_2056_b200 import device as D  # noqa: E402
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+
+
+KWS = [{}, {"t_medium": 16}, {"t_medium": 200, "variant": "equal"}, {"v": 7, "t_medium": 40},
+       {"seed": 5, "t_medium": 1000}]
+
+
+@pytest.mark.parametrize("kw", KWS, ids=lambda k: ",".join(f"{a}={b}" for a, b in k.items()) or "default")
+@pytest.mark.parametrize("name", G.cases())
+def test_golden_parity(name, kw):
+    c = G.case(name)
+    s = P.StringSet(c["buffer_bytes"], c["handles"])
+    res = P.s5_sort(s, depth=c["depth"], want_lcps=True, want_dchar=True, **kw)
+    assert np.array_equal(res.set.handles, c["out_handles"])
+    assert np.array_equal(res.lcps, c["lcps"])
+    assert np.array_equal(res.dchar, c["dchar"])
+
+
+def test_return_types_follow_reference():
+    c = G.case("random_3000")
+    s = P.StringSet(c["buffer_bytes"], c["handles"])
+    out = P.s5_sort(s)
+    assert isinstance(out, P.StringSet) and np.array_equal(out.handles, c["out_handles"])
+    out = P.s5_sort(s, want_dchar=True)  # reference: dchar without lcps -> StringSet
+    assert isinstance(out, P.StringSet)
+    stats = P.SortStats()
+    res = P.parallel_s5(s, p=1, want_dchar=True, stats=stats)
+    assert np.array_equal(res.lcps, c["lcps"]) and np.array_equal(res.dchar, c["dchar"])
+    assert stats.scratch_words == 3000 and stats.word_fetches >= 3000
+    assert np.array_equal(s.handles, c["handles"])  # input never mutated
+
+
+text = st.binary(min_size=0, max_size=24).map(lambda b: bytes(c if c else 1 for c in b))
+
+
+@given(st.lists(text, max_size=300), st.sampled_from([16, 64, 1 << 20]),
+       st.sampled_from(["unroll", "equal"]))
+@settings(max_examples=60, deadline=None)
+def test_property_vs_oracle(items, t_medium, variant):
+    s = P.from_strings(items)
+    res = P.s5_sort(s, want_lcps=True, t_medium=t_medium, variant=variant)
+    h, lcps, _ = oracle.s5_sort(s.buffer, s.handles)
+    assert np.array_equal(res.set.handles, h)
+    assert np.array_equal(res.lcps, lcps)
+
+
+def test_kernel_extract_keys():
+    for name in ("random_3000", "high_bytes_1500", "all_empty_300", "suffixes_1800"):
+        c = G.case(name)
+        ds = D.upload(c["buffer_bytes"], c["handles"])
+        for dep in (0, 2, 5, 9):
+            got = D.extract_keys(ds, dep).cpu().numpy().view(np.uint64)
+            assert np.array_equal(got, c[f"keys_d{dep}"]), (name, dep)
+
+
+@pytest.mark.parametrize("name", G.kats())
+def test_kernel_select_and_classify(name):
+    k = G.kat(name)
+    v = k["v"]
+    sample = torch.from_numpy(k["sample"].view(np.int64)).cuda()
+    tree, inorder, tpos, eqb = D.select_splitters(sample, v)
+    assert np.array_equal(tree.cpu().numpy().view(np.uint64)[1:], k["tree"][1:])
+    assert np.array_equal(inorder.cpu().numpy().view(np.uint64), k["inorder"])
+    assert np.array_equal(tpos.cpu().numpy(), k["term_pos"])
+    want_eqb = 2 * k["eq_leftmost"][k["node_to_inorder"][1:]] + 1
+    assert np.array_equal(eqb.cpu().numpy()[1:].astype(np.int64), want_eqb)
+    keys = torch.from_numpy(k["keys"].view(np.int64)).cuda()
+    for variant in ("unroll", "equal"):
+        got = D.classify(keys, tree, eqb, v, variant).cpu().numpy().astype(np.int64)
+        assert np.array_equal(got, k["oracle"]), variant
+
+
+def _clusters(n, seed=1, prefix_len=8, clusters=4):
+    rng = np.random.default_rng(seed)
+    pre = [bytes(rng.integers(97, 123, size=prefix_len, dtype=np.uint8)) for _ in range(clusters)]
+    return P.from_strings(
+        pre[int(rng.integers(0, clusters))]
+        + bytes(rng.integers(33, 127, size=int(rng.integers(1, 8)), dtype=np.uint8))
+        for _ in range(n))
+
+
+def test_step_hook_equality_buckets_advance_by_word():
+    # test_ssss.py:205-217 restated
+    s = _clusters(4000)
+    records = []
+    res = P.s5_sort(s, want_lcps=True, t_medium=512, step_hook=records.append)
+    h, lcps, _ = oracle.s5_sort(s.buffer, s.handles)
+    assert np.array_equal(res.set.handles, h) and np.array_equal(res.lcps, lcps)
+    assert records
+    root = records[0]
+    assert (root.child_depths[1::2] == root.depth + 8).all()
+    assert [r for r in records[1:] if r.depth == 8]
+
+
+def test_step_hook_bucket_lcp_property():
+    # Eq. 1 (test_ssss.py:231-256 restated): members of every bucket share
+    # at least the documented prefix credit
+    buf, hnd = corpora.gen_random(10_000, 13)
+    s = P.StringSet(buf.tobytes(), hnd)
+    records = []
+    res = P.s5_sort(s, t_medium=1024, step_hook=records.append)
+    rng = np.random.default_rng(0)
+    checked = 0
+    for rec in records:
+        for i in range(rec.tree.num_buckets):
+            lo, hi = rec.lo + int(rec.bounds[i]), rec.lo + int(rec.bounds[i + 1])
+            if hi - lo < 2:
+                continue
+            credit = int(rec.child_depths[i])
+            for a, b in rng.integers(lo, hi, size=(min(20, hi - lo), 2)):
+                assert oracle.lcp(s.buffer, res.handles[a], res.handles[b]) >= credit
+                checked += 1
+    assert checked > 100
+
+
+def test_hook_errors_propagate():
+    s = _clusters(3000)
+
+    def boom(rec):
+        raise KeyError("hook exploded")
+
+    with pytest.raises(KeyError, match="hook exploded"):
+        P.s5_sort(s, t_medium=64, step_hook=boom)
+
+
+def test_sort_host_abi_matches_device_path():
+    buf, hnd = corpora.gen_urls(20_000, hosts=200, pool=8)
+    oh, ol, od = D.sort_host(buf, hnd, want_lcps=True, want_dchar=True)
+    h, lcps, _ = oracle.parallel_s5(buf, hnd)
+    assert np.array_equal(oh, h) and np.array_equal(ol, lcps)
+    assert np.array_equal(od, oracle.fill_dchar(buf, h, lcps))
+
+
+SCALED = [("c1_random", 1.0), ("c2_dna", 1 / 16), ("c3_urls", 1 / 16), ("c4_suffixes", 1 / 64),
+          ("c5_nodup", 1 / 256)]
+
+
+@pytest.mark.parametrize("cfg,scale", SCALED)
+def test_config_parity_scaled(cfg, scale):
+    buf, hnd = corpora.CONFIGS[cfg](scale)
+    ds = D.upload(buf, hnd)
+    out_h, lcps, _ = D.sort(ds, want_lcps=True)
+    h, l, _ = oracle.parallel_s5(buf, hnd)
+    got_h = out_h.cpu().numpy()
+    assert np.array_equal(got_h, h)
+    assert np.array_equal(lcps.cpu().numpy(), l)

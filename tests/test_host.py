@@ -1,0 +1,78 @@
+"""Host-side logic of the drop-in (no GPU): argument errors, data model,
+splitter-tree metadata for step hooks, corpora."""
+
+import numpy as np
+import pytest
+
+import oracle
+import golden_io as G
+from paper_1403_2056_b200 import corpora
+from paper_1403_2056_b200.ssss import SplitterTree, check_set, s5_sort, tree_capacity
+from paper_1403_2056_b200.strset import (
+    StringSet, from_strings, load_delimited, shared_chars, word_terminator_pos)
+
+
+def test_unknown_variant_is_value_error():
+    s = from_strings([b"a", b"b"])
+    with pytest.raises(ValueError, match="unknown classify variant"):
+        s5_sort(s, variant="bogus")
+
+
+def test_not_zero_terminated():
+    with pytest.raises(ValueError, match="not zero-terminated"):
+        check_set(b"abc", np.array([0]))
+    with pytest.raises(ValueError, match="not zero-terminated"):
+        check_set(b"ab\0cd", np.array([0, 3]))
+    check_set(b"ab\0cd", np.array([0]))
+    check_set(b"", np.zeros(0, np.int64))
+
+
+def test_empty_set_needs_no_device():
+    res = s5_sort(from_strings([]), want_lcps=True, want_dchar=True)
+    assert len(res.set) == 0 and len(res.lcps) == 0 and len(res.dchar) == 0
+
+
+def test_load_delimited_and_from_strings():
+    s = load_delimited(b"ab\ncd", ord("\n"))
+    assert list(s.handles) == [0, 3] and s.strings() == [b"ab", b"cd"]
+    s = from_strings([b"x", b"", b"yz"])
+    assert s.buffer == b"x\0\0yz\0" and list(s.handles) == [0, 2, 3]
+
+
+@pytest.mark.parametrize("name", G.kats())
+def test_splitter_tree_metadata_matches_reference(name):
+    k = G.kat(name)
+    t = SplitterTree.from_inorder(k["v"], k["inorder"])
+    for fld in ("tree", "node_to_inorder", "slcp", "eq_leftmost", "term_pos"):
+        assert np.array_equal(getattr(t, fld), k[fld]), fld
+    assert np.array_equal(t.eq_final, k["eq_final"].astype(bool))
+
+
+def test_word_helpers_match_oracle():
+    rng = np.random.default_rng(0)
+    a = rng.integers(0, 4, size=(500, 8), dtype=np.uint8)
+    b = a.copy(); b[:, 5] ^= rng.integers(0, 2, size=500, dtype=np.uint8)
+    ka = a.view(">u8").reshape(-1).astype(np.uint64)
+    kb = b.view(">u8").reshape(-1).astype(np.uint64)
+    assert list(word_terminator_pos(ka)) == [oracle.term_pos(x) for x in ka]
+    assert list(shared_chars(ka, kb)) == [oracle.shared_chars(x, y) for x, y in zip(ka, kb)]
+
+
+def test_tree_capacity_matches_oracle():
+    for n in (0, 1, 2, 3, 5, 16, 100, 16381, 16382, 10**7):
+        for v in (1, 7, 8191, 10000):
+            assert tree_capacity(n, v) == oracle.tree_capacity(n, v)
+
+
+def test_corpora_shapes():
+    buf, h = corpora.gen_dna(1000)
+    assert len(h) == 1000 and buf[100] == 0 and set(np.unique(buf[:100])) <= set(b"ACGT")
+    buf, h = corpora.gen_suffix_markov(1 << 14, chains=16)
+    assert len(h) == 1 << 14 and buf[-1] == 0 and (buf[:-1] >= 97).all()
+    buf, h = corpora.gen_urls(2000, hosts=50, pool=8)
+    s = StringSet(buf.tobytes(), h)
+    assert all(x.startswith(b"http://") for x in s.strings()[:50])
+    buf, h = corpora.gen_nodup(5000, vocab=64)
+    s = StringSet(buf.tobytes(), h)
+    strs = s.strings()
+    assert len(set(strs)) == 5000 and all(32 <= len(x) <= 200 for x in strs)
