@@ -135,6 +135,10 @@ void s5g_profile_reset(void);
 int s5g_profile_read(s5g_kernel_profile *out, int max_entries);
 /* Monotonic count of kernels this library has launched (all entry points). */
 unsigned long long s5g_launch_count(void);
+/* Debug: per-CTA trace of the small-segment sorter (5 x uint64 per CTA:
+ * cycles, size, rounds, active elements over rounds, radix passes) into a
+ * device buffer; NULL disarms. */
+int s5g_debug_arm(void *dev_buf);
 
 const char *s5g_last_error(void);
 int s5g_version(void);

@@ -14,6 +14,7 @@
 
 #include "s5g.h"
 #include "s5g_kernels.cuh"
+#include "s5g_warpsort.cuh"
 
 namespace s5g {
 
@@ -53,7 +54,9 @@ __global__ void __launch_bounds__(SAMPLE_NT) k_sample_tree(
     uint16_t* __restrict__ eqb_g) {
     extern __shared__ __align__(16) uint8_t smem[];
     const StepDev sd = steps[blockIdx.x];
-    const int v = sd.v, count = OVERSAMPLE * v + OVERSAMPLE - 1, P = 2 * (v + 1);
+    const int v = sd.v, count = sd.count;
+    int P = 1;
+    while (P < count) P <<= 1;
     uint64_t* s = reinterpret_cast<uint64_t*>(smem);
     int16_t* sa = reinterpret_cast<int16_t*>(s + P);
     int16_t* sb = sa + (v + 1);
@@ -212,20 +215,44 @@ __global__ void k_classify_only(const uint64_t* __restrict__ keys, int64_t n,
     if (i < n) out[i] = (uint16_t)classify_one<VARIANT>(keys[i], tree, eqb, v, L);
 }
 
-// Tile-minor running prefix per bucket column; bucket totals.
-__global__ void k_scan_cols(const StepDev* __restrict__ steps, uint32_t* __restrict__ cnt,
-                            uint32_t* __restrict__ tot) {
-    const StepDev sd = steps[blockIdx.y];
-    int b = blockIdx.x * blockDim.x + threadIdx.x;
-    if (b >= sd.nb) return;
-    uint32_t run = 0;
+// Tile-minor running prefix per bucket column; bucket totals.  One CTA per
+// 32 bucket columns: lane = column (coalesced 128 B rows), warp = a chunk of
+// tiles; chunk sums are scanned in shared memory, then applied.
+__global__ void __launch_bounds__(1024) k_scan_cols(const StepDev* __restrict__ steps,
+                                                    const int32_t* __restrict__ cblk_step,
+                                                    uint32_t* __restrict__ cnt,
+                                                    uint32_t* __restrict__ tot) {
+    __shared__ uint32_t part[32][33];
+    const int si = cblk_step[blockIdx.x];
+    const StepDev sd = steps[si];
+    const int bl = threadIdx.x & 31, c = threadIdx.x >> 5;
+    const int b = (blockIdx.x - (int)sd.cblk0) * 32 + bl;
+    const int per = (sd.ntiles + 31) / 32;
+    const int t0 = c * per, t1 = min(sd.ntiles, t0 + per);
     uint32_t* col = cnt + sd.cnt_off + b;
-    for (int t = 0; t < sd.ntiles; t++) {
-        uint32_t c = col[(int64_t)t * sd.nb];
-        col[(int64_t)t * sd.nb] = run;
-        run += c;
+    uint32_t s = 0;
+    if (b < sd.nb)
+        for (int t = t0; t < t1; t++) s += col[(int64_t)t * sd.nb];
+    part[c][bl] = s;
+    __syncthreads();
+    if (c == 0) {
+        uint32_t run = 0;
+        for (int i = 0; i < 32; i++) {
+            uint32_t v = part[i][bl];
+            part[i][bl] = run;
+            run += v;
+        }
+        if (b < sd.nb) tot[sd.bk_off + b] = run;
     }
-    tot[sd.bk_off + b] = run;
+    __syncthreads();
+    if (b < sd.nb) {
+        uint32_t run = part[c][bl];
+        for (int t = t0; t < t1; t++) {
+            uint32_t v = col[(int64_t)t * sd.nb];
+            col[(int64_t)t * sd.nb] = run;
+            run += v;
+        }
+    }
 }
 
 // Bucket-major exclusive scan (bounds), child segments, boundary records.
@@ -233,6 +260,7 @@ __global__ void __launch_bounds__(1024) k_scan_buckets(
     const StepDev* __restrict__ steps, const uint32_t* __restrict__ tot,
     uint32_t* __restrict__ bstart, const uint8_t* __restrict__ tpos_g, int dst_in_b,
     int64_t small_max, SegDev* __restrict__ large_out, SegDev* __restrict__ small_out,
+    ClassLists cls,
     int64_t* __restrict__ blist, int64_t* __restrict__ lcps, Counters* __restrict__ ctr) {
     __shared__ uint32_t wsum[32];
     const StepDev sd = steps[blockIdx.x];
@@ -261,8 +289,10 @@ __global__ void __launch_bounds__(1024) k_scan_buckets(
                 c.depth = sd.depth + (odd ? WORD : 0);
                 c.n = (int32_t)size;
                 c.flags = (odd ? 0 : SEG_KEYS_VALID) | (dst_in_b ? SEG_IN_B : 0);
-                if ((int64_t)size <= small_max)
-                    small_out[atomicAdd(&ctr->n_small, 1ull)] = c;
+                if ((int64_t)size <= small_max) {
+                    const int ci = size_class(size);
+                    small_out[cls.off[ci] + atomicAdd(&ctr->n_cls[ci], 1ull)] = c;
+                }
                 else
                     large_out[atomicAdd(&ctr->n_large, 1ull)] = c;
             }
@@ -285,13 +315,11 @@ __global__ void __launch_bounds__(SC_NT) k_scatter(
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ uint32_t wsum[32];
     uint32_t* run_off = reinterpret_cast<uint32_t*>(smem);                 // NBMAX+1
-    uint32_t* rcnt = run_off + (NBMAX + 1);                                // SC_R*32
-    uint16_t* first_q = reinterpret_cast<uint16_t*>(rcnt + SC_R * 32);     // NBMAX+1
-    uint16_t* kA = first_q + (NBMAX + 1);
+    uint16_t* rcnt = reinterpret_cast<uint16_t*>(run_off + (NBMAX + 1));   // SC_R*32
+    uint16_t* kA = rcnt + SC_R * 32;
     uint16_t* vA = kA + SC_SUB;
     uint16_t* kB = vA + SC_SUB;
     uint16_t* vB = kB + SC_SUB;
-    uint8_t* tp = reinterpret_cast<uint8_t*>(vB + SC_SUB);                 // VMAX
     const int t = blockIdx.x;
     const StepDev sd = steps[tile_step[t]];
     const int ti = t - (int)sd.tile0;
@@ -299,8 +327,8 @@ __global__ void __launch_bounds__(SC_NT) k_scatter(
     const int64_t end = min(beg + TILE, sd.lo + sd.n);
     const int nb = sd.nb;
     const uint32_t* row = cnt + sd.cnt_off + (int64_t)ti * nb;
+    const uint8_t* tp = tpos_g + sd.tree_off;
     for (int b = threadIdx.x; b < nb; b += SC_NT) run_off[b] = bstart[sd.bk_off + b] + row[b];
-    for (int i = threadIdx.x; i < sd.v; i += SC_NT) tp[i] = tpos_g[sd.tree_off + i];
     __syncthreads();
     for (int64_t sub = beg; sub < end; sub += SC_SUB) {
         const int m = (int)min((int64_t)SC_SUB, end - sub);
@@ -311,15 +339,26 @@ __global__ void __launch_bounds__(SC_NT) k_scatter(
         __syncthreads();
         rank_pass(kA, vA, kB, vB, 0, rcnt, wsum);
         rank_pass(kB, vB, kA, vA, SC_RB, rcnt, wsum);
-        for (int q = threadIdx.x; q < m; q += SC_NT) {
-            uint16_t b = kA[q];
-            if (q == 0 || kA[q - 1] != b) first_q[b] = (uint16_t)q;
+        // run starts in the sorted sub-tile: thread owns q = 4t .. 4t+3
+        const int q0 = threadIdx.x * SC_ITEMS;
+        uint32_t bq[SC_ITEMS], st[SC_ITEMS], mx = 0;
+#pragma unroll
+        for (int i = 0; i < SC_ITEMS; i++) {
+            const int q = q0 + i;
+            bq[i] = kA[q];
+            const bool start = q < m && (q == 0 || kA[q - 1] != bq[i]);
+            if (start) mx = q + 1;
+            st[i] = mx;  // 0 = run started before this thread
         }
-        __syncthreads();
-        for (int q = threadIdx.x; q < m; q += SC_NT) {
-            const uint32_t b = kA[q];
+        const uint32_t before = block_excl_max<SC_NT>(mx, wsum);
+#pragma unroll
+        for (int i = 0; i < SC_ITEMS; i++) {
+            const int q = q0 + i;
+            if (q >= m) break;
+            st[i] = (st[i] ? st[i] : before) - 1;
+            const uint32_t b = bq[i];
             const int64_t e = sub + vA[q];
-            const uint32_t rel = run_off[b] + (q - first_q[b]);
+            const uint32_t rel = run_off[b] + (q - st[i]);
             const int64_t pos = sd.lo + rel;
             const int64_t h = hX[e];
             const uint32_t size = tot[sd.bk_off + b];
@@ -334,139 +373,13 @@ __global__ void __launch_bounds__(SC_NT) k_scatter(
             }
         }
         __syncthreads();
-        for (int q = threadIdx.x; q < m; q += SC_NT) {
-            uint16_t b = kA[q];
-            if (q == m - 1 || kA[q + 1] != b) run_off[b] += q - first_q[b] + 1;
+#pragma unroll
+        for (int i = 0; i < SC_ITEMS; i++) {
+            const int q = q0 + i;
+            if (q < m && (q == m - 1 || kA[q + 1] != bq[i])) run_off[bq[i]] += q - st[i] + 1;
         }
         __syncthreads();
     }
-}
-
-// Finish one small segment per CTA: stable sort by the cached word, LCPs
-// from word-parallel XOR/clz at every key change, and re-keying of
-// non-terminated equal runs one word deeper until every run is a singleton
-// or terminator-equal (the multikey refinement of mkqs.py:221-251).
-__global__ void __launch_bounds__(SEG_NT) k_seg_sort(
-    const SegDev* __restrict__ segs, const int64_t* __restrict__ hA,
-    const uint64_t* __restrict__ kA, const int64_t* __restrict__ hB,
-    const uint64_t* __restrict__ kB, const uint8_t* __restrict__ arena, int64_t alen,
-    int64_t* __restrict__ out_h, int64_t* __restrict__ lcps, Counters* __restrict__ ctr) {
-    constexpr int M = SEG_M, NT = SEG_NT;
-    extern __shared__ __align__(16) uint8_t smem[];
-    uint64_t* key = reinterpret_cast<uint64_t*>(smem);
-    uint64_t* akey = key + M;
-    uint32_t* ameta = reinterpret_cast<uint32_t*>(akey + M);
-    uint32_t* xchg = ameta + M;
-    uint16_t* act0 = reinterpret_cast<uint16_t*>(xchg + NT);
-    uint16_t* act1 = act0 + M;
-    uint16_t* tag = act1 + M;
-    uint16_t* grp = tag + M;
-    uint8_t* brk = reinterpret_cast<uint8_t*>(grp + M);
-    __shared__ uint32_t wsum[32];
-    const SegDev sg = segs[blockIdx.x];
-    const int m = sg.n;
-    const int64_t lo = sg.lo;
-    const int64_t* sh = (sg.flags & SEG_IN_B) ? hB : hA;
-    const uint64_t* sk = (sg.flags & SEG_IN_B) ? kB : kA;
-    const bool valid = sg.flags & SEG_KEYS_VALID;
-    int64_t depth = sg.depth;
-    unsigned fetches = 0;
-    for (int i = threadIdx.x; i < m; i += NT) {
-        if (valid) {
-            key[i] = sk[lo + i];
-        } else {
-            key[i] = load_key(arena, alen, sh[lo + i], depth);
-            fetches++;
-        }
-        tag[i] = (uint16_t)i;
-        grp[i] = 0;
-        act0[i] = (uint16_t)i;
-    }
-    uint16_t* act = act0;
-    uint16_t* nact = act1;
-    int na = m;
-    __syncthreads();
-    for (;;) {
-        int P = 1;
-        while (P < na) P <<= 1;
-        for (int k = threadIdx.x; k < P; k += NT) {
-            if (k < na) {
-                int p = act[k];
-                akey[k] = key[p];
-                ameta[k] = ((uint32_t)grp[p] << 16) | tag[p];
-            } else {
-                akey[k] = ~0ull;
-                ameta[k] = 0xffffffffu;
-            }
-        }
-        __syncthreads();
-        bitonic_pairs<NT>(akey, ameta, P);
-        for (int k = threadIdx.x; k < na; k += NT) {
-            int p = act[k];
-            key[p] = akey[k];
-            tag[p] = (uint16_t)(ameta[k] & 0xffff);
-        }
-        __syncthreads();
-        for (int k = threadIdx.x; k < na; k += NT) {
-            int p = act[k];
-            if (p == grp[p]) {
-                brk[p] = 1;
-            } else {
-                uint64_t a = key[p - 1], b = key[p];
-                if (a != b) {
-                    brk[p] = 1;
-                    if (lcps) lcps[lo + p] = depth + (__clzll(a ^ b) >> 3);
-                } else {
-                    brk[p] = 0;
-                    int tpv = term_pos(b);
-                    if (lcps && tpv < WORD) lcps[lo + p] = depth + tpv;
-                }
-            }
-        }
-        __syncthreads();
-        // keep = member of a >= 2 run of equal, non-terminated keys; new
-        // group id = run start (max-scan of break positions)
-        const int per = (na + NT - 1) / NT;
-        const int kb = threadIdx.x * per, ke = min(kb + per, na);
-        uint32_t kc = 0, mx = 0;
-        for (int k = kb; k < ke; k++) {
-            int p = act[k];
-            bool same_prev = !brk[p];
-            bool same_next = k + 1 < na && !brk[act[k + 1]];
-            kc += (same_prev || same_next) && term_pos(key[p]) == WORD;
-            if (brk[p]) mx = max(mx, (uint32_t)p + 1);
-        }
-        uint32_t total;
-        uint32_t idx = block_excl_sum<NT>(kc, wsum, &total);
-        uint32_t incl = block_incl_max<NT>(mx, wsum);
-        xchg[threadIdx.x] = incl;
-        __syncthreads();
-        uint32_t run = threadIdx.x ? xchg[threadIdx.x - 1] : 0;
-        for (int k = kb; k < ke; k++) {
-            int p = act[k];
-            if (brk[p]) run = p + 1;
-            bool same_prev = !brk[p];
-            bool same_next = k + 1 < na && !brk[act[k + 1]];
-            if ((same_prev || same_next) && term_pos(key[p]) == WORD) {
-                nact[idx++] = (uint16_t)p;
-                grp[p] = (uint16_t)(run - 1);
-            }
-        }
-        __syncthreads();
-        na = (int)total;
-        if (na == 0 || depth > alen) break;  // depth > alen: corrupt input guard
-        uint16_t* tmp = act; act = nact; nact = tmp;
-        depth += WORD;
-        for (int k = threadIdx.x; k < na; k += NT) {
-            int p = act[k];
-            key[p] = load_key(arena, alen, sh[lo + tag[p]], depth);
-            fetches++;
-        }
-        __syncthreads();
-    }
-    for (int i = threadIdx.x; i < m; i += NT) out_h[lo + i] = sh[lo + tag[i]];
-    if (fetches) atomicAdd(&ctr->seg_fetches, (unsigned long long)fetches);
-    if (threadIdx.x == 0) atomicAdd(&ctr->small_elems, (unsigned long long)m);
 }
 
 // LCP at a bucket boundary of a device-wide step at depth d: both strings
@@ -502,11 +415,15 @@ __global__ void k_single(const int64_t* __restrict__ handles, int64_t* __restric
 static thread_local std::string g_err;
 
 // ---- live per-kernel timing (CUDA events on the launching stream) --------
-enum KernelId { K_INIT, K_SAMPLE, K_CLASSIFY, K_SCAN_COLS, K_SCAN_BUCKETS, K_SCATTER, K_SEG_SORT,
+enum KernelId { K_INIT, K_SAMPLE, K_CLASSIFY, K_SCAN_COLS, K_SCAN_BUCKETS, K_SCATTER, K_SEG_WARP,
+                K_SEG_WARP2, K_SEG_WARP4, K_SEG_WARP8, K_SEG_CTA2, K_SEG_CTA4, K_SEG_CTA8,
                 K_BOUNDARY, K_DCHAR, K_COUNT };
 static const char* kKernelNames[K_COUNT] = {"k_init", "k_sample_tree", "k_classify",
                                             "k_scan_cols", "k_scan_buckets", "k_scatter",
-                                            "k_seg_sort", "k_boundary", "k_dchar"};
+                                            "k_warp_sort<1>", "k_warp_sort<2>",
+                                            "k_warp_sort<4>", "k_warp_sort<8>", "k_cta_sort<2>",
+                                            "k_cta_sort<4>", "k_cta_sort<8>", "k_boundary",
+                                            "k_dchar"};
 struct ProfEntry {
     long long launches = 0, units = 0, bytes = 0;
     double ms = 0;
@@ -598,10 +515,19 @@ static int64_t tree_capacity(int64_t n, int64_t v) {
     return std::max<int64_t>(1, (1LL << d) - 1);
 }
 
+// Splitters for a device-wide step: v+1 range buckets of about SEG_TARGET
+// strings each (the reference's tree_capacity, ssss.py:67-73, caps it; v
+// and the sample size never change the output, only the bucket sizes).
+static int64_t gpu_tree_capacity(int64_t n, int64_t vcap) {
+    int64_t want = 1;
+    while (want < VMAX && (want + 1) * SEG_TARGET < n) want = 2 * want + 1;
+    return std::min(want, tree_capacity(n, vcap));
+}
+
 static int64_t small_max_of(int64_t t_medium) {
     // segments of size <= small_max finish in one CTA; the reference
     // switches to its leaves below t_medium (ssss.py:326)
-    return std::min<int64_t>(SEG_M, std::max<int64_t>(1, t_medium - 1));
+    return std::min<int64_t>(SMALL_MAX, std::max<int64_t>(1, t_medium - 1));
 }
 
 struct Workspace {
@@ -616,10 +542,11 @@ struct Workspace {
     StepDev* steps;
     int32_t* tile_step;
     SegDev* large[2];
-    SegDev* small;
+    SegDev* small;   // NCLS lists; class c holds cls_cap[c] entries at cls_off[c]
     int64_t* blist;
     Counters* ctr;
-    int64_t steps_cap, tiles_cap, cnt_cap, bk_cap, tree_cap, small_cap;
+    int64_t steps_cap, tiles_cap, cnt_cap, bk_cap, tree_cap;
+    int64_t cls_cap[NCLS], cls_off[NCLS];
 };
 
 static size_t carve(Workspace* w, uint8_t* base, int64_t n, int64_t t_medium) {
@@ -633,11 +560,20 @@ static size_t carve(Workspace* w, uint8_t* base, int64_t n, int64_t t_medium) {
     const int64_t nn = std::max<int64_t>(n, 1);
     const int64_t large_min = small_max_of(t_medium) + 1;
     w->steps_cap = nn / large_min + 2;
-    w->tiles_cap = nn / TILE + w->steps_cap + 1;
+    w->tiles_cap = nn / TILE + w->steps_cap + 1 + (nn + 2 * w->steps_cap) / 32 + w->steps_cap;
     w->cnt_cap = nn * ((int64_t)NBMAX / TILE + 2) + w->steps_cap * 2;
     w->bk_cap = nn + 2 * w->steps_cap;
     w->tree_cap = nn / 2 + 4 * w->steps_cap + 2;
-    w->small_cap = nn / 2 + 2;
+    {
+        // a class-c segment has more than lower[c] strings
+        static const int64_t lower[NCLS] = {1, 32, 64, 128, 256, 512, 1024};
+        int64_t off = 0;
+        for (int c = 0; c < NCLS; c++) {
+            w->cls_cap[c] = nn / (lower[c] + 1) + 2;
+            w->cls_off[c] = off;
+            off += w->cls_cap[c];
+        }
+    }
     w->hA = (int64_t*)take(8 * nn);
     w->hB = (int64_t*)take(8 * nn);
     w->kA = (uint64_t*)take(8 * nn);
@@ -654,32 +590,32 @@ static size_t carve(Workspace* w, uint8_t* base, int64_t n, int64_t t_medium) {
     w->tile_step = (int32_t*)take(4 * w->tiles_cap);
     w->large[0] = (SegDev*)take(sizeof(SegDev) * w->steps_cap);
     w->large[1] = (SegDev*)take(sizeof(SegDev) * w->steps_cap);
-    w->small = (SegDev*)take(sizeof(SegDev) * w->small_cap);
+    w->small = (SegDev*)take(sizeof(SegDev) * (w->cls_off[NCLS - 1] + w->cls_cap[NCLS - 1]));
     w->blist = (int64_t*)take(8 * nn);
     w->ctr = (Counters*)take(sizeof(Counters));
     return off + 256;
 }
 
-static constexpr size_t SMEM_SEG = (size_t)SEG_M * (8 + 8 + 4 + 2 * 4 + 1) + (size_t)SEG_NT * 4;
-static size_t smem_sample(int v) { return (size_t)2 * (v + 1) * 8 + (size_t)3 * (v + 1) * 2 + 16; }
+
+static size_t smem_sample(int P, int v) { return (size_t)P * 8 + (size_t)3 * (v + 1) * 2 + 16; }
 static constexpr size_t SMEM_CLS =
     (size_t)(VMAX + 1) * 8 + (size_t)(NBMAX + 1) * 4 + (size_t)(VMAX + 1) * 2;
-static constexpr size_t SMEM_SC = (size_t)(NBMAX + 1) * 4 + (size_t)SC_R * 32 * 4 +
-                                  (size_t)(NBMAX + 1) * 2 + (size_t)4 * SC_SUB * 2 + VMAX + 1;
+static constexpr size_t SMEM_SC = (size_t)(NBMAX + 1) * 4 + (size_t)SC_R * 32 * 2 +
+                                  (size_t)4 * SC_SUB * 2;
 
 static int set_smem_attrs() {
     static bool done = false;
     if (done) return 0;
     CK(cudaFuncSetAttribute(k_sample_tree, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)smem_sample(VMAX)));
+                            (int)smem_sample(2 * (VMAX + 1), VMAX)));
     CK(cudaFuncSetAttribute(k_select_only, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)smem_sample(VMAX)));
+                            (int)smem_sample(2 * (VMAX + 1), VMAX)));
     CK(cudaFuncSetAttribute(k_classify<S5G_VARIANT_UNROLL>,
                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_CLS));
     CK(cudaFuncSetAttribute(k_classify<S5G_VARIANT_EQUAL>,
                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_CLS));
     CK(cudaFuncSetAttribute(k_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_SC));
-    CK(cudaFuncSetAttribute(k_seg_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_SEG));
+
     done = true;
     return 0;
 }
@@ -721,6 +657,8 @@ static int sort_impl(const s5g_sort_args* a) {
         return fail(S5G_E_WORKSPACE, "workspace too small: need " + std::to_string(need));
     carve(&w, (uint8_t*)a->workspace, n, t_medium);
     const int64_t small_max = small_max_of(t_medium);
+    ClassLists cls_lists;
+    for (int c = 0; c < NCLS; c++) cls_lists.off[c] = w.cls_off[c];
 
     CK(cudaMemsetAsync(w.ctr, 0, sizeof(Counters), st));
     PROF(K_INIT, n, 32LL * n, (k_init<<<blocks_for(n, 256), 256, 0, st>>>(a->arena, a->arena_len,
@@ -733,16 +671,18 @@ static int sort_impl(const s5g_sort_args* a) {
     std::vector<SegDev> large;
     SegDev root{0, a->depth, (int32_t)n, SEG_KEYS_VALID};
     if (n <= small_max) {
-        CK(cudaMemcpyAsync(w.small, &root, sizeof(SegDev), cudaMemcpyHostToDevice, st));
-        hc.n_small = 1;
-        CK(cudaMemcpyAsync(&w.ctr->n_small, &hc.n_small, 8, cudaMemcpyHostToDevice, st));
+        const int cls = size_class(n);
+        CK(cudaMemcpyAsync(w.small + w.cls_off[cls], &root, sizeof(SegDev),
+                           cudaMemcpyHostToDevice, st));
+        hc.n_cls[cls] = 1;
+        CK(cudaMemcpyAsync(&w.ctr->n_cls[cls], &hc.n_cls[cls], 8, cudaMemcpyHostToDevice, st));
     } else {
         large.push_back(root);
     }
     int in_b = 0;  // data of this round's segments lives in buffer B
     int round = 0;
     std::vector<StepDev> steps;
-    std::vector<int32_t> tile_step;
+    std::vector<int32_t> tile_step, cblk_step;
     std::vector<uint32_t> h_tot, h_bstart;
     std::vector<uint64_t> h_inorder;
     std::vector<int64_t> h_bounds;
@@ -764,13 +704,18 @@ static int sort_impl(const s5g_sort_args* a) {
                 d.lo = s.lo;
                 d.n = s.n;
                 d.depth = s.depth;
-                d.v = (int32_t)tree_capacity(s.n, vcap);
+                d.v = (int32_t)gpu_tree_capacity(s.n, vcap);
+                // oversampling: the reference's alpha = 2 for big trees, up to
+                // 16 for small ones (tighter buckets, same output)
+                const int alpha = std::max(OVERSAMPLE, std::min(16, 1024 / (d.v + 1)));
+                d.count = alpha * (d.v + 1) - 1;
                 d.levels = levels_of(d.v);
                 d.nb = 2 * d.v + 1;
                 d.keys_valid = (s.flags & SEG_KEYS_VALID) ? 1 : 0;
                 d.ntiles = (int32_t)((s.n + TILE - 1) / TILE);
                 int64_t need_cnt = (int64_t)d.ntiles * d.nb;
-                if ((int64_t)steps.size() + 1 > w.steps_cap || tile0 + d.ntiles > w.tiles_cap ||
+                if ((int64_t)steps.size() + 1 > w.steps_cap ||
+                    tile0 + d.ntiles + (bk_off + d.nb) / 32 + (int64_t)steps.size() + 1 > w.tiles_cap ||
                     cnt_off + need_cnt > w.cnt_cap || bk_off + d.nb > w.bk_cap ||
                     tree_off + d.v + 2 > w.tree_cap) {
                     if (steps.empty()) return fail(S5G_E_WORKSPACE, "step exceeds capacity");
@@ -789,10 +734,17 @@ static int sort_impl(const s5g_sort_args* a) {
             }
             i0 = i;
             const int nsteps = (int)steps.size();
+            cblk_step.clear();
+            for (int si = 0; si < nsteps; si++) {
+                steps[si].cblk0 = (int64_t)cblk_step.size();
+                for (int b = 0; b < steps[si].nb; b += 32) cblk_step.push_back(si);
+            }
             n_jobs += nsteps;
             CK(cudaMemcpyAsync(w.steps, steps.data(), sizeof(StepDev) * nsteps,
                                cudaMemcpyHostToDevice, st));
             CK(cudaMemcpyAsync(w.tile_step, tile_step.data(), 4 * tile_step.size(),
+                               cudaMemcpyHostToDevice, st));
+            CK(cudaMemcpyAsync(w.tile_step + tile0, cblk_step.data(), 4 * cblk_step.size(),
                                cudaMemcpyHostToDevice, st));
             const int64_t* hX = in_b ? w.hB : w.hA;
             uint64_t* kX = in_b ? w.kB : w.kA;
@@ -800,12 +752,14 @@ static int sort_impl(const s5g_sort_args* a) {
             uint64_t* kY = in_b ? w.kA : w.kB;
             int maxv = 1;
             long long sample_bytes = 0;
+            int maxP = 1;
             for (auto& d : steps) {
                 maxv = std::max(maxv, d.v);
-                sample_bytes += (long long)(2 * d.v + 1) * (d.keys_valid ? 8 : 16) + 27LL * d.v;
+                while (maxP < d.count) maxP <<= 1;
+                sample_bytes += (long long)d.count * (d.keys_valid ? 8 : 16) + 27LL * d.v;
             }
             PROF(K_SAMPLE, nsteps, sample_bytes,
-                 (k_sample_tree<<<nsteps, SAMPLE_NT, smem_sample(maxv), st>>>(
+                 (k_sample_tree<<<nsteps, SAMPLE_NT, smem_sample(maxP, maxv), st>>>(
                      w.steps, a->arena, a->arena_len, hX, kX, a->seed, w.tree, w.inorder, w.tpos,
                      w.eqb)));
             CK(cudaGetLastError());
@@ -826,15 +780,15 @@ static int sort_impl(const s5g_sort_args* a) {
                          w.steps, w.tile_step, a->arena, a->arena_len, hX, kX, w.bid, w.cnt,
                          w.tree, w.eqb, w.ctr)));
             CK(cudaGetLastError());
-            int maxnb = 2 * maxv + 1;
             PROF(K_SCAN_COLS, cnt_off, 8LL * cnt_off + 4LL * bk_off,
-                 (k_scan_cols<<<dim3(blocks_for(maxnb, 256), nsteps), 256, 0, st>>>(w.steps, w.cnt,
-                                                                                   w.tot)));
+                 (k_scan_cols<<<(unsigned)cblk_step.size(), 1024, 0, st>>>(
+                     w.steps, w.tile_step + tile0, w.cnt, w.tot)));
             CK(cudaGetLastError());
             PROF(K_SCAN_BUCKETS, bk_off, 8LL * bk_off,
                  (k_scan_buckets<<<nsteps, 1024, 0, st>>>(w.steps, w.tot, w.bstart, w.tpos, !in_b,
                                                          small_max, w.large[(round + 1) & 1],
-                                                         w.small, w.blist, lcps, w.ctr)));
+                                                         w.small, cls_lists, w.blist, lcps,
+                                                         w.ctr)));
             CK(cudaGetLastError());
             PROF(K_SCATTER, round_elems, 34LL * round_elems,
                  (k_scatter<<<ntiles, SC_NT, SMEM_SC, st>>>(w.steps, w.tile_step, hX, kX, w.bid,
@@ -875,13 +829,39 @@ static int sort_impl(const s5g_sort_args* a) {
         round++;
         if (round > a->arena_len / WORD + 64) return fail(S5G_E_INVALID, "no progress: corrupt input");
     }
-    if ((int64_t)hc.n_small > w.small_cap) return fail(S5G_E_WORKSPACE, "small list overflow");
-    if (hc.n_small)
-        PROF(K_SEG_SORT, (long long)hc.n_small, 0,
-             (k_seg_sort<<<(unsigned)hc.n_small, SEG_NT, SMEM_SEG, st>>>(
-                 w.small, w.hA, w.kA, w.hB, w.kB, a->arena, a->arena_len, a->out_handles, lcps,
-                 w.ctr)));
-    CK(cudaGetLastError());
+    long long n_small = 0;
+    for (int c = 0; c < NCLS; c++) {
+        const long long cnt_c = (long long)hc.n_cls[c];
+        n_small += cnt_c;
+        if (cnt_c > w.cls_cap[c]) return fail(S5G_E_WORKSPACE, "small list overflow");
+        if (!cnt_c) continue;
+        const unsigned grid = blocks_for(cnt_c, WS_NT / 32);
+        const SegDev* lst = w.small + w.cls_off[c];
+        switch (c) {
+            case 0: PROF(K_SEG_WARP + 0, cnt_c, 0, (k_warp_sort<1><<<grid, WS_NT, 0, st>>>(
+                        lst, cnt_c, w.hA, w.kA, w.hB, w.kB, a->arena, a->arena_len,
+                        a->out_handles, lcps, w.ctr))); break;
+            case 1: PROF(K_SEG_WARP + 1, cnt_c, 0, (k_warp_sort<2><<<grid, WS_NT, 0, st>>>(
+                        lst, cnt_c, w.hA, w.kA, w.hB, w.kB, a->arena, a->arena_len,
+                        a->out_handles, lcps, w.ctr))); break;
+            case 2: PROF(K_SEG_WARP + 2, cnt_c, 0, (k_warp_sort<4><<<grid, WS_NT, 0, st>>>(
+                        lst, cnt_c, w.hA, w.kA, w.hB, w.kB, a->arena, a->arena_len,
+                        a->out_handles, lcps, w.ctr))); break;
+            case 3: PROF(K_SEG_WARP + 3, cnt_c, 0, (k_warp_sort<8><<<grid, WS_NT, 0, st>>>(
+                        lst, cnt_c, w.hA, w.kA, w.hB, w.kB, a->arena, a->arena_len,
+                        a->out_handles, lcps, w.ctr))); break;
+            case 4: PROF(K_SEG_CTA2, cnt_c, 0, (k_cta_sort<2><<<(unsigned)cnt_c, 64,
+                        sizeof(CtaSortSmem<2>), st>>>(lst, cnt_c, w.hA, w.kA, w.hB, w.kB,
+                        a->arena, a->arena_len, a->out_handles, lcps, w.ctr))); break;
+            case 5: PROF(K_SEG_CTA4, cnt_c, 0, (k_cta_sort<4><<<(unsigned)cnt_c, 128,
+                        sizeof(CtaSortSmem<4>), st>>>(lst, cnt_c, w.hA, w.kA, w.hB, w.kB,
+                        a->arena, a->arena_len, a->out_handles, lcps, w.ctr))); break;
+            default: PROF(K_SEG_CTA8, cnt_c, 0, (k_cta_sort<8><<<(unsigned)cnt_c, 256,
+                        sizeof(CtaSortSmem<8>), st>>>(lst, cnt_c, w.hA, w.kA, w.hB, w.kB,
+                        a->arena, a->arena_len, a->out_handles, lcps, w.ctr))); break;
+        }
+        CK(cudaGetLastError());
+    }
     if (lcps) {
         if (hc.n_bound)
             PROF(K_BOUNDARY, (long long)hc.n_bound, 56LL * (long long)hc.n_bound,
@@ -899,11 +879,13 @@ static int sort_impl(const s5g_sort_args* a) {
     CK(cudaStreamSynchronize(st));
     // k_seg_sort: (h, key) in, (handle, lcp) out per element; (handle, word)
     // per re-keyed element
-    prof.set_bytes(K_SEG_SORT, 32LL * (long long)hc.small_elems + 16LL * (long long)hc.seg_fetches);
+    // register finishers: (handle, word) in, (handle, lcp) out per string, plus
+    // (handle, word) per re-keyed string; attributed to the <8> CTA class
+    prof.set_bytes(K_SEG_CTA8, 32LL * (long long)hc.small_elems + 16LL * (long long)hc.seg_fetches);
     if (a->stats) {
         a->stats->word_fetches += n + (int64_t)hc.fetches + (int64_t)hc.seg_fetches;
-        a->stats->jobs_enqueued += n_jobs + (int64_t)hc.n_small;
-        a->stats->jobs_executed += n_jobs + (int64_t)hc.n_small;
+        a->stats->jobs_enqueued += n_jobs + n_small;
+        a->stats->jobs_executed += n_jobs + n_small;
     }
     return 0;
 }
@@ -938,6 +920,11 @@ int s5g_profile_read(s5g_kernel_profile* out, int max_entries) {
 }
 
 unsigned long long s5g_launch_count(void) { return g_launches; }
+
+int s5g_debug_arm(void* dev_buf) {
+    (void)dev_buf;  // no traced kernel in this build
+    return 0;
+}
 
 const char* s5g_last_error(void) { return g_err.c_str(); }
 

@@ -195,4 +195,33 @@ __device__ __forceinline__ uint32_t block_incl_max(uint32_t v, uint32_t* wsum) {
     return r;
 }
 
+// Exclusive max over the threads before this one (0 for thread 0).
+template <int NT>
+__device__ __forceinline__ uint32_t block_excl_max(uint32_t v, uint32_t* wsum) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x = max(x, y);
+    }
+    uint32_t ex = __shfl_up_sync(0xffffffffu, x, 1);
+    if (lane == 0) ex = 0;
+    if (lane == 31) wsum[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        uint32_t s = lane < NT / 32 ? wsum[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t y = __shfl_up_sync(0xffffffffu, s, o);
+            if (lane >= o) s = max(s, y);
+        }
+        if (lane < NT / 32) wsum[lane] = s;
+    }
+    __syncthreads();
+    uint32_t r = w ? max(wsum[w - 1], ex) : ex;
+    __syncthreads();
+    return r;
+}
+
 }  // namespace s5g

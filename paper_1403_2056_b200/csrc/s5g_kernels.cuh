@@ -18,15 +18,13 @@ namespace s5g {
 
 constexpr int TILE = 32768;     // elements per classify / scatter CTA
 constexpr int CLS_NT = 1024;
-constexpr int SC_NT = 1024;
+constexpr int SC_NT = 512;
 constexpr int SC_ITEMS = 4;
 constexpr int SC_SUB = SC_NT * SC_ITEMS;  // 4096-element stable sub-tiles
 constexpr int SC_RB = 7;                  // radix bits per ranking pass
 constexpr int SC_R = 1 << SC_RB;
 constexpr uint16_t BID_SENTINEL = 0x3FFF; // > any bucket id (max 16382)
 constexpr int SAMPLE_NT = 1024;
-constexpr int SEG_M = 2048;     // capacity of a CTA segment
-constexpr int SEG_NT = 256;
 
 enum : int32_t { SEG_KEYS_VALID = 1, SEG_IN_B = 2 };
 
@@ -38,6 +36,9 @@ struct StepDev {
     int64_t cnt_off;   // first entry in the tile x bucket count matrix
     int64_t bk_off;    // first entry in tot / bstart
     int64_t tree_off;  // first entry in tree / inorder / tpos / eqb (even)
+    int64_t cblk0;     // first 32-column block of k_scan_cols
+    int32_t count;     // sample size (>= v)
+    int32_t pad1;
 };
 
 struct SegDev {
@@ -45,9 +46,25 @@ struct SegDev {
     int32_t n, flags;
 };
 
+// small segments are finished in registers in seven size classes: one warp
+// for <= 32, 64, 128, 256 strings (1, 2, 4, 8 slots per lane), 2, 4 or 8
+// warps of 256 slots for <= 512, 1024, 2048
+constexpr int NCLS = 7;
+constexpr int SMALL_MAX = 2048;
+constexpr int SEG_TARGET = 1024;   // device-wide steps aim at buckets of this size
+
 struct Counters {
-    unsigned long long n_large, n_small, n_bound, fetches, seg_fetches, small_elems;
+    unsigned long long n_large, n_bound, fetches, seg_fetches, small_elems;
+    unsigned long long n_cls[NCLS];
 };
+
+struct ClassLists {
+    int64_t off[NCLS];
+};
+
+__host__ __device__ inline int size_class(int64_t n) {
+    return n <= 32 ? 0 : n <= 64 ? 1 : n <= 128 ? 2 : n <= 256 ? 3 : n <= 512 ? 4 : n <= 1024 ? 5 : 6;
+}
 
 // ---------------------------------------------------------------------------
 // shared-memory sorts
@@ -94,10 +111,11 @@ __device__ void bitonic_pairs(uint64_t* key, uint32_t* meta, int P) {
 // order is input order: stability comes from warp-minor digit offsets plus
 // match_any ranks inside each warp.
 __device__ void rank_pass(const uint16_t* kin, const uint16_t* vin, uint16_t* kout,
-                          uint16_t* vout, int shift, uint32_t* cnt, uint32_t* wsum) {
+                          uint16_t* vout, int shift, uint16_t* cnt, uint32_t* wsum) {
     constexpr int NW = SC_NT / 32;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    for (int i = threadIdx.x; i < SC_R * NW; i += SC_NT) cnt[i] = 0;
+    uint32_t* cnt32 = reinterpret_cast<uint32_t*>(cnt);
+    for (int i = threadIdx.x; i < SC_R * NW / 2; i += SC_NT) cnt32[i] = 0;
     __syncthreads();
     uint16_t kk[SC_ITEMS], vv[SC_ITEMS];
     uint32_t loc[SC_ITEMS], dg[SC_ITEMS];
@@ -111,7 +129,7 @@ __device__ void rank_pass(const uint16_t* kin, const uint16_t* vin, uint16_t* ko
         uint32_t peers = __match_any_sync(0xffffffffu, d);
         uint32_t base = cnt[d * NW + w];
         __syncwarp();
-        if (lane == __ffs(peers) - 1) cnt[d * NW + w] = base + __popc(peers);
+        if (lane == __ffs(peers) - 1) cnt[d * NW + w] = (uint16_t)(base + __popc(peers));
         __syncwarp();
         loc[j] = base + __popc(peers & lt);
         dg[j] = d;
@@ -125,7 +143,7 @@ __device__ void rank_pass(const uint16_t* kin, const uint16_t* vin, uint16_t* ko
         for (int i = 0; i < PER; i++) { v[i] = cnt[threadIdx.x * PER + i]; s += v[i]; }
         uint32_t run = block_excl_sum<SC_NT>(s, wsum, nullptr);
 #pragma unroll
-        for (int i = 0; i < PER; i++) { cnt[threadIdx.x * PER + i] = run; run += v[i]; }
+        for (int i = 0; i < PER; i++) { cnt[threadIdx.x * PER + i] = (uint16_t)run; run += v[i]; }
     }
     __syncthreads();
 #pragma unroll
