@@ -197,6 +197,7 @@ def run_ours(args):
     from paper_1403_2056_b200 import device as DV
 
     rank, world, local = dist_env()
+    _lib.lib().s5g_set_l2_fetch_granularity(args.l2_fetch)
     if world > 1:
         torch.cuda.set_device(local)
         dist.init_process_group("nccl")
@@ -298,6 +299,7 @@ def run_ours(args):
                           "frac": sort_gbs / peak, "unit": "GB/s"},
         "kernels": {k: {"ms_per_step": v["ms"] / args.steps,
                         "launches_per_step": v["launches"] / args.steps,
+                        "units_per_step": v["units"] / args.steps,
                         "GBps": v["bytes"] / (v["ms"] / 1000) / 1e9 if v["ms"] else None}
                     for k, v in kernels.items()},
         "kernel_ms_per_step": step_ms_sum,
@@ -324,6 +326,7 @@ def main(argv=None):
     ap.add_argument("--cpu-sample", type=int, default=1 << 22)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--l2-fetch", type=int, default=32)
     args = ap.parse_args(argv)
     if args.impl == "reference":
         return run_reference(args)

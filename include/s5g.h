@@ -135,6 +135,10 @@ void s5g_profile_reset(void);
 int s5g_profile_read(s5g_kernel_profile *out, int max_entries);
 /* Monotonic count of kernels this library has launched (all entry points). */
 unsigned long long s5g_launch_count(void);
+/* L2 fetch granularity (bytes: 32, 64 or 128) requested for the duration of
+ * each sort (cudaLimitMaxL2FetchGranularity; restored afterwards).  Default 32:
+ * the sort is dominated by random 8-byte gathers and stores. */
+void s5g_set_l2_fetch_granularity(int bytes);
 /* Debug: per-CTA trace of the small-segment sorter (5 x uint64 per CTA:
  * cycles, size, rounds, active elements over rounds, radix passes) into a
  * device buffer; NULL disarms. */

@@ -64,6 +64,7 @@ SIGNATURES = {
     "s5g_profile_reset": (None, []),
     "s5g_profile_read": (C.c_int, [C.POINTER(KernelProfile), C.c_int]),
     "s5g_launch_count": (C.c_ulonglong, []),
+    "s5g_set_l2_fetch_granularity": (None, [C.c_int]),
     "s5g_debug_arm": (C.c_int, [_p]),
     "s5g_last_error": (C.c_char_p, []),
     "s5g_version": (C.c_int, []),

@@ -292,6 +292,7 @@ __global__ void __launch_bounds__(1024) k_scan_buckets(
                 if ((int64_t)size <= small_max) {
                     const int ci = size_class(size);
                     small_out[cls.off[ci] + atomicAdd(&ctr->n_cls[ci], 1ull)] = c;
+                    atomicAdd(&ctr->cls_elems[ci], (unsigned long long)size);
                 }
                 else
                     large_out[atomicAdd(&ctr->n_large, 1ull)] = c;
@@ -413,6 +414,7 @@ __global__ void k_single(const int64_t* __restrict__ handles, int64_t* __restric
 // host side
 
 static thread_local std::string g_err;
+static size_t g_l2_fetch = 32;  // s5g_set_l2_fetch_granularity
 
 // ---- live per-kernel timing (CUDA events on the launching stream) --------
 enum KernelId { K_INIT, K_SAMPLE, K_CLASSIFY, K_SCAN_COLS, K_SCAN_BUCKETS, K_SCATTER, K_SEG_WARP,
@@ -615,6 +617,12 @@ static int set_smem_attrs() {
     CK(cudaFuncSetAttribute(k_classify<S5G_VARIANT_EQUAL>,
                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_CLS));
     CK(cudaFuncSetAttribute(k_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_SC));
+    CK(cudaFuncSetAttribute(k_cta_sort<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)sizeof(CtaSortSmem<2>)));
+    CK(cudaFuncSetAttribute(k_cta_sort<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)sizeof(CtaSortSmem<4>)));
+    CK(cudaFuncSetAttribute(k_cta_sort<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)sizeof(CtaSortSmem<8>)));
 
     done = true;
     return 0;
@@ -622,7 +630,31 @@ static int set_smem_attrs() {
 
 static inline unsigned blocks_for(int64_t n, int nt) { return (unsigned)((n + nt - 1) / nt); }
 
+// Random 8-byte gathers from the arena and scattered 8-byte stores: ask the
+// L2 for 32-byte (sector) fetches instead of whole lines while we sort, and
+// put the caller's setting back afterwards.
+struct L2Granularity {
+    size_t saved = 0;
+    bool ok = false;
+    explicit L2Granularity(size_t bytes) {
+        ok = cudaDeviceGetLimit(&saved, cudaLimitMaxL2FetchGranularity) == cudaSuccess &&
+             cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, bytes) == cudaSuccess;
+        cudaGetLastError();
+    }
+    ~L2Granularity() {
+        if (ok) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, saved);
+        cudaGetLastError();
+    }
+};
+
+static int sort_impl_body(const s5g_sort_args* a);
+
 static int sort_impl(const s5g_sort_args* a) {
+    L2Granularity l2g(g_l2_fetch);
+    return sort_impl_body(a);
+}
+
+static int sort_impl_body(const s5g_sort_args* a) {
     const int64_t n = a->n;
     cudaStream_t st = (cudaStream_t)a->stream;
     if (n < 0 || a->arena_len < 0) return fail(S5G_E_INVALID, "negative size");
@@ -675,7 +707,9 @@ static int sort_impl(const s5g_sort_args* a) {
         CK(cudaMemcpyAsync(w.small + w.cls_off[cls], &root, sizeof(SegDev),
                            cudaMemcpyHostToDevice, st));
         hc.n_cls[cls] = 1;
+        hc.cls_elems[cls] = n;
         CK(cudaMemcpyAsync(&w.ctr->n_cls[cls], &hc.n_cls[cls], 8, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(&w.ctr->cls_elems[cls], &hc.cls_elems[cls], 8, cudaMemcpyHostToDevice, st));
     } else {
         large.push_back(root);
     }
@@ -838,25 +872,25 @@ static int sort_impl(const s5g_sort_args* a) {
         const unsigned grid = blocks_for(cnt_c, WS_NT / 32);
         const SegDev* lst = w.small + w.cls_off[c];
         switch (c) {
-            case 0: PROF(K_SEG_WARP + 0, cnt_c, 0, (k_warp_sort<1><<<grid, WS_NT, 0, st>>>(
+            case 0: PROF(K_SEG_WARP + 0, (long long)hc.cls_elems[0], 0, (k_warp_sort<1><<<grid, WS_NT, 0, st>>>(
                         lst, cnt_c, w.hA, w.kA, w.hB, w.kB, a->arena, a->arena_len,
                         a->out_handles, lcps, w.ctr))); break;
-            case 1: PROF(K_SEG_WARP + 1, cnt_c, 0, (k_warp_sort<2><<<grid, WS_NT, 0, st>>>(
+            case 1: PROF(K_SEG_WARP + 1, (long long)hc.cls_elems[1], 0, (k_warp_sort<2><<<grid, WS_NT, 0, st>>>(
                         lst, cnt_c, w.hA, w.kA, w.hB, w.kB, a->arena, a->arena_len,
                         a->out_handles, lcps, w.ctr))); break;
-            case 2: PROF(K_SEG_WARP + 2, cnt_c, 0, (k_warp_sort<4><<<grid, WS_NT, 0, st>>>(
+            case 2: PROF(K_SEG_WARP + 2, (long long)hc.cls_elems[2], 0, (k_warp_sort<4><<<grid, WS_NT, 0, st>>>(
                         lst, cnt_c, w.hA, w.kA, w.hB, w.kB, a->arena, a->arena_len,
                         a->out_handles, lcps, w.ctr))); break;
-            case 3: PROF(K_SEG_WARP + 3, cnt_c, 0, (k_warp_sort<8><<<grid, WS_NT, 0, st>>>(
+            case 3: PROF(K_SEG_WARP + 3, (long long)hc.cls_elems[3], 0, (k_warp_sort<8><<<grid, WS_NT, 0, st>>>(
                         lst, cnt_c, w.hA, w.kA, w.hB, w.kB, a->arena, a->arena_len,
                         a->out_handles, lcps, w.ctr))); break;
-            case 4: PROF(K_SEG_CTA2, cnt_c, 0, (k_cta_sort<2><<<(unsigned)cnt_c, 64,
+            case 4: PROF(K_SEG_CTA2, (long long)hc.cls_elems[4], 0, (k_cta_sort<2><<<(unsigned)cnt_c, 64,
                         sizeof(CtaSortSmem<2>), st>>>(lst, cnt_c, w.hA, w.kA, w.hB, w.kB,
                         a->arena, a->arena_len, a->out_handles, lcps, w.ctr))); break;
-            case 5: PROF(K_SEG_CTA4, cnt_c, 0, (k_cta_sort<4><<<(unsigned)cnt_c, 128,
+            case 5: PROF(K_SEG_CTA4, (long long)hc.cls_elems[5], 0, (k_cta_sort<4><<<(unsigned)cnt_c, 128,
                         sizeof(CtaSortSmem<4>), st>>>(lst, cnt_c, w.hA, w.kA, w.hB, w.kB,
                         a->arena, a->arena_len, a->out_handles, lcps, w.ctr))); break;
-            default: PROF(K_SEG_CTA8, cnt_c, 0, (k_cta_sort<8><<<(unsigned)cnt_c, 256,
+            default: PROF(K_SEG_CTA8, (long long)hc.cls_elems[6], 0, (k_cta_sort<8><<<(unsigned)cnt_c, 256,
                         sizeof(CtaSortSmem<8>), st>>>(lst, cnt_c, w.hA, w.kA, w.hB, w.kB,
                         a->arena, a->arena_len, a->out_handles, lcps, w.ctr))); break;
         }
@@ -920,6 +954,8 @@ int s5g_profile_read(s5g_kernel_profile* out, int max_entries) {
 }
 
 unsigned long long s5g_launch_count(void) { return g_launches; }
+
+void s5g_set_l2_fetch_granularity(int bytes) { g_l2_fetch = bytes > 0 ? (size_t)bytes : 32; }
 
 int s5g_debug_arm(void* dev_buf) {
     (void)dev_buf;  // no traced kernel in this build

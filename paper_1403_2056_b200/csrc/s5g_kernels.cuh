@@ -56,6 +56,7 @@ constexpr int SEG_TARGET = 1024;   // device-wide steps aim at buckets of this s
 struct Counters {
     unsigned long long n_large, n_bound, fetches, seg_fetches, small_elems;
     unsigned long long n_cls[NCLS];
+    unsigned long long cls_elems[NCLS];
 };
 
 struct ClassLists {

@@ -216,15 +216,151 @@ __device__ __forceinline__ bool cs_less(uint64_t ka, uint32_t ma, uint64_t kb, u
 
 template <int W>
 struct CtaSortSmem {
-    int64_t h[256 * W];
+    int64_t h[256 * W];           // handle by tag
     uint64_t xk[256 * W];
     uint32_t xm[256 * W];
+    uint16_t ord[256 * W];        // tag at slot (group mode)
+    uint16_t gs[128 * W], ge[128 * W];  // group mode: first / last slot of each run
     uint64_t last_key[W];
-    uint32_t first_brk[W], first_act[W], wmax[W];
+    uint32_t first_brk[W], first_act[W], wmax[W], wcnt[W];
 };
 
+// Bitonic network on one warp's 32*IT slots, comparator cs_less.
+template <int IT>
+__device__ __forceinline__ void cs_bitonic(uint64_t (&key)[IT], uint32_t (&meta)[IT], int lane) {
+    constexpr int P = 32 * IT;
+#pragma unroll
+    for (int k = 2; k <= P; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j < IT) {
+#pragma unroll
+                for (int e = 0; e < IT; e++) {
+                    const int f = e ^ j;
+                    if (f > e) {
+                        const bool up = ((lane * IT + e) & k) == 0;
+                        if (cs_less(key[f], meta[f], key[e], meta[e]) == up) {
+                            uint64_t tk = key[e]; key[e] = key[f]; key[f] = tk;
+                            uint32_t tm = meta[e]; meta[e] = meta[f]; meta[f] = tm;
+                        }
+                    }
+                }
+            } else {
+                const int lx = j / IT;
+#pragma unroll
+                for (int e = 0; e < IT; e++) {
+                    const uint64_t ok = __shfl_xor_sync(0xffffffffu, key[e], lx);
+                    const uint32_t om = __shfl_xor_sync(0xffffffffu, meta[e], lx);
+                    const int i = lane * IT + e;
+                    const bool up = (i & k) == 0, lower = (i & j) == 0;
+                    if (cs_less(ok, om, key[e], meta[e]) == (lower == up)) {
+                        key[e] = ok;
+                        meta[e] = om;
+                    }
+                }
+            }
+        }
+    }
+}
+
+// One warp finishes one run of gn <= 32*IT strings (slots g0.. of the
+// segment) that share `depth` characters: re-key one word deeper, sort,
+// LCPs, recurse on equal runs -- all in registers.  Writes the final tag
+// order back to ord[g0 .. g0+gn).
+template <int IT>
+__device__ void cs_finish_group(const int64_t* __restrict__ hbt, uint16_t* __restrict__ ord,
+                                int g0, int gn, int64_t depth, const uint8_t* __restrict__ arena,
+                                int64_t alen, int64_t* __restrict__ lcp_seg, unsigned& fetches,
+                                int lane) {
+    uint64_t key[IT];
+    uint32_t meta[IT];
+#pragma unroll
+    for (int e = 0; e < IT; e++) {
+        const int i = lane * IT + e;
+        if (i < gn) {
+            const uint32_t tag = ord[g0 + i];
+            key[e] = load_key(arena, alen, hbt[tag], depth);
+            meta[e] = (1u << 22) | tag;
+            fetches++;
+        } else {
+            key[e] = ~0ull;
+            meta[e] = (uint32_t)i << 11;
+        }
+    }
+    for (;;) {
+        cs_bitonic<IT>(key, meta, lane);
+        const uint64_t prev_last = __shfl_up_sync(0xffffffffu, key[IT - 1], 1);
+        bool brk[IT];
+#pragma unroll
+        for (int e = 0; e < IT; e++) {
+            const int i = lane * IT + e;
+            const bool act = meta[e] >> 22 & 1;
+            brk[e] = true;
+            if (act && i != (int)(meta[e] >> 11 & 0x7ff)) {
+                const uint64_t pk = e ? key[e - 1] : prev_last;
+                if (pk != key[e]) {
+                    if (lcp_seg) lcp_seg[g0 + i] = depth + (__clzll(pk ^ key[e]) >> 3);
+                } else {
+                    brk[e] = false;
+                    const int tpv = term_pos(key[e]);
+                    if (lcp_seg && tpv < WORD) lcp_seg[g0 + i] = depth + tpv;
+                }
+            }
+        }
+        const bool next_brk0 = __shfl_down_sync(0xffffffffu, brk[0], 1);
+        const bool next_act0 = __shfl_down_sync(0xffffffffu, meta[0] >> 22 & 1u, 1);
+        bool keep[IT];
+        bool any = false;
+        uint32_t run = 0;
+#pragma unroll
+        for (int e = 0; e < IT; e++) {
+            const int i = lane * IT + e;
+            const bool act = meta[e] >> 22 & 1;
+            bool nb, na;
+            if (e + 1 < IT) {
+                nb = brk[e + 1];
+                na = meta[e + 1] >> 22 & 1;
+            } else {
+                nb = next_brk0;
+                na = next_act0 && lane < 31;
+            }
+            keep[e] = act && term_pos(key[e]) == WORD && (!brk[e] || (na && !nb));
+            any |= keep[e];
+            if (keep[e] && brk[e]) run = i + 1;
+        }
+        if (!__any_sync(0xffffffffu, any) || depth > alen) break;  // alen: corrupt-input guard
+        uint32_t incl = run;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl = max(incl, y);
+        }
+        uint32_t cur = __shfl_up_sync(0xffffffffu, incl, 1);
+        if (lane == 0) cur = 0;
+        depth += WORD;
+#pragma unroll
+        for (int e = 0; e < IT; e++) {
+            const int i = lane * IT + e;
+            if (keep[e] && brk[e]) cur = i + 1;
+            const uint32_t tag = meta[e] & 0x7ff;
+            meta[e] = keep[e] ? ((1u << 22) | ((cur - 1) << 11) | tag) : (((uint32_t)i << 11) | tag);
+        }
+#pragma unroll
+        for (int e = 0; e < IT; e++)
+            if (meta[e] >> 22 & 1) {
+                key[e] = load_key(arena, alen, hbt[meta[e] & 0x7ff], depth);
+                fetches++;
+            }
+    }
+#pragma unroll
+    for (int e = 0; e < IT; e++) {
+        const int i = lane * IT + e;
+        if (i < gn) ord[g0 + i] = (uint16_t)(meta[e] & 0x7ff);
+    }
+}
+
 template <int W>
-__global__ void __launch_bounds__(32 * W) k_cta_sort(
+__global__ void __launch_bounds__(32 * W, 24 / W) k_cta_sort(
     const SegDev* __restrict__ segs, int64_t nsegs, const int64_t* __restrict__ hA,
     const uint64_t* __restrict__ kA, const int64_t* __restrict__ hB,
     const uint64_t* __restrict__ kB, const uint8_t* __restrict__ arena, int64_t alen,
@@ -239,6 +375,7 @@ __global__ void __launch_bounds__(32 * W) k_cta_sort(
     const int64_t* sh = (sg.flags & SEG_IN_B) ? hB : hA;
     const uint64_t* sk = (sg.flags & SEG_IN_B) ? kB : kA;
     const bool valid = sg.flags & SEG_KEYS_VALID;
+    int64_t* lcp_seg = lcps ? lcps + lo : nullptr;
     int64_t depth = sg.depth;
     unsigned fetches = 0;
     for (int i = threadIdx.x; i < m; i += NT) S.h[i] = sh[lo + i];
@@ -258,6 +395,7 @@ __global__ void __launch_bounds__(32 * W) k_cta_sort(
         }
     }
     if (!valid) fetches += min(ITEMS, max(0, m - base));
+    bool group_mode = false;
     for (;;) {
         // ---- bitonic network over (group, word, tag) ----------------------
 #pragma unroll 1
@@ -330,11 +468,11 @@ __global__ void __launch_bounds__(32 * W) k_cta_sort(
             if (act && i != grp) {
                 const uint64_t pk = e ? key[e - 1] : prev_last;
                 if (pk != key[e]) {
-                    if (lcps) lcps[lo + i] = depth + (__clzll(pk ^ key[e]) >> 3);
+                    if (lcp_seg) lcp_seg[i] = depth + (__clzll(pk ^ key[e]) >> 3);
                 } else {
                     brk[e] = false;
                     const int tpv = term_pos(key[e]);
-                    if (lcps && tpv < WORD) lcps[lo + i] = depth + tpv;
+                    if (lcp_seg && tpv < WORD) lcp_seg[i] = depth + tpv;
                 }
             }
         }
@@ -349,9 +487,9 @@ __global__ void __launch_bounds__(32 * W) k_cta_sort(
             next_brk0 = w + 1 < W ? S.first_brk[w + 1] : true;
             next_act0 = w + 1 < W ? S.first_act[w + 1] : false;
         }
-        bool keep[ITEMS];
+        bool keep[ITEMS], kend[ITEMS];
         bool any = false;
-        uint32_t run = 0;
+        uint32_t run = 0, nstart = 0, nend = 0;
 #pragma unroll
         for (int e = 0; e < ITEMS; e++) {
             const int i = base + e;
@@ -365,11 +503,13 @@ __global__ void __launch_bounds__(32 * W) k_cta_sort(
                 na = next_act0;
             }
             keep[e] = act && term_pos(key[e]) == WORD && (!brk[e] || (na && !nb));
+            kend[e] = keep[e] && (!na || nb);  // last slot of a kept run
             any |= keep[e];
-            if (keep[e] && brk[e]) run = i + 1;
+            if (keep[e] && brk[e]) { run = i + 1; nstart++; }
+            nend += kend[e];
         }
         if (!__syncthreads_or(any) || depth > alen) break;  // alen: corrupt-input guard
-        // run starts: max-scan over the CTA
+        // run starts: max-scan over the CTA (next round's group ids)
         uint32_t incl = run;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -381,6 +521,54 @@ __global__ void __launch_bounds__(32 * W) k_cta_sort(
         uint32_t cur = __shfl_up_sync(0xffffffffu, incl, 1);
         if (lane == 0) cur = 0;
         for (int v = 0; v < w; v++) cur = max(cur, S.wmax[v]);
+        // longest kept run decides: CTA round again, or one warp per run
+        uint32_t longest = 0, c2 = cur;
+#pragma unroll
+        for (int e = 0; e < ITEMS; e++) {
+            const int i = base + e;
+            if (keep[e] && brk[e]) c2 = i + 1;
+            if (kend[e]) longest = max(longest, (uint32_t)i + 2 - c2);
+        }
+        longest = __reduce_max_sync(0xffffffffu, longest);
+        if (lane == 0) S.wcnt[w] = longest;
+        __syncthreads();
+        uint32_t lmax = 0;
+        for (int v = 0; v < W; v++) lmax = max(lmax, S.wcnt[v]);
+        if (W == 8 && lmax <= 256) {
+            // ---- group mode: write the slot order, list the kept runs --------
+#pragma unroll
+            for (int e = 0; e < ITEMS; e++) S.ord[base + e] = (uint16_t)(meta[e] & 0x7ff);
+            // starts and ends are counted separately: a run may span threads
+            const uint32_t mine = nstart | (nend << 16);
+            const uint32_t ns = __reduce_add_sync(0xffffffffu, mine);
+            uint32_t pre = mine;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, pre, o);
+                if (lane >= o) pre += y;
+            }
+            pre -= mine;
+            __syncthreads();
+            if (lane == 0) S.wcnt[w] = ns;
+            __syncthreads();
+            uint32_t off = 0, tot2 = 0;
+            for (int v = 0; v < W; v++) {
+                if (v < w) off += S.wcnt[v];
+                tot2 += S.wcnt[v];
+            }
+            const uint32_t ngroups = tot2 & 0xffff;
+            uint32_t gi = (off + pre) & 0xffff, ge_i = (off + pre) >> 16;
+#pragma unroll
+            for (int e = 0; e < ITEMS; e++) {
+                const int i = base + e;
+                if (keep[e] && brk[e]) S.gs[gi++] = (uint16_t)i;
+                if (kend[e]) S.ge[ge_i++] = (uint16_t)i;
+            }
+            if (threadIdx.x == 0) S.wcnt[0] = ngroups;
+            __syncthreads();
+            group_mode = true;
+            break;
+        }
         depth += WORD;
 #pragma unroll
         for (int e = 0; e < ITEMS; e++) {
@@ -395,13 +583,28 @@ __global__ void __launch_bounds__(32 * W) k_cta_sort(
                 key[e] = load_key(arena, alen, S.h[meta[e] & 0x7ff], depth);
                 fetches++;
             }
-        __syncthreads();  // S.wmax / S.last_key reuse
+        __syncthreads();  // S.wmax / S.last_key / S.wcnt reuse
     }
+    if (!group_mode) {
 #pragma unroll
-    for (int e = 0; e < ITEMS; e++) {
-        const int i = base + e;
-        if (i < m) out_h[lo + i] = S.h[meta[e] & 0x7ff];
+        for (int e = 0; e < ITEMS; e++) S.ord[base + e] = (uint16_t)(meta[e] & 0x7ff);
+    } else {
+        // one warp per remaining run, each finished entirely in registers
+        const uint32_t ngroups = S.wcnt[0];
+        for (uint32_t g = w; g < ngroups; g += W) {
+            const int g0 = S.gs[g], gn = S.ge[g] - g0 + 1;
+            if (gn <= 32)
+                cs_finish_group<1>(S.h, S.ord, g0, gn, depth + WORD, arena, alen, lcp_seg, fetches, lane);
+            else if (gn <= 64)
+                cs_finish_group<2>(S.h, S.ord, g0, gn, depth + WORD, arena, alen, lcp_seg, fetches, lane);
+            else if (gn <= 128)
+                cs_finish_group<4>(S.h, S.ord, g0, gn, depth + WORD, arena, alen, lcp_seg, fetches, lane);
+            else
+                cs_finish_group<8>(S.h, S.ord, g0, gn, depth + WORD, arena, alen, lcp_seg, fetches, lane);
+        }
     }
+    __syncthreads();
+    for (int i = threadIdx.x; i < m; i += NT) out_h[lo + i] = S.h[S.ord[i]];
     fetches = __reduce_add_sync(0xffffffffu, fetches);
     if (lane == 0 && fetches) atomicAdd(&ctr->seg_fetches, (unsigned long long)fetches);
     if (threadIdx.x == 0) atomicAdd(&ctr->small_elems, (unsigned long long)m);
