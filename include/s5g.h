@@ -114,6 +114,27 @@ int s5g_classify(const uint64_t *keys, int64_t n, const uint64_t *tree,
                  const uint16_t *eq_bucket, int64_t v, int32_t variant, uint16_t *out_bucket,
                  void *stream);
 
+/* Multi-GPU partition step (the G-rank form of _phased_step's classify,
+ * parallel.py:359-398): out_rank[i] = number of splitters
+ * (splitters[splitter_off[j] .. splitter_off[j+1]), splitter_gidx[j]) ordered
+ * before (string at handles[i], base_index + i) -- full-string comparison,
+ * ties broken by global input index, so equal strings keep input order
+ * across ranks.  All pointers are device pointers. */
+int s5g_partition(const uint8_t *arena, int64_t arena_len, const int64_t *handles, int64_t n,
+                  int64_t base_index, const uint8_t *splitters, const int64_t *splitter_off,
+                  const int64_t *splitter_gidx, int32_t nsplitters, int32_t *out_rank,
+                  void *stream);
+
+/* String lengths (StringSet.ends - handles, strset.py:64-78). */
+int s5g_lengths(const uint8_t *arena, int64_t arena_len, const int64_t *handles, int64_t n,
+                int64_t *out_len, void *stream);
+
+/* Pack strings with their terminators into dst at dst_off[i] (the send
+ * buffer of the multi-GPU exchange). */
+int s5g_pack(const uint8_t *arena, int64_t arena_len, const int64_t *handles,
+             const int64_t *lengths, const int64_t *dst_off, int64_t n, uint8_t *dst,
+             void *stream);
+
 /* fill_dchar (basecase.py:36-42). */
 int s5g_fill_dchar(const uint8_t *arena, const int64_t *handles, const int64_t *lcps, int64_t n,
                    uint8_t *out_dchar, void *stream);

@@ -60,6 +60,9 @@ SIGNATURES = {
     "s5g_select_splitters": (C.c_int, [_p, _i64, _i64, _p, _p, _p, _p, _p]),
     "s5g_classify": (C.c_int, [_p, _i64, _p, _p, _i64, _i32, _p, _p]),
     "s5g_fill_dchar": (C.c_int, [_p, _p, _p, _i64, _p, _p]),
+    "s5g_partition": (C.c_int, [_p, _i64, _p, _i64, _i64, _p, _p, _p, _i32, _p, _p]),
+    "s5g_lengths": (C.c_int, [_p, _i64, _p, _i64, _p, _p]),
+    "s5g_pack": (C.c_int, [_p, _i64, _p, _p, _p, _i64, _p, _p]),
     "s5g_profile_enable": (None, [C.c_int]),
     "s5g_profile_reset": (None, []),
     "s5g_profile_read": (C.c_int, [C.POINTER(KernelProfile), C.c_int]),

@@ -150,8 +150,9 @@ def gen_suffix_markov(n: int = 1 << 24, seed: int = 3, copy_frac: float = 0.05,
     text = text.reshape(-1)[:n]
     copied = 0
     target = int(copy_frac * n)
+    hi_len = max(2, min(4097, n // 4))
     while copied < target:
-        L = int(rng.integers(1024, 4097))
+        L = int(rng.integers(min(1024, hi_len - 1), hi_len))
         p = int(rng.integers(L + 1, n - L))
         q = int(rng.integers(0, p - L))
         text[p:p + L] = text[q:q + L]

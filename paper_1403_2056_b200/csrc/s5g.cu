@@ -406,6 +406,67 @@ __global__ void k_dchar(const uint8_t* __restrict__ arena, const int64_t* __rest
     }
 }
 
+// Multi-GPU partition: destination rank of every string =
+// number of splitters (s_j, g_j) ordered before (string, global index),
+// comparing full strings against the splitter byte strings, ties by global
+// input index.  Splitters live in one device blob (sp_off[j]..sp_off[j+1]).
+__device__ __forceinline__ int cmp_string_splitter(const uint8_t* __restrict__ arena, int64_t alen,
+                                                   int64_t h, const uint8_t* __restrict__ sp,
+                                                   int64_t sp_len) {
+    for (int64_t i = 0;; i++) {
+        const int c = (h + i) < alen ? arena[h + i] : 0;
+        const int d = i < sp_len ? sp[i] : 0;
+        if (c != d) return c < d ? -1 : 1;
+        if (c == 0) return 0;
+    }
+}
+
+__global__ void k_partition(const uint8_t* __restrict__ arena, int64_t alen,
+                            const int64_t* __restrict__ handles, int64_t n, int64_t base_index,
+                            const uint8_t* __restrict__ sp_blob, const int64_t* __restrict__ sp_off,
+                            const int64_t* __restrict__ sp_gidx, int nsp,
+                            int32_t* __restrict__ out_rank) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int64_t h = handles[i], g = base_index + i;
+    int lo = 0, hi = nsp;  // first splitter greater than (string, g)
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        int c = cmp_string_splitter(arena, alen, h, sp_blob + sp_off[mid], sp_off[mid + 1] - sp_off[mid]);
+        if (c == 0) c = g < sp_gidx[mid] ? -1 : (g > sp_gidx[mid] ? 1 : 0);
+        if (c < 0) hi = mid; else lo = mid + 1;
+    }
+    out_rank[i] = lo;
+}
+
+// String lengths (terminator scan, word at a time).
+__global__ void k_lengths(const uint8_t* __restrict__ arena, int64_t alen,
+                          const int64_t* __restrict__ handles, int64_t n, int64_t* __restrict__ out) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int64_t h = handles[i];
+    int64_t len = 0;
+    for (;;) {
+        const uint64_t be = bswap64(load_word_le(arena, alen, h + len));
+        const uint64_t z = zero_bytes(be);
+        if (z) { len += __clzll(z) >> 3; break; }
+        len += WORD;
+    }
+    out[i] = len;
+}
+
+// Pack strings (terminator included) to dst[dst_off[i] ..]: the send buffer
+// of the multi-GPU exchange.  One warp per string, 8-byte chunks.
+__global__ void k_pack(const uint8_t* __restrict__ arena, int64_t alen,
+                       const int64_t* __restrict__ handles, const int64_t* __restrict__ lens,
+                       const int64_t* __restrict__ dst_off, int64_t n, uint8_t* __restrict__ dst) {
+    const int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (i >= n) return;
+    const int64_t h = handles[i], L = lens[i] + 1, o = dst_off[i];
+    for (int64_t b = lane; b < L; b += 32) dst[o + b] = b < L - 1 && h + b < alen ? arena[h + b] : 0;
+}
+
 __global__ void k_single(const int64_t* __restrict__ handles, int64_t* __restrict__ out_h) {
     out_h[0] = handles[0];
 }
@@ -1087,6 +1148,46 @@ int s5g_classify(const uint64_t* keys, int64_t n, const uint64_t* tree, const ui
     else
         k_classify_only<S5G_VARIANT_EQUAL><<<blocks_for(n, 256), 256, smem, st>>>(
             keys, n, tree, eq_bucket, (int)v, levels_of(v), out_bucket);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(st));
+    return 0;
+}
+
+int s5g_partition(const uint8_t* arena, int64_t arena_len, const int64_t* handles, int64_t n,
+                  int64_t base_index, const uint8_t* splitters, const int64_t* splitter_off,
+                  const int64_t* splitter_gidx, int32_t nsplitters, int32_t* out_rank,
+                  void* stream) {
+    if (n <= 0) return n < 0 ? fail(S5G_E_INVALID, "negative n") : 0;
+    if (nsplitters < 0) return fail(S5G_E_INVALID, "negative splitter count");
+    cudaStream_t st = (cudaStream_t)stream;
+    g_launches++;
+    k_partition<<<blocks_for(n, 256), 256, 0, st>>>(arena, arena_len, handles, n, base_index,
+                                                    splitters, splitter_off, splitter_gidx,
+                                                    nsplitters, out_rank);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(st));
+    return 0;
+}
+
+int s5g_lengths(const uint8_t* arena, int64_t arena_len, const int64_t* handles, int64_t n,
+                int64_t* out_len, void* stream) {
+    if (n <= 0) return n < 0 ? fail(S5G_E_INVALID, "negative n") : 0;
+    cudaStream_t st = (cudaStream_t)stream;
+    g_launches++;
+    k_lengths<<<blocks_for(n, 256), 256, 0, st>>>(arena, arena_len, handles, n, out_len);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(st));
+    return 0;
+}
+
+int s5g_pack(const uint8_t* arena, int64_t arena_len, const int64_t* handles,
+             const int64_t* lengths, const int64_t* dst_off, int64_t n, uint8_t* dst,
+             void* stream) {
+    if (n <= 0) return n < 0 ? fail(S5G_E_INVALID, "negative n") : 0;
+    cudaStream_t st = (cudaStream_t)stream;
+    g_launches++;
+    k_pack<<<blocks_for(n * 32, 256), 256, 0, st>>>(arena, arena_len, handles, lengths, dst_off,
+                                                    n, dst);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(st));
     return 0;

@@ -160,3 +160,38 @@ def sort_host(buffer, handles, depth: int = 0, want_lcps: bool = True, want_dcha
                               _lib.VARIANTS[variant], int(min(max(v, 1), 8191)), int(seed),
                               int(t_medium), C.byref(st)))
     return oh, ol, od
+
+
+def partition(ds: DeviceStrings, base_index: int, splitters: list[bytes], splitter_gidx) -> torch.Tensor:
+    """Destination rank of every string (s5g_partition); splitters sorted."""
+    dev = ds.handles.device
+    blob = b"".join(splitters)
+    off = np.zeros(len(splitters) + 1, dtype=np.int64)
+    if splitters:
+        np.cumsum([len(x) for x in splitters], out=off[1:])
+    blob_d = torch.from_numpy(np.frombuffer(blob, dtype=np.uint8).copy() if blob else
+                              np.zeros(1, np.uint8)).to(dev)
+    off_d = torch.from_numpy(off).to(dev)
+    gidx_d = torch.as_tensor(np.asarray(splitter_gidx, dtype=np.int64), device=dev)
+    out = torch.empty(ds.n, dtype=torch.int32, device=dev)
+    check(lib().s5g_partition(ds.arena.data_ptr(), ds.arena_len, ds.handles.data_ptr(), ds.n,
+                              int(base_index), blob_d.data_ptr(), off_d.data_ptr(),
+                              gidx_d.data_ptr() if len(splitters) else None, len(splitters),
+                              out.data_ptr(), torch.cuda.current_stream(dev).cuda_stream))
+    return out
+
+
+def lengths(ds: DeviceStrings) -> torch.Tensor:
+    out = torch.empty(ds.n, dtype=torch.int64, device=ds.handles.device)
+    check(lib().s5g_lengths(ds.arena.data_ptr(), ds.arena_len, ds.handles.data_ptr(), ds.n,
+                            out.data_ptr(), torch.cuda.current_stream().cuda_stream))
+    return out
+
+
+def pack(ds: DeviceStrings, handles: torch.Tensor, lens: torch.Tensor, dst_off: torch.Tensor,
+         total: int) -> torch.Tensor:
+    dst = torch.empty(max(total, 1), dtype=torch.uint8, device=ds.handles.device)
+    check(lib().s5g_pack(ds.arena.data_ptr(), ds.arena_len, handles.data_ptr(), lens.data_ptr(),
+                         dst_off.data_ptr(), handles.numel(), dst.data_ptr(),
+                         torch.cuda.current_stream().cuda_stream))
+    return dst

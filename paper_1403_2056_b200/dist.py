@@ -1,0 +1,257 @@
+"""Multi-GPU S^5: one process per GPU, sample-sort partition + all-to-all.
+
+The reference's fully parallel step (``_ParallelS5Run._phased_step``,
+parallel.py:359-398: sample -> splitters -> classify per shard -> interleaved
+prefix sum -> scatter) lifted to G ranks:
+
+1. every rank samples strings of its shard; the samples are all-gathered and
+   every rank picks the same G-1 *string* splitters (byte prefixes of sampled
+   strings, capped at ``max_splitter_len``) with a (string, global index)
+   tie-break -- so equal strings split by input position and the result stays
+   the stable order;
+2. classify: destination rank of every string (``s5g_partition`` on the GPU);
+3. exchange counts, then the strings' bytes and global input indices with
+   one all-to-all (NCCL over NVLink; ``packed`` mode) -- or only the handles
+   when every rank holds the whole arena (``replicated`` mode, e.g. a suffix
+   set's text);
+4. local S^5 sort of the received strings (they arrive in global input order,
+   so the local stable sort is the global stable order);
+5. boundary-LCP fix-up: each rank gets the last string of the previous
+   non-empty rank and sets ``lcps[0]`` (rank 0 keeps -1) -- the analogue of
+   ``_boundary_lcps`` (parallel.py:447-455) and the merge-boundary recompute
+   of partitioned_merge_sort (parallel.py:989-991).
+
+The concatenation of the ranks' outputs is the reference's output.
+
+Compute is pluggable (``backend``): ``GpuBackend`` runs every step in the
+sm_100a library; tests substitute a CPU backend to run the collective logic
+on ``gloo`` without a GPU.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+LCP_UNDEF = -1
+
+
+@dataclass
+class Shard:
+    """One rank's input: a zero-terminated buffer, handles into it, and the
+    global input index of its first string."""
+
+    buffer: object          # np.ndarray[uint8] (host) -- the backend uploads it
+    handles: np.ndarray     # int64
+    base_index: int
+
+
+@dataclass
+class DistResult:
+    gidx: torch.Tensor      # global input index of every string this rank holds, sorted
+    lcps: torch.Tensor | None
+    arena: object           # the rank-local arena the strings live in
+    handles: torch.Tensor   # sorted handles into `arena`
+    n_total: int
+
+
+def _alltoallv(send: torch.Tensor, send_counts: list[int], recv_counts: list[int], group):
+    """Variable-size all-to-all of a 1-D tensor (NCCL all_to_all_single;
+    point-to-point pairs on backends without all-to-all, e.g. gloo)."""
+    G = dist.get_world_size(group)
+    r = dist.get_rank(group)
+    recv = torch.empty(sum(recv_counts), dtype=send.dtype, device=send.device)
+    if dist.get_backend(group) == "nccl":
+        dist.all_to_all_single(recv, send, recv_counts, send_counts, group=group)
+        return recv
+    so = np.r_[0, np.cumsum(send_counts)]
+    ro = np.r_[0, np.cumsum(recv_counts)]
+    recv[ro[r]:ro[r + 1]] = send[so[r]:so[r + 1]]
+    reqs = []
+    for k in range(1, G):
+        dst, src = (r + k) % G, (r - k) % G
+        if send_counts[dst]:
+            reqs.append(dist.isend(send[so[dst]:so[dst + 1]].contiguous(), dst, group=group))
+        if recv_counts[src]:
+            buf = torch.empty(recv_counts[src], dtype=send.dtype, device=send.device)
+            reqs.append((dist.irecv(buf, src, group=group), buf, ro[src]))
+    for q in reqs:
+        if isinstance(q, tuple):
+            q[0].wait()
+            recv[q[2]:q[2] + len(q[1])] = q[1]
+        else:
+            q.wait()
+    return recv
+
+
+def pick_splitters(samples: list[tuple[bytes, int]], G: int) -> tuple[list[bytes], list[int]]:
+    """G-1 equally spaced splitters from the sorted (string, global index) samples."""
+    samples = sorted(samples)
+    if not samples:
+        return [], []
+    picks = [samples[(k * len(samples)) // G] for k in range(1, G)]
+    return [p[0] for p in picks], [p[1] for p in picks]
+
+
+def distributed_sort(shard: Shard, backend, group=None, samples_per_rank: int = 1024,
+                     max_splitter_len: int = 64, want_lcps: bool = True,
+                     mode: str = "packed", **sort_kw) -> DistResult:
+    """Globally stable sort of the union of all ranks' shards (see module doc)."""
+    G = dist.get_world_size(group)
+    r = dist.get_rank(group)
+    local = backend.prepare(shard)
+    n_local = len(shard.handles)
+    # 1. samples -> identical splitters on every rank
+    mine = backend.sample(local, shard, samples_per_rank, max_splitter_len)
+    gathered: list = [None] * G
+    dist.all_gather_object(gathered, mine, group=group)
+    sp, sp_g = pick_splitters([s for part in gathered for s in part], G)
+    # 2. destination rank of every local string (stable within a destination)
+    dest = backend.partition(local, shard, sp, sp_g)
+    order, counts = backend.group_by_dest(dest, G)
+    # 3. exchange
+    cnt = torch.tensor(counts, dtype=torch.int64, device=backend.comm_device)
+    rcnt = torch.empty_like(cnt)
+    dist.all_to_all_single(rcnt, cnt, group=group) if dist.get_backend(group) == "nccl" else \
+        _gather_counts(cnt, rcnt, group)
+    recv_counts = [int(x) for x in rcnt.tolist()]
+    gidx_send = backend.global_index(shard, order)
+    gidx = _alltoallv(gidx_send, counts, recv_counts, group)
+    if mode == "replicated":
+        h_send = backend.take_handles(local, order)
+        handles = _alltoallv(h_send, counts, recv_counts, group)
+        arena = local
+    elif mode == "packed":
+        payload, byte_counts = backend.pack(local, order, counts)
+        bcnt = torch.tensor(byte_counts, dtype=torch.int64, device=backend.comm_device)
+        rbcnt = torch.empty_like(bcnt)
+        dist.all_to_all_single(rbcnt, bcnt, group=group) if dist.get_backend(group) == "nccl" else \
+            _gather_counts(bcnt, rbcnt, group)
+        rbytes = _alltoallv(payload, byte_counts, [int(x) for x in rbcnt.tolist()], group)
+        arena, handles = backend.unpack(rbytes)
+    else:
+        raise ValueError(f"unknown exchange mode: {mode}")
+    # 4. local sort: received in global input order -> stable local sort
+    perm, lcps = backend.local_sort(arena, handles, want_lcps, **sort_kw)
+    sorted_h = handles[perm]
+    sorted_g = gidx[perm]
+    # 5. LCP at the rank boundary
+    if want_lcps:
+        first = backend.string_bytes(arena, sorted_h[:1]) if len(sorted_h) else None
+        last = backend.string_bytes(arena, sorted_h[-1:]) if len(sorted_h) else None
+        ends: list = [None] * G
+        dist.all_gather_object(ends, last, group=group)
+        prev = next((ends[q] for q in range(r - 1, -1, -1) if ends[q] is not None), None)
+        if len(sorted_h):
+            lcps[0] = LCP_UNDEF if prev is None else _lcp_bytes(prev, first)
+    total = torch.tensor([n_local], dtype=torch.int64, device=backend.comm_device)
+    dist.all_reduce(total, group=group)
+    return DistResult(sorted_g, lcps, arena, sorted_h, int(total.item()))
+
+
+def handle_positions(handles: torch.Tensor, out_h: torch.Tensor) -> torch.Tensor:
+    """Input position of every sorted handle (handles unique; in packed mode
+    they are increasing string starts)."""
+    srt, inv = torch.sort(handles)
+    return inv[torch.searchsorted(srt, out_h)]
+
+
+def _gather_counts(cnt: torch.Tensor, out: torch.Tensor, group) -> None:
+    G = dist.get_world_size(group)
+    r = dist.get_rank(group)
+    rows = [torch.empty_like(cnt) for _ in range(G)]
+    dist.all_gather(rows, cnt, group=group)
+    for q in range(G):
+        out[q] = rows[q][r]
+
+
+def _lcp_bytes(a: bytes, b: bytes) -> int:
+    i = 0
+    while i < len(a) and i < len(b) and a[i] == b[i]:
+        i += 1
+    return i
+
+
+class GpuBackend:
+    """Every compute step in libs5gpu.so (sm_100a); collectives over NCCL."""
+
+    def __init__(self, device=None):
+        self.comm_device = device or torch.device("cuda", torch.cuda.current_device())
+
+    def prepare(self, shard: Shard):
+        from . import device as D
+
+        return D.upload(shard.buffer, shard.handles, self.comm_device)
+
+    def sample(self, ds, shard: Shard, k: int, maxlen: int):
+        n = ds.n
+        if n == 0:
+            return []
+        pos = np.unique(np.linspace(0, n - 1, num=min(k, n)).astype(np.int64))
+        h = ds.handles[torch.as_tensor(pos, device=ds.handles.device)]
+        idx = h[:, None] + torch.arange(maxlen, device=h.device)[None, :]
+        idx = idx.clamp_(max=ds.arena.numel() - 1)
+        chunk = ds.arena[idx].cpu().numpy()
+        out = []
+        for row, p in zip(chunk, pos):
+            z = np.flatnonzero(row == 0)
+            out.append((row[: z[0] if len(z) else maxlen].tobytes(), int(shard.base_index + p)))
+        return out
+
+    def partition(self, ds, shard: Shard, sp, sp_g):
+        from . import device as D
+
+        return D.partition(ds, shard.base_index, sp, sp_g)
+
+    def group_by_dest(self, dest: torch.Tensor, G: int):
+        order = torch.sort(dest, stable=True).indices
+        counts = torch.bincount(dest.long(), minlength=G).tolist()
+        return order, counts
+
+    def global_index(self, shard: Shard, order: torch.Tensor):
+        return order.to(torch.int64) + shard.base_index
+
+    def take_handles(self, ds, order):
+        return ds.handles[order]
+
+    def pack(self, ds, order, counts):
+        from . import device as D
+
+        h = ds.handles[order]
+        lens = D.lengths(D.DeviceStrings(ds.arena, ds.arena_len, h))
+        off = torch.cumsum(lens + 1, 0) - (lens + 1)
+        total = int((lens + 1).sum().item()) if len(lens) else 0
+        payload = D.pack(ds, h, lens, off, total)[:total]
+        bounds = np.r_[0, np.cumsum(counts)]
+        cum = torch.cat([torch.zeros(1, dtype=torch.int64, device=lens.device),
+                         torch.cumsum(lens + 1, 0)])
+        byte_counts = [int(cum[bounds[q + 1]] - cum[bounds[q]]) for q in range(len(counts))]
+        return payload, byte_counts
+
+    def unpack(self, rbytes: torch.Tensor):
+        from . import device as D
+
+        alen = int(rbytes.numel())
+        arena = D.alloc_arena(alen, rbytes.device)
+        arena[:alen] = rbytes
+        zeros = torch.nonzero(rbytes == 0).squeeze(1)
+        starts = torch.cat([torch.zeros(1, dtype=torch.int64, device=rbytes.device),
+                            zeros[:-1] + 1]) if len(zeros) else zeros
+        return D.DeviceStrings(arena, alen, starts), starts
+
+    def local_sort(self, ds, handles, want_lcps, **kw):
+        from . import device as D
+
+        local = D.DeviceStrings(ds.arena, ds.arena_len, handles)
+        out_h, lcps, _ = D.sort(local, want_lcps=want_lcps, **kw)
+        return handle_positions(handles, out_h), lcps
+
+    def string_bytes(self, ds, h1: torch.Tensor) -> bytes:
+        from . import device as D
+
+        one = D.DeviceStrings(ds.arena, ds.arena_len, h1)
+        L = int(D.lengths(one)[0].item())
+        return ds.arena[int(h1[0]): int(h1[0]) + L].cpu().numpy().tobytes()

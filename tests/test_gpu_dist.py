@@ -1,0 +1,59 @@
+"""GPU pieces of the multi-GPU path: the partition / lengths / pack kernels
+against the CPU test backend, and a world_size-1 NCCL run of the whole
+distributed sort (the exchange degenerates, every kernel still runs)."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+from paper_1403_2056_b200 import corpora  # noqa: E402
+from paper_1403_2056_b200 import device as D  # noqa: E402
+from paper_1403_2056_b200.dist import (GpuBackend, Shard, distributed_sort,  # noqa: E402
+                                       handle_positions, pick_splitters)
+from test_dist import CpuBackend  # noqa: E402
+
+
+def test_partition_lengths_pack_match_cpu_backend():
+    buf, hnd = corpora.gen_urls(5000, hosts=40, pool=6)
+    shard = Shard(buf, hnd, 777)
+    cpu, gpu = CpuBackend(), GpuBackend()
+    cpu._handles = hnd
+    ds = gpu.prepare(shard)
+    samples = cpu.sample(buf, shard, 64, 12)
+    for G in (2, 3, 8):
+        sp, g = pick_splitters(samples, G)
+        assert np.array_equal(gpu.partition(ds, shard, sp, g).cpu().numpy(),
+                              cpu.partition(buf, shard, sp, g).numpy())
+    assert np.array_equal(D.lengths(ds).cpu().numpy(), oracle.lengths(buf, hnd))
+    dest = gpu.partition(ds, shard, *pick_splitters(samples, 4))
+    order, counts = gpu.group_by_dest(dest, 4)
+    payload, bc = gpu.pack(ds, order, counts)
+    p2, bc2 = cpu.pack(buf, order.cpu(), counts)
+    assert bc == bc2 and np.array_equal(payload.cpu().numpy(), p2.numpy())
+
+
+def test_distributed_sort_world1_nccl():
+    import torch.distributed as dist
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        for cfg in ("c1_random", "c3_urls"):
+            buf, hnd = corpora.CONFIGS[cfg](1 / 64)
+            res = distributed_sort(Shard(buf, hnd, 0), GpuBackend(), samples_per_rank=64)
+            h, l, _ = oracle.parallel_s5(buf, hnd)
+            want = handle_positions(torch.from_numpy(hnd), torch.from_numpy(h)).numpy()
+            assert np.array_equal(res.gidx.cpu().numpy(), want)
+            assert np.array_equal(res.lcps.cpu().numpy(), l)
+    finally:
+        dist.destroy_process_group()
