@@ -189,6 +189,78 @@ def dist_stats_device(ds, out_h, lcps):
     return D, L
 
 
+def run_dist(args):
+    """N > 1 (torchrun): weak scaling -- every rank owns a 2^24-string shard of
+    the workload (seed + rank); one step is the full multi-GPU sort (sample,
+    partition, NCCL all-to-all, local S^5, boundary LCP), timed on the device
+    and reported as the max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1403_2056_b200 import _lib
+    from paper_1403_2056_b200 import corpora
+    from paper_1403_2056_b200 import device as DV
+    from paper_1403_2056_b200.dist import GpuBackend, Shard, distributed_sort
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl")
+    dev = torch.device("cuda", local)
+    gen = {"c1_random": lambda s: corpora.gen_random(int(1_000_000 * args.scale), s),
+           "c2_dna": lambda s: corpora.gen_dna(int((1 << 24) * args.scale), 100, s),
+           "c3_urls": lambda s: corpora.gen_urls(int((1 << 23) * args.scale), s),
+           "c5_nodup": lambda s: corpora.gen_nodup(int((1 << 28) * args.scale), s)}[args.config]
+    seed0 = {"c1_random": 0, "c2_dna": 1, "c3_urls": 2, "c5_nodup": 4}[args.config]
+    buf, hnd = gen(seed0 + rank)
+    n = len(hnd)
+    ds = DV.upload(buf, hnd, dev)
+    shard = Shard(ds, hnd, rank * n)
+    be = GpuBackend(dev)
+
+    def step():
+        return distributed_sort(shard, be, want_lcps=True)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    l0 = _lib.launch_count()
+    with ClockSampler(local) as clk:
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.steps):
+            res = step()
+        e1.record()
+        torch.cuda.synchronize()
+        dist.barrier()
+    ms = torch.tensor([e0.elapsed_time(e1)], device=dev)
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms_step = float(ms.item()) / args.steps
+    launches = _lib.launch_count() - l0
+    total = res.n_total
+    peak, peak_src = hbm_peak()
+    line = {
+        "metric": METRIC, "value": total / (ms_step / 1000.0), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+        "data": "synthetic",
+        "config": {"workload": args.config, "n_per_rank": n, "n_total": total,
+                   "parallelism": f"dp{world} (sample-sort partition + NCCL all-to-all)",
+                   "l2": "inputs larger than L2 (arena > 126 MB), no flush"},
+        "roofline": {"bound": "hbm", "kernel": "whole multi-GPU sort", "achieved": None,
+                     "peak": peak, "unit": "GB/s", "frac": None, "traffic": None,
+                     "peak_source": peak_src},
+        "gpu_launches": int(launches), "clocks": clk.summary(), "cpu_baseline": None,
+        "e2e": None,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+    return 0
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -330,6 +402,8 @@ def main(argv=None):
     args = ap.parse_args(argv)
     if args.impl == "reference":
         return run_reference(args)
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        return run_dist(args)
     return run_ours(args)
 
 

@@ -184,6 +184,8 @@ class GpuBackend:
     def prepare(self, shard: Shard):
         from . import device as D
 
+        if isinstance(shard.buffer, D.DeviceStrings):  # already resident in HBM
+            return shard.buffer
         return D.upload(shard.buffer, shard.handles, self.comm_device)
 
     def sample(self, ds, shard: Shard, k: int, maxlen: int):
