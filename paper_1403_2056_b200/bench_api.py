@@ -1,0 +1,26 @@
+"""Registration with the reference harness's plugin API
+(``strsort.bench.register_algorithm``, bench.py:151-152)."""
+
+from __future__ import annotations
+
+from .parallel import parallel_s5
+from .ssss import s5_sort
+
+
+def _algo_gpu_s5(sset, threads, seed, stats):
+    return s5_sort(sset, seed=seed, stats=stats)
+
+
+def _algo_gpu_ps5(sset, threads, seed, stats):
+    return parallel_s5(sset, p=threads, seed=seed, stats=stats)
+
+
+def register_with_strsort() -> bool:
+    """Register ``gpu-s5`` and ``gpu-ps5``; False when strsort is absent."""
+    try:
+        import strsort.bench as B
+    except ImportError:
+        return False
+    B.register_algorithm("gpu-s5", _algo_gpu_s5)
+    B.register_algorithm("gpu-ps5", _algo_gpu_ps5)
+    return True

@@ -76,3 +76,15 @@ def test_corpora_shapes():
     s = StringSet(buf.tobytes(), h)
     strs = s.strings()
     assert len(set(strs)) == 5000 and all(32 <= len(x) <= 200 for x in strs)
+
+
+def test_register_with_reference_harness():
+    import sys
+    sys.path.insert(0, "/root/reference/pkg/src")
+    try:
+        import strsort.bench as B
+    except ImportError:
+        pytest.skip("reference not importable here")
+    from paper_1403_2056_b200.bench_api import register_with_strsort
+    assert register_with_strsort()
+    assert "gpu-s5" in B.ALGORITHMS and "gpu-ps5" in B.ALGORITHMS
