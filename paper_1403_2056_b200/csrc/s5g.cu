@@ -130,9 +130,11 @@ __global__ void __launch_bounds__(CLS_NT) k_classify(
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ __align__(8) uint64_t bar;
     __shared__ unsigned fetched;
-    uint64_t* tree = reinterpret_cast<uint64_t*>(smem);            // VMAX+1
-    uint32_t* hist = reinterpret_cast<uint32_t*>(tree + VMAX + 1);  // NBMAX+1
-    uint16_t* eqb = reinterpret_cast<uint16_t*>(hist + NBMAX + 1);  // VMAX+1 (equal only)
+    // tree (level order) | per-tile histogram as packed u16 pairs (a tile has
+    // < 65536 strings) | eq-bucket table (equal variant only)
+    uint64_t* tree = reinterpret_cast<uint64_t*>(smem);                  // VMAX+1
+    uint32_t* hist = reinterpret_cast<uint32_t*>(tree + VMAX + 1);        // (NBMAX+1)/2
+    uint16_t* eqb = reinterpret_cast<uint16_t*>(hist + (NBMAX + 1) / 2);  // VMAX+1
     const int t = blockIdx.x;
     const StepDev sd = steps[tile_step[t]];
     const int ti = t - (int)sd.tile0;
@@ -150,14 +152,14 @@ __global__ void __launch_bounds__(CLS_NT) k_classify(
             bulk_g2s(reinterpret_cast<uint8_t*>(tree) + off, src + off,
                      min(32768u, tree_bytes - off), &bar);
     }
-    for (int b = threadIdx.x; b < nb; b += CLS_NT) hist[b] = 0;
+    for (int b = threadIdx.x; b < (nb + 1) / 2; b += CLS_NT) hist[b] = 0;
     if (VARIANT == S5G_VARIANT_EQUAL)
         for (int i = threadIdx.x; i <= v; i += CLS_NT) eqb[i] = eqb_g[sd.tree_off + i];
     __syncthreads();
     mbar_wait(&bar, 0);
     const int lane = threadIdx.x & 31;
     unsigned my_fetch = 0;
-    constexpr int U = 4;
+    constexpr int U = 8;
     for (int64_t base = beg; base < end; base += (int64_t)CLS_NT * U) {
         uint64_t key[U];
         bool ok[U];
@@ -186,14 +188,15 @@ __global__ void __launch_bounds__(CLS_NT) k_classify(
             if (ok[u]) {
                 bid[i] = (uint16_t)b[u];
                 uint32_t peers = __match_any_sync(mask, b[u]);
-                if (lane == __ffs(peers) - 1) atomicAdd(&hist[b[u]], (uint32_t)__popc(peers));
+                if (lane == __ffs(peers) - 1)
+                    atomicAdd(&hist[b[u] >> 1], (uint32_t)__popc(peers) << (16 * (b[u] & 1)));
             }
         }
     }
     if (my_fetch) atomicAdd(&fetched, my_fetch);
     __syncthreads();
     uint32_t* row = cnt + sd.cnt_off + (int64_t)ti * nb;
-    for (int b = threadIdx.x; b < nb; b += CLS_NT) row[b] = hist[b];
+    for (int b = threadIdx.x; b < nb; b += CLS_NT) row[b] = (hist[b >> 1] >> (16 * (b & 1))) & 0xffffu;
     if (threadIdx.x == 0 && fetched) atomicAdd(&ctr->fetches, (unsigned long long)fetched);
 }
 
@@ -661,20 +664,34 @@ static size_t carve(Workspace* w, uint8_t* base, int64_t n, int64_t t_medium) {
 
 
 static size_t smem_sample(int P, int v) { return (size_t)P * 8 + (size_t)3 * (v + 1) * 2 + 16; }
-static constexpr size_t SMEM_CLS =
-    (size_t)(VMAX + 1) * 8 + (size_t)(NBMAX + 1) * 4 + (size_t)(VMAX + 1) * 2;
+static constexpr size_t SMEM_CLS_UNROLL = (size_t)(VMAX + 1) * 8 + (size_t)(NBMAX + 1) / 2 * 4;
+static constexpr size_t SMEM_CLS = SMEM_CLS_UNROLL + (size_t)(VMAX + 1) * 2;
 static constexpr size_t SMEM_SC = (size_t)(NBMAX + 1) * 4 + (size_t)SC_R * 32 * 2 +
                                   (size_t)4 * SC_SUB * 2;
 
 static int set_smem_attrs() {
-    static bool done = false;
-    if (done) return 0;
+    // per device: kernel attributes + the byte-PEXT table of the finishers
+    static unsigned long long done_mask = 0;
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    if (dev < 64 && (done_mask >> dev & 1ull)) return 0;
+    {
+        static uint8_t lut[256 * 256];
+        for (int m = 0; m < 256; m++)
+            for (int x = 0; x < 256; x++) {
+                int r = 0, k = 0;
+                for (int b = 0; b < 8; b++)
+                    if (m >> b & 1) r |= ((x >> b) & 1) << k++;
+                lut[m * 256 + x] = (uint8_t)r;
+            }
+        CK(cudaMemcpyToSymbol(g_pext8, lut, sizeof(lut)));
+    }
     CK(cudaFuncSetAttribute(k_sample_tree, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)smem_sample(2 * (VMAX + 1), VMAX)));
     CK(cudaFuncSetAttribute(k_select_only, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)smem_sample(2 * (VMAX + 1), VMAX)));
     CK(cudaFuncSetAttribute(k_classify<S5G_VARIANT_UNROLL>,
-                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_CLS));
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_CLS_UNROLL));
     CK(cudaFuncSetAttribute(k_classify<S5G_VARIANT_EQUAL>,
                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_CLS));
     CK(cudaFuncSetAttribute(k_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_SC));
@@ -685,7 +702,7 @@ static int set_smem_attrs() {
     CK(cudaFuncSetAttribute(k_cta_sort<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)sizeof(CtaSortSmem<8>)));
 
-    done = true;
+    if (dev < 64) done_mask |= 1ull << dev;
     return 0;
 }
 
@@ -866,7 +883,7 @@ static int sort_impl_body(const s5g_sort_args* a) {
             }
             if (a->variant == S5G_VARIANT_UNROLL)
                 PROF(K_CLASSIFY, round_elems, cls_bytes,
-                     (k_classify<S5G_VARIANT_UNROLL><<<ntiles, CLS_NT, SMEM_CLS, st>>>(
+                     (k_classify<S5G_VARIANT_UNROLL><<<ntiles, CLS_NT, SMEM_CLS_UNROLL, st>>>(
                          w.steps, w.tile_step, a->arena, a->arena_len, hX, kX, w.bid, w.cnt,
                          w.tree, w.eqb, w.ctr)));
             else

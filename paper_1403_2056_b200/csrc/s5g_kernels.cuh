@@ -17,7 +17,7 @@
 namespace s5g {
 
 constexpr int TILE = 32768;     // elements per classify / scatter CTA
-constexpr int CLS_NT = 1024;
+constexpr int CLS_NT = 512;
 constexpr int SC_NT = 512;
 constexpr int SC_ITEMS = 4;
 constexpr int SC_SUB = SC_NT * SC_ITEMS;  // 4096-element stable sub-tiles

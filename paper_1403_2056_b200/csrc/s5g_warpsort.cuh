@@ -1,212 +1,29 @@
-// s5g_warpsort.cuh -- one warp finishes one segment of <= 32*ITEMS strings.
+// s5g_warpsort.cuh -- register-resident finishers for segments of <= 2048
+// strings: the GPU stand-in for the reference's leaves (caching MKQS
+// mkqs.py:196-253, LCP insertion sort basecase.py:67-116).
 //
-// The GPU stand-in for the reference's leaves (caching MKQS mkqs.py:196-253,
-// LCP insertion sort basecase.py:67-116) once the device-wide S^5 steps have
-// cut the input into segments of at most 256 strings.  Lane l holds slots
-// l*ITEMS .. l*ITEMS+ITEMS-1 in registers: (word, group<<8 | tag).  A round is
-// a bitonic network over (group, word, tag) -- in-lane stages for distances
-// below ITEMS, shuffle stages above -- followed by word-parallel LCPs at
-// every word change (XOR/clz), terminator-equal runs finalised, and runs of
-// equal non-terminated words re-keyed one word deeper as the next round's
-// groups.  A group id is the slot its run starts at, so finished slots
-// (group = own slot) never move.  No shared-memory barriers: the latency of
-// the re-keying gathers is hidden by the other warps of the SM.
+// A round sorts the active slots by (group, 8-byte word at the round's depth,
+// tag) with a bitonic network held in registers (in-lane stages below 8 /
+// IT, shuffle stages below 256, shared-memory stages above), then writes the
+// LCPs at every word change from XOR/clz (shared_chars, strset.py:194-206),
+// finalises terminator-equal runs, and re-keys runs of equal non-terminated
+// words one word deeper as the next round's groups.  A group id is the slot
+// its run starts at, so finished slots (group = own slot) never move, and
+// the tag (position in the segment) keeps ties in input order: stable.
+//
+// Compare-exchange cost is the bottleneck (ncu: ~45% of the instructions in
+// a 3-way comparator), so whenever the varying bits of the round's words fit,
+// a slot is ONE u64: group | PEXT(word, varying-bit mask) | tag, compared and
+// moved as a single value; the words stay in shared memory by tag.  The
+// PEXT runs byte-wise through a 256x256 lookup table in global memory (L1).
 #pragma once
 #include "s5g_kernels.cuh"
 
 namespace s5g {
 
-constexpr int WS_NT = 256;  // 8 warps per CTA, one segment per warp
+__device__ uint8_t g_pext8[256 * 256];  // [mask * 256 + byte] = pext(byte, mask)
 
-template <int ITEMS>
-struct WarpLists {
-    static constexpr int CAP = 32 * ITEMS;
-};
-
-__device__ __forceinline__ bool ws_less(uint64_t ka, uint32_t ma, uint64_t kb, uint32_t mb) {
-    const uint32_t ga = ma >> 8 & 0xff, gb = mb >> 8 & 0xff;
-    if (ga != gb) return ga < gb;
-    if (ka != kb) return ka < kb;
-    return (ma & 0xff) < (mb & 0xff);
-}
-
-template <int ITEMS>
-__device__ __forceinline__ void ws_bitonic(uint64_t (&key)[ITEMS], uint32_t (&meta)[ITEMS],
-                                           int lane) {
-    constexpr int P = 32 * ITEMS;
-#pragma unroll
-    for (int k = 2; k <= P; k <<= 1) {
-#pragma unroll
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            if (j < ITEMS) {
-#pragma unroll
-                for (int e = 0; e < ITEMS; e++) {
-                    const int f = e ^ j;
-                    if (f > e) {
-                        const int i = lane * ITEMS + e;
-                        const bool up = (i & k) == 0;
-                        if (ws_less(key[f], meta[f], key[e], meta[e]) == up) {
-                            uint64_t tk = key[e]; key[e] = key[f]; key[f] = tk;
-                            uint32_t tm = meta[e]; meta[e] = meta[f]; meta[f] = tm;
-                        }
-                    }
-                }
-            } else {
-                const int lx = j / ITEMS;
-#pragma unroll
-                for (int e = 0; e < ITEMS; e++) {
-                    const uint64_t ok = __shfl_xor_sync(0xffffffffu, key[e], lx);
-                    const uint32_t om = __shfl_xor_sync(0xffffffffu, meta[e], lx);
-                    const int i = lane * ITEMS + e;
-                    const bool up = (i & k) == 0;
-                    const bool lower = (i & j) == 0;  // this slot keeps the smaller if up
-                    const bool other_less = ws_less(ok, om, key[e], meta[e]);
-                    if (other_less == (lower == up)) {
-                        key[e] = ok;
-                        meta[e] = om;
-                    }
-                }
-            }
-        }
-    }
-}
-
-template <int ITEMS>
-__global__ void __launch_bounds__(WS_NT) k_warp_sort(
-    const SegDev* __restrict__ segs, int64_t nsegs, const int64_t* __restrict__ hA,
-    const uint64_t* __restrict__ kA, const int64_t* __restrict__ hB,
-    const uint64_t* __restrict__ kB, const uint8_t* __restrict__ arena, int64_t alen,
-    int64_t* __restrict__ out_h, int64_t* __restrict__ lcps, Counters* __restrict__ ctr) {
-    constexpr int CAP = 32 * ITEMS;
-    __shared__ int64_t s_h[WS_NT / 32][CAP];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int64_t gw = (int64_t)blockIdx.x * (WS_NT / 32) + w;
-    if (gw >= nsegs) return;  // whole warp
-    const SegDev sg = segs[gw];
-    const int m = sg.n;
-    const int64_t lo = sg.lo;
-    const int64_t* sh = (sg.flags & SEG_IN_B) ? hB : hA;
-    const uint64_t* sk = (sg.flags & SEG_IN_B) ? kB : kA;
-    const bool valid = sg.flags & SEG_KEYS_VALID;
-    int64_t* wh = s_h[w];
-    int64_t depth = sg.depth;
-    unsigned fetches = 0;
-    uint64_t key[ITEMS];
-    uint32_t meta[ITEMS];  // bit 16 active | group << 8 | tag
-    // coalesced handle loads into the warp's staging area
-#pragma unroll
-    for (int e = 0; e < ITEMS; e++) {
-        const int i = e * 32 + lane;
-        if (i < m) wh[i] = sh[lo + i];
-    }
-    __syncwarp();
-#pragma unroll
-    for (int e = 0; e < ITEMS; e++) {
-        const int i = lane * ITEMS + e;
-        if (i < m) {
-            key[e] = valid ? sk[lo + i] : load_key(arena, alen, wh[i], depth);
-            meta[e] = (1u << 16) | (0u << 8) | (uint32_t)i;
-        } else {
-            key[e] = ~0ull;
-            meta[e] = ((uint32_t)i << 8) | (uint32_t)i;  // own group, stays last
-        }
-    }
-    if (!valid) fetches += min(ITEMS, max(0, m - lane * ITEMS));
-    for (;;) {
-        ws_bitonic<ITEMS>(key, meta, lane);
-        // predecessor / successor slots
-        const uint64_t prev_last = __shfl_up_sync(0xffffffffu, key[ITEMS - 1], 1);
-        bool brk[ITEMS];
-#pragma unroll
-        for (int e = 0; e < ITEMS; e++) {
-            const int i = lane * ITEMS + e;
-            const bool act = meta[e] >> 16 & 1;
-            const int grp = meta[e] >> 8 & 0xff;
-            brk[e] = true;
-            if (act && i != grp) {
-                const uint64_t pk = e ? key[e - 1] : prev_last;
-                if (pk != key[e]) {
-                    if (lcps) lcps[lo + i] = depth + (__clzll(pk ^ key[e]) >> 3);
-                } else {
-                    brk[e] = false;
-                    const int tpv = term_pos(key[e]);
-                    if (lcps && tpv < WORD) lcps[lo + i] = depth + tpv;
-                }
-            }
-        }
-        // next slot's break flag (first item of the next lane)
-        const bool next_brk0 = __shfl_down_sync(0xffffffffu, brk[0], 1);
-        const bool next_act0 = __shfl_down_sync(0xffffffffu, meta[0] >> 16 & 1u, 1);
-        bool keep[ITEMS];
-        bool any = false;
-        uint32_t run = 0;  // 1 + start slot of the latest kept run start in this lane
-#pragma unroll
-        for (int e = 0; e < ITEMS; e++) {
-            const int i = lane * ITEMS + e;
-            const bool act = meta[e] >> 16 & 1;
-            bool nb, na;
-            if (e + 1 < ITEMS) {
-                nb = brk[e + 1];
-                na = meta[e + 1] >> 16 & 1;
-            } else {
-                nb = next_brk0;
-                na = next_act0 && lane < 31;
-            }
-            keep[e] = act && term_pos(key[e]) == WORD && (!brk[e] || (na && !nb));
-            any |= keep[e];
-            if (keep[e] && brk[e]) run = i + 1;
-        }
-        if (!__any_sync(0xffffffffu, any) || depth > alen) break;  // alen: corrupt-input guard
-        // inclusive max-scan of run starts across lanes
-        uint32_t incl = run;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl = max(incl, y);
-        }
-        uint32_t cur = __shfl_up_sync(0xffffffffu, incl, 1);
-        if (lane == 0) cur = 0;
-        depth += WORD;
-#pragma unroll
-        for (int e = 0; e < ITEMS; e++) {
-            const int i = lane * ITEMS + e;
-            if (keep[e] && brk[e]) cur = i + 1;
-            const uint32_t tag = meta[e] & 0xff;
-            if (keep[e]) {
-                meta[e] = (1u << 16) | ((cur - 1) << 8) | tag;
-            } else {
-                meta[e] = ((uint32_t)i << 8) | tag;  // finished: own group, inactive
-            }
-        }
-#pragma unroll
-        for (int e = 0; e < ITEMS; e++)
-            if (meta[e] >> 16 & 1) {
-                key[e] = load_key(arena, alen, wh[meta[e] & 0xff], depth);
-                fetches++;
-            }
-    }
-#pragma unroll
-    for (int e = 0; e < ITEMS; e++) {
-        const int i = lane * ITEMS + e;
-        if (i < m) out_h[lo + i] = wh[meta[e] & 0xff];
-    }
-    fetches = __reduce_add_sync(0xffffffffu, fetches);
-    if (lane == 0) {
-        if (fetches) atomicAdd(&ctr->seg_fetches, (unsigned long long)fetches);
-        atomicAdd(&ctr->small_elems, (unsigned long long)m);
-    }
-}
-
-}  // namespace s5g
-
-namespace s5g {
-
-// ---------------------------------------------------------------------------
-// CTA form: W warps x 256 slots (8 per lane) finish one segment of up to
-// 256*W strings.  Distances below 256 run in registers / shuffles exactly as
-// in k_warp_sort; distances >= 256 cross warps through shared memory.
-// meta = active << 22 | group << 11 | tag (11-bit slots).
-
+// meta = active << 22 | group << 11 | tag   (11-bit slots and tags)
 __device__ __forceinline__ bool cs_less(uint64_t ka, uint32_t ma, uint64_t kb, uint32_t mb) {
     const uint32_t ga = ma >> 11 & 0x7ff, gb = mb >> 11 & 0x7ff;
     if (ga != gb) return ga < gb;
@@ -214,20 +31,74 @@ __device__ __forceinline__ bool cs_less(uint64_t ka, uint32_t ma, uint64_t kb, u
     return (ma & 0x7ff) < (mb & 0x7ff);
 }
 
-template <int W>
-struct CtaSortSmem {
-    int64_t h[256 * W];           // handle by tag
-    uint64_t xk[256 * W];
-    uint32_t xm[256 * W];
-    uint16_t ord[256 * W];        // tag at slot (group mode)
-    uint16_t gs[128 * W], ge[128 * W];  // group mode: first / last slot of each run
-    uint64_t last_key[W];
-    uint32_t first_brk[W], first_act[W], wmax[W], wcnt[W];
+struct Pext {
+    uint64_t V;
+    int cb;
+    int sh[8];
 };
 
-// Bitonic network on one warp's 32*IT slots, comparator cs_less.
+__device__ __forceinline__ Pext pext_setup(uint64_t V) {
+    Pext p;
+    p.V = V;
+    p.cb = __popcll(V);
+    int acc = 0;
+#pragma unroll
+    for (int b = 0; b < 8; b++) {
+        p.sh[b] = acc;
+        acc += __popc((uint32_t)(V >> (8 * b)) & 255u);
+    }
+    return p;
+}
+
+__device__ __forceinline__ uint64_t pext_key(uint64_t x, const Pext& p) {
+    uint64_t c = 0;
+#pragma unroll
+    for (int b = 0; b < 8; b++) {
+        const uint32_t m = (uint32_t)(p.V >> (8 * b)) & 255u;
+        if (m) c |= (uint64_t)__ldg(&g_pext8[m * 256 + ((uint32_t)(x >> (8 * b)) & 255u)]) << p.sh[b];
+    }
+    return c;
+}
+
+__device__ __forceinline__ void cex_u64(uint64_t& a, uint64_t& b, bool up) {
+    const uint64_t lo = min(a, b), hi = max(a, b);
+    a = up ? lo : hi;
+    b = up ? hi : lo;
+}
+
+// ---------------------------------------------------------------------------
+// warp-level networks over 32*IT slots (slot = lane*IT + e)
+
 template <int IT>
-__device__ __forceinline__ void cs_bitonic(uint64_t (&key)[IT], uint32_t (&meta)[IT], int lane) {
+__device__ __forceinline__ void warp_bitonic_u64(uint64_t (&c)[IT], int lane) {
+    constexpr int P = 32 * IT;
+#pragma unroll
+    for (int k = 2; k <= P; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j < IT) {
+#pragma unroll
+                for (int e = 0; e < IT; e++) {
+                    const int f = e ^ j;
+                    if (f > e) cex_u64(c[e], c[f], ((lane * IT + e) & k) == 0);
+                }
+            } else {
+                const int lx = j / IT;
+#pragma unroll
+                for (int e = 0; e < IT; e++) {
+                    const uint64_t o = __shfl_xor_sync(0xffffffffu, c[e], lx);
+                    const int i = lane * IT + e;
+                    const bool keep_min = ((i & j) == 0) == ((i & k) == 0);
+                    c[e] = keep_min ? min(c[e], o) : max(c[e], o);
+                }
+            }
+        }
+    }
+}
+
+template <int IT>
+__device__ __forceinline__ void warp_bitonic_generic(uint64_t (&key)[IT], uint32_t (&meta)[IT],
+                                                     int lane) {
     constexpr int P = 32 * IT;
 #pragma unroll
     for (int k = 2; k <= P; k <<= 1) {
@@ -263,32 +134,76 @@ __device__ __forceinline__ void cs_bitonic(uint64_t (&key)[IT], uint32_t (&meta)
     }
 }
 
-// One warp finishes one run of gn <= 32*IT strings (slots g0.. of the
-// segment) that share `depth` characters: re-key one word deeper, sort,
-// LCPs, recurse on equal runs -- all in registers.  Writes the final tag
-// order back to ord[g0 .. g0+gn).
+__device__ __forceinline__ uint64_t warp_or64(uint64_t x) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) x |= __shfl_xor_sync(0xffffffffu, x, o);
+    return x;
+}
+__device__ __forceinline__ uint64_t warp_and64(uint64_t x) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) x &= __shfl_xor_sync(0xffffffffu, x, o);
+    return x;
+}
+
+// One warp finishes one run of gn <= 32*IT strings that occupy slots
+// g0 .. g0+gn-1 of the segment and share `depth` characters.  On entry the
+// words at `depth` are in key[] (slot order = ord[g0 + i]) when have_keys,
+// else they are fetched.  Writes LCPs (absolute depths) for the run's
+// interior and the final tag order back to ord[g0 ..].
 template <int IT>
-__device__ void cs_finish_group(const int64_t* __restrict__ hbt, uint16_t* __restrict__ ord,
-                                int g0, int gn, int64_t depth, const uint8_t* __restrict__ arena,
-                                int64_t alen, int64_t* __restrict__ lcp_seg, unsigned& fetches,
-                                int lane) {
-    uint64_t key[IT];
+__device__ void warp_finish(const int64_t* __restrict__ hbt, uint16_t* __restrict__ ord,
+                            uint64_t* __restrict__ kb, int g0, int gn, int64_t depth,
+                            bool have_keys, uint64_t (&key)[IT], const uint8_t* __restrict__ arena,
+                            int64_t alen, int64_t* __restrict__ lcp_seg, unsigned& fetches,
+                            int lane) {
     uint32_t meta[IT];
 #pragma unroll
     for (int e = 0; e < IT; e++) {
         const int i = lane * IT + e;
         if (i < gn) {
             const uint32_t tag = ord[g0 + i];
-            key[e] = load_key(arena, alen, hbt[tag], depth);
+            if (!have_keys) {
+                key[e] = load_key(arena, alen, hbt[tag], depth);
+                fetches++;
+            }
             meta[e] = (1u << 22) | tag;
-            fetches++;
         } else {
             key[e] = ~0ull;
             meta[e] = (uint32_t)i << 11;
         }
     }
     for (;;) {
-        cs_bitonic<IT>(key, meta, lane);
+        // ---- sort the active slots by (group, word, tag) ------------------
+        uint64_t o = 0, a = ~0ull;
+#pragma unroll
+        for (int e = 0; e < IT; e++)
+            if (meta[e] >> 22 & 1) { o |= key[e]; a &= key[e]; }
+        const Pext px = pext_setup(warp_or64(o) ^ warp_and64(a));
+        if (px.cb <= 45) {
+            uint64_t c[IT];
+#pragma unroll
+            for (int e = 0; e < IT; e++) {
+                const uint32_t tag = meta[e] & 0x7ff;
+                if (meta[e] >> 22 & 1) {
+                    kb[tag] = key[e];
+                    c[e] = ((uint64_t)(meta[e] >> 11 & 0xff) << 56) | (pext_key(key[e], px) << 11) | tag;
+                } else {
+                    c[e] = ((uint64_t)(lane * IT + e) << 56) | tag;
+                }
+            }
+            __syncwarp();
+            warp_bitonic_u64<IT>(c, lane);
+#pragma unroll
+            for (int e = 0; e < IT; e++) {
+                const uint32_t tag = (uint32_t)c[e] & 0x7ff;
+                if (meta[e] >> 22 & 1) key[e] = kb[tag];
+                meta[e] = (meta[e] & ~0x7ffu) | tag;
+            }
+            __syncwarp();
+        } else {
+            warp_bitonic_generic<IT>(key, meta, lane);
+        }
+        // ---- LCPs at word changes, run breaks -----------------------------
         const uint64_t prev_last = __shfl_up_sync(0xffffffffu, key[IT - 1], 1);
         bool brk[IT];
 #pragma unroll
@@ -331,9 +246,9 @@ __device__ void cs_finish_group(const int64_t* __restrict__ hbt, uint16_t* __res
         if (!__any_sync(0xffffffffu, any) || depth > alen) break;  // alen: corrupt-input guard
         uint32_t incl = run;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl = max(incl, y);
+        for (int o2 = 1; o2 < 32; o2 <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o2);
+            if (lane >= o2) incl = max(incl, y);
         }
         uint32_t cur = __shfl_up_sync(0xffffffffu, incl, 1);
         if (lane == 0) cur = 0;
@@ -359,13 +274,199 @@ __device__ void cs_finish_group(const int64_t* __restrict__ hbt, uint16_t* __res
     }
 }
 
+// ---------------------------------------------------------------------------
+// k_warp_sort: one warp per segment of <= 32*ITEMS strings
+
+constexpr int WS_NT = 256;  // 8 warps per CTA, one segment per warp
+
+template <int ITEMS>
+__global__ void __launch_bounds__(WS_NT) k_warp_sort(
+    const SegDev* __restrict__ segs, int64_t nsegs, const int64_t* __restrict__ hA,
+    const uint64_t* __restrict__ kA, const int64_t* __restrict__ hB,
+    const uint64_t* __restrict__ kB, const uint8_t* __restrict__ arena, int64_t alen,
+    int64_t* __restrict__ out_h, int64_t* __restrict__ lcps, Counters* __restrict__ ctr) {
+    constexpr int CAP = 32 * ITEMS;
+    __shared__ int64_t s_h[WS_NT / 32][CAP];
+    __shared__ uint64_t s_k[WS_NT / 32][CAP];
+    __shared__ uint16_t s_o[WS_NT / 32][CAP];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t gw = (int64_t)blockIdx.x * (WS_NT / 32) + w;
+    if (gw >= nsegs) return;  // whole warp
+    const SegDev sg = segs[gw];
+    const int m = sg.n;
+    const int64_t lo = sg.lo;
+    const int64_t* sh = (sg.flags & SEG_IN_B) ? hB : hA;
+    const uint64_t* sk = (sg.flags & SEG_IN_B) ? kB : kA;
+    const bool valid = sg.flags & SEG_KEYS_VALID;
+    int64_t* wh = s_h[w];
+    uint16_t* wo = s_o[w];
+    unsigned fetches = 0;
+#pragma unroll
+    for (int e = 0; e < ITEMS; e++) {
+        const int i = e * 32 + lane;
+        if (i < m) {
+            wh[i] = sh[lo + i];
+            wo[i] = (uint16_t)i;
+        }
+    }
+    __syncwarp();
+    uint64_t key[ITEMS];
+    if (valid) {
+#pragma unroll
+        for (int e = 0; e < ITEMS; e++) {
+            const int i = lane * ITEMS + e;
+            key[e] = i < m ? sk[lo + i] : ~0ull;
+        }
+    }
+    warp_finish<ITEMS>(wh, wo, s_k[w], 0, m, sg.depth, valid, key, arena, alen,
+                       lcps ? lcps + lo : nullptr, fetches, lane);
+    __syncwarp();
+#pragma unroll
+    for (int e = 0; e < ITEMS; e++) {
+        const int i = e * 32 + lane;
+        if (i < m) out_h[lo + i] = wh[wo[i]];
+    }
+    fetches = __reduce_add_sync(0xffffffffu, fetches);
+    if (lane == 0) {
+        if (fetches) atomicAdd(&ctr->seg_fetches, (unsigned long long)fetches);
+        atomicAdd(&ctr->small_elems, (unsigned long long)m);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// k_cta_sort: W warps x 256 slots (8 per lane) finish one segment of up to
+// 256*W strings.  The first round(s) run CTA-wide; once every remaining run
+// has <= 256 strings, each run goes to one warp (warp_finish).
+
+template <int W>
+struct CtaSortSmem {
+    int64_t h[256 * W];           // handle by tag
+    uint64_t kb[256 * W];         // word by tag (composite rounds, warp runs)
+    uint64_t xk[256 * W];         // cross-warp exchange
+    uint32_t xm[256 * W];
+    uint16_t ord[256 * W];        // tag at slot
+    uint16_t gs[128 * W], ge[128 * W];  // first / last slot of each remaining run
+    uint64_t red[2 * W];
+    uint64_t last_key[W];
+    uint32_t first_brk[W], first_act[W], wmax[W], wcnt[W];
+};
+
+template <int J>
+__device__ __forceinline__ void cta_inlane(uint64_t (&c)[8], int base, int k) {
+#pragma unroll
+    for (int e = 0; e < 8; e++) {
+        const int f = e ^ J;
+        if (f > e) cex_u64(c[e], c[f], ((base + e) & k) == 0);
+    }
+}
+
+template <int W>
+__device__ void cta_bitonic_u64(uint64_t (&c)[8], int base, CtaSortSmem<W>& S) {
+    constexpr int P = 256 * W;
+#pragma unroll 1
+    for (int k = 2; k <= P; k <<= 1) {
+#pragma unroll 1
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j == 1) {
+                cta_inlane<1>(c, base, k);
+            } else if (j == 2) {
+                cta_inlane<2>(c, base, k);
+            } else if (j == 4) {
+                cta_inlane<4>(c, base, k);
+            } else if (j < 256) {
+                const int lx = j / 8;
+#pragma unroll
+                for (int e = 0; e < 8; e++) {
+                    const uint64_t o = __shfl_xor_sync(0xffffffffu, c[e], lx);
+                    const int i = base + e;
+                    const bool keep_min = ((i & j) == 0) == ((i & k) == 0);
+                    c[e] = keep_min ? min(c[e], o) : max(c[e], o);
+                }
+            } else {
+#pragma unroll
+                for (int e = 0; e < 8; e++) S.xk[base + e] = c[e];
+                __syncthreads();
+#pragma unroll
+                for (int e = 0; e < 8; e++) {
+                    const int i = base + e;
+                    const uint64_t o = S.xk[i ^ j];
+                    const bool keep_min = ((i & j) == 0) == ((i & k) == 0);
+                    c[e] = keep_min ? min(c[e], o) : max(c[e], o);
+                }
+                __syncthreads();
+            }
+        }
+    }
+}
+
+template <int W>
+__device__ void cta_bitonic_generic(uint64_t (&key)[8], uint32_t (&meta)[8], int base,
+                                    CtaSortSmem<W>& S) {
+    constexpr int P = 256 * W;
+#pragma unroll 1
+    for (int k = 2; k <= P; k <<= 1) {
+#pragma unroll 1
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j < 8) {
+#pragma unroll
+                for (int e = 0; e < 8; e++) {
+#pragma unroll
+                    for (int jj = 1; jj < 8; jj <<= 1) {
+                        if (jj != j) continue;
+                        const int f = e ^ jj;
+                        if (f > e) {
+                            const bool up = ((base + e) & k) == 0;
+                            if (cs_less(key[f], meta[f], key[e], meta[e]) == up) {
+                                uint64_t tk = key[e]; key[e] = key[f]; key[f] = tk;
+                                uint32_t tm = meta[e]; meta[e] = meta[f]; meta[f] = tm;
+                            }
+                        }
+                    }
+                }
+            } else if (j < 256) {
+                const int lx = j / 8;
+#pragma unroll
+                for (int e = 0; e < 8; e++) {
+                    const uint64_t ok = __shfl_xor_sync(0xffffffffu, key[e], lx);
+                    const uint32_t om = __shfl_xor_sync(0xffffffffu, meta[e], lx);
+                    const int i = base + e;
+                    const bool up = (i & k) == 0, lower = (i & j) == 0;
+                    if (cs_less(ok, om, key[e], meta[e]) == (lower == up)) {
+                        key[e] = ok;
+                        meta[e] = om;
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int e = 0; e < 8; e++) {
+                    S.xk[base + e] = key[e];
+                    S.xm[base + e] = meta[e];
+                }
+                __syncthreads();
+#pragma unroll
+                for (int e = 0; e < 8; e++) {
+                    const int i = base + e;
+                    const uint64_t ok = S.xk[i ^ j];
+                    const uint32_t om = S.xm[i ^ j];
+                    const bool up = (i & k) == 0, lower = (i & j) == 0;
+                    if (cs_less(ok, om, key[e], meta[e]) == (lower == up)) {
+                        key[e] = ok;
+                        meta[e] = om;
+                    }
+                }
+                __syncthreads();
+            }
+        }
+    }
+}
+
 template <int W>
 __global__ void __launch_bounds__(32 * W, 24 / W) k_cta_sort(
     const SegDev* __restrict__ segs, int64_t nsegs, const int64_t* __restrict__ hA,
     const uint64_t* __restrict__ kA, const int64_t* __restrict__ hB,
     const uint64_t* __restrict__ kB, const uint8_t* __restrict__ arena, int64_t alen,
     int64_t* __restrict__ out_h, int64_t* __restrict__ lcps, Counters* __restrict__ ctr) {
-    constexpr int ITEMS = 8, P = 256 * W, NT = 32 * W;
+    constexpr int ITEMS = 8, NT = 32 * W;
     extern __shared__ __align__(16) uint8_t smem_raw[];
     CtaSortSmem<W>& S = *reinterpret_cast<CtaSortSmem<W>*>(smem_raw);
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -397,60 +498,43 @@ __global__ void __launch_bounds__(32 * W, 24 / W) k_cta_sort(
     if (!valid) fetches += min(ITEMS, max(0, m - base));
     bool group_mode = false;
     for (;;) {
-        // ---- bitonic network over (group, word, tag) ----------------------
-#pragma unroll 1
-        for (int k = 2; k <= P; k <<= 1) {
-#pragma unroll 1
-            for (int j = k >> 1; j > 0; j >>= 1) {
-                if (j < ITEMS) {
+        // ---- sort by (group, word, tag): packed u64 when the bits fit ------
+        {
+            uint64_t o = 0, a = ~0ull;
 #pragma unroll
-                    for (int e = 0; e < ITEMS; e++) {
+            for (int e = 0; e < ITEMS; e++)
+                if (meta[e] >> 22 & 1) { o |= key[e]; a &= key[e]; }
+            o = warp_or64(o);
+            a = warp_and64(a);
+            if (lane == 0) { S.red[w] = o; S.red[W + w] = a; }
+            __syncthreads();
+            o = 0;
+            a = ~0ull;
 #pragma unroll
-                        for (int jj = 1; jj < ITEMS; jj <<= 1) {
-                            if (jj != j) continue;
-                            const int f = e ^ jj;
-                            if (f > e) {
-                                const bool up = ((base + e) & k) == 0;
-                                if (cs_less(key[f], meta[f], key[e], meta[e]) == up) {
-                                    uint64_t tk = key[e]; key[e] = key[f]; key[f] = tk;
-                                    uint32_t tm = meta[e]; meta[e] = meta[f]; meta[f] = tm;
-                                }
-                            }
-                        }
+            for (int v = 0; v < W; v++) { o |= S.red[v]; a &= S.red[W + v]; }
+            const Pext px = pext_setup(o ^ a);
+            if (px.cb <= 42) {
+                uint64_t c[ITEMS];
+#pragma unroll
+                for (int e = 0; e < ITEMS; e++) {
+                    const uint32_t tag = meta[e] & 0x7ff;
+                    if (meta[e] >> 22 & 1) {
+                        S.kb[tag] = key[e];
+                        c[e] = ((uint64_t)(meta[e] >> 11 & 0x7ff) << 53) | (pext_key(key[e], px) << 11) | tag;
+                    } else {
+                        c[e] = ((uint64_t)(base + e) << 53) | tag;
                     }
-                } else if (j < 256) {
-                    const int lx = j / ITEMS;
-#pragma unroll
-                    for (int e = 0; e < ITEMS; e++) {
-                        const uint64_t ok = __shfl_xor_sync(0xffffffffu, key[e], lx);
-                        const uint32_t om = __shfl_xor_sync(0xffffffffu, meta[e], lx);
-                        const int i = base + e;
-                        const bool up = (i & k) == 0, lower = (i & j) == 0;
-                        if (cs_less(ok, om, key[e], meta[e]) == (lower == up)) {
-                            key[e] = ok;
-                            meta[e] = om;
-                        }
-                    }
-                } else {
-#pragma unroll
-                    for (int e = 0; e < ITEMS; e++) {
-                        S.xk[base + e] = key[e];
-                        S.xm[base + e] = meta[e];
-                    }
-                    __syncthreads();
-#pragma unroll
-                    for (int e = 0; e < ITEMS; e++) {
-                        const int i = base + e;
-                        const uint64_t ok = S.xk[i ^ j];
-                        const uint32_t om = S.xm[i ^ j];
-                        const bool up = (i & k) == 0, lower = (i & j) == 0;
-                        if (cs_less(ok, om, key[e], meta[e]) == (lower == up)) {
-                            key[e] = ok;
-                            meta[e] = om;
-                        }
-                    }
-                    __syncthreads();
                 }
+                __syncthreads();
+                cta_bitonic_u64<W>(c, base, S);
+#pragma unroll
+                for (int e = 0; e < ITEMS; e++) {
+                    const uint32_t tag = (uint32_t)c[e] & 0x7ff;
+                    if (meta[e] >> 22 & 1) key[e] = S.kb[tag];
+                    meta[e] = (meta[e] & ~0x7ffu) | tag;
+                }
+            } else {
+                cta_bitonic_generic<W>(key, meta, base, S);
             }
         }
         // ---- LCPs at word changes, run breaks -------------------------------
@@ -521,7 +605,7 @@ __global__ void __launch_bounds__(32 * W, 24 / W) k_cta_sort(
         uint32_t cur = __shfl_up_sync(0xffffffffu, incl, 1);
         if (lane == 0) cur = 0;
         for (int v = 0; v < w; v++) cur = max(cur, S.wmax[v]);
-        // longest kept run decides: CTA round again, or one warp per run
+        // longest kept run decides: another CTA round, or one warp per run
         uint32_t longest = 0, c2 = cur;
 #pragma unroll
         for (int e = 0; e < ITEMS; e++) {
@@ -535,10 +619,9 @@ __global__ void __launch_bounds__(32 * W, 24 / W) k_cta_sort(
         uint32_t lmax = 0;
         for (int v = 0; v < W; v++) lmax = max(lmax, S.wcnt[v]);
         if (W == 8 && lmax <= 256) {
-            // ---- group mode: write the slot order, list the kept runs --------
+            // ---- group mode: slot order + list of the kept runs -------------
 #pragma unroll
             for (int e = 0; e < ITEMS; e++) S.ord[base + e] = (uint16_t)(meta[e] & 0x7ff);
-            // starts and ends are counted separately: a run may span threads
             const uint32_t mine = nstart | (nend << 16);
             const uint32_t ns = __reduce_add_sync(0xffffffffu, mine);
             uint32_t pre = mine;
@@ -556,7 +639,6 @@ __global__ void __launch_bounds__(32 * W, 24 / W) k_cta_sort(
                 if (v < w) off += S.wcnt[v];
                 tot2 += S.wcnt[v];
             }
-            const uint32_t ngroups = tot2 & 0xffff;
             uint32_t gi = (off + pre) & 0xffff, ge_i = (off + pre) >> 16;
 #pragma unroll
             for (int e = 0; e < ITEMS; e++) {
@@ -564,7 +646,8 @@ __global__ void __launch_bounds__(32 * W, 24 / W) k_cta_sort(
                 if (keep[e] && brk[e]) S.gs[gi++] = (uint16_t)i;
                 if (kend[e]) S.ge[ge_i++] = (uint16_t)i;
             }
-            if (threadIdx.x == 0) S.wcnt[0] = ngroups;
+            __syncthreads();
+            if (threadIdx.x == 0) S.wcnt[0] = tot2 & 0xffff;
             __syncthreads();
             group_mode = true;
             break;
@@ -583,7 +666,7 @@ __global__ void __launch_bounds__(32 * W, 24 / W) k_cta_sort(
                 key[e] = load_key(arena, alen, S.h[meta[e] & 0x7ff], depth);
                 fetches++;
             }
-        __syncthreads();  // S.wmax / S.last_key / S.wcnt reuse
+        __syncthreads();  // S.wmax / S.last_key / S.wcnt / S.red reuse
     }
     if (!group_mode) {
 #pragma unroll
@@ -593,14 +676,20 @@ __global__ void __launch_bounds__(32 * W, 24 / W) k_cta_sort(
         const uint32_t ngroups = S.wcnt[0];
         for (uint32_t g = w; g < ngroups; g += W) {
             const int g0 = S.gs[g], gn = S.ge[g] - g0 + 1;
-            if (gn <= 32)
-                cs_finish_group<1>(S.h, S.ord, g0, gn, depth + WORD, arena, alen, lcp_seg, fetches, lane);
-            else if (gn <= 64)
-                cs_finish_group<2>(S.h, S.ord, g0, gn, depth + WORD, arena, alen, lcp_seg, fetches, lane);
-            else if (gn <= 128)
-                cs_finish_group<4>(S.h, S.ord, g0, gn, depth + WORD, arena, alen, lcp_seg, fetches, lane);
-            else
-                cs_finish_group<8>(S.h, S.ord, g0, gn, depth + WORD, arena, alen, lcp_seg, fetches, lane);
+            const int64_t d = depth + WORD;
+            if (gn <= 32) {
+                uint64_t k1[1];
+                warp_finish<1>(S.h, S.ord, S.kb, g0, gn, d, false, k1, arena, alen, lcp_seg, fetches, lane);
+            } else if (gn <= 64) {
+                uint64_t k2[2];
+                warp_finish<2>(S.h, S.ord, S.kb, g0, gn, d, false, k2, arena, alen, lcp_seg, fetches, lane);
+            } else if (gn <= 128) {
+                uint64_t k4[4];
+                warp_finish<4>(S.h, S.ord, S.kb, g0, gn, d, false, k4, arena, alen, lcp_seg, fetches, lane);
+            } else {
+                uint64_t k8[8];
+                warp_finish<8>(S.h, S.ord, S.kb, g0, gn, d, false, k8, arena, alen, lcp_seg, fetches, lane);
+            }
         }
     }
     __syncthreads();
