@@ -35,22 +35,22 @@ __global__ void k_extract_keys(const uint8_t* __restrict__ arena, int64_t alen,
     if (i < n) out[i] = exact_key(arena, alen, handles[i], depth);
 }
 
-// Copy handles into the work array and cache each string's first key.
+// Copy handles into the work records and cache each string's first three words.
 __global__ void k_init(const uint8_t* __restrict__ arena, int64_t alen,
                        const int64_t* __restrict__ handles, int64_t n, int64_t depth,
-                       int64_t* __restrict__ hA, uint64_t* __restrict__ kA) {
+                       Rec* __restrict__ recA) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i < n) {
-        int64_t h = handles[i];
-        hA[i] = h;
-        kA[i] = load_key(arena, alen, h, depth);
+        Rec r;
+        r.h = handles[i];
+        load_words3(arena, alen, r.h, depth, r.w);
+        recA[i] = r;
     }
 }
 
 __global__ void __launch_bounds__(SAMPLE_NT) k_sample_tree(
     const StepDev* __restrict__ steps, const uint8_t* __restrict__ arena, int64_t alen,
-    const int64_t* __restrict__ hX, const uint64_t* __restrict__ kX, uint64_t seed,
-    uint64_t* __restrict__ tree_g, uint64_t* __restrict__ inorder_g, uint8_t* __restrict__ tpos_g,
+    const Rec* __restrict__ recX, uint64_t seed, uint64_t* __restrict__ tree_g, uint64_t* __restrict__ inorder_g, uint8_t* __restrict__ tpos_g,
     uint16_t* __restrict__ eqb_g) {
     extern __shared__ __align__(16) uint8_t smem[];
     const StepDev sd = steps[blockIdx.x];
@@ -69,7 +69,8 @@ __global__ void __launch_bounds__(SAMPLE_NT) k_sample_tree(
         uint64_t x = ~0ull;
         if (j < count) {
             int64_t idx = (int64_t)(splitmix64(key0 + j) % (uint64_t)sd.n);
-            x = sd.keys_valid ? kX[sd.lo + idx] : load_key(arena, alen, hX[sd.lo + idx], sd.depth);
+            const Rec* r = recX + sd.lo + idx;
+            x = sd.nvalid ? r->w[0] : load_key(arena, alen, r->h, sd.depth);
         }
         s[j] = x;
     }
@@ -123,8 +124,8 @@ __device__ __forceinline__ uint32_t classify_one(uint64_t key, const uint64_t* t
 template <int VARIANT>
 __global__ void __launch_bounds__(CLS_NT) k_classify(
     const StepDev* __restrict__ steps, const int32_t* __restrict__ tile_step,
-    const uint8_t* __restrict__ arena, int64_t alen, const int64_t* __restrict__ hX,
-    uint64_t* __restrict__ kX, uint16_t* __restrict__ bid, uint32_t* __restrict__ cnt,
+    const uint8_t* __restrict__ arena, int64_t alen, Rec* __restrict__ recX,
+    uint16_t* __restrict__ bid, uint32_t* __restrict__ cnt,
     const uint64_t* __restrict__ tree_g, const uint16_t* __restrict__ eqb_g,
     Counters* __restrict__ ctr) {
     extern __shared__ __align__(16) uint8_t smem[];
@@ -169,12 +170,16 @@ __global__ void __launch_bounds__(CLS_NT) k_classify(
             ok[u] = i < end;
             key[u] = 0;
             if (ok[u]) {
-                if (sd.keys_valid) {
-                    key[u] = kX[i];
-                } else {
-                    key[u] = load_key(arena, alen, hX[i], sd.depth);
-                    kX[i] = key[u];
-                    my_fetch++;
+                if (sd.nvalid) {
+                    key[u] = recX[i].w[0];
+                } else {  // refill the record's three cached words
+                    uint64_t wv[3];
+                    load_words3(arena, alen, recX[i].h, sd.depth, wv);
+                    recX[i].w[0] = wv[0];
+                    recX[i].w[1] = wv[1];
+                    recX[i].w[2] = wv[2];
+                    key[u] = wv[0];
+                    my_fetch += 3;
                 }
             }
         }
@@ -291,7 +296,8 @@ __global__ void __launch_bounds__(1024) k_scan_buckets(
                 c.lo = sd.lo + run;
                 c.depth = sd.depth + (odd ? WORD : 0);
                 c.n = (int32_t)size;
-                c.flags = (odd ? 0 : SEG_KEYS_VALID) | (dst_in_b ? SEG_IN_B : 0);
+                const int nv = sd.nvalid ? sd.nvalid : NCACHE;  // classify refilled
+                c.flags = (odd ? nv - 1 : nv) | (dst_in_b ? SEG_IN_B : 0);
                 if ((int64_t)size <= small_max) {
                     const int ci = size_class(size);
                     small_out[cls.off[ci] + atomicAdd(&ctr->n_cls[ci], 1ull)] = c;
@@ -311,11 +317,10 @@ __global__ void __launch_bounds__(1024) k_scan_buckets(
 // (ssss.py:345-357).
 __global__ void __launch_bounds__(SC_NT) k_scatter(
     const StepDev* __restrict__ steps, const int32_t* __restrict__ tile_step,
-    const int64_t* __restrict__ hX, const uint64_t* __restrict__ kX,
-    const uint16_t* __restrict__ bid, const uint32_t* __restrict__ cnt,
-    const uint32_t* __restrict__ tot, const uint32_t* __restrict__ bstart,
-    const uint8_t* __restrict__ tpos_g, int64_t* __restrict__ hY, uint64_t* __restrict__ kY,
-    int64_t* __restrict__ out_h, int64_t* __restrict__ lcps) {
+    const Rec* __restrict__ recX, const uint16_t* __restrict__ bid,
+    const uint32_t* __restrict__ cnt, const uint32_t* __restrict__ tot,
+    const uint32_t* __restrict__ bstart, const uint8_t* __restrict__ tpos_g,
+    Rec* __restrict__ recY, int64_t* __restrict__ out_h, int64_t* __restrict__ lcps) {
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ uint32_t wsum[32];
     uint32_t* run_off = reinterpret_cast<uint32_t*>(smem);                 // NBMAX+1
@@ -364,16 +369,23 @@ __global__ void __launch_bounds__(SC_NT) k_scatter(
             const int64_t e = sub + vA[q];
             const uint32_t rel = run_off[b] + (q - st[i]);
             const int64_t pos = sd.lo + rel;
-            const int64_t h = hX[e];
+            const Rec r = recX[e];
             const uint32_t size = tot[sd.bk_off + b];
             const bool odd = b & 1;
             const int tpv = odd ? tp[b >> 1] : WORD;
             if (size == 1 || (odd && tpv < WORD)) {
-                out_h[pos] = h;
+                out_h[pos] = r.h;
                 if (lcps && size > 1 && rel != bstart[sd.bk_off + b]) lcps[pos] = sd.depth + tpv;
+            } else if (odd) {
+                // equality bucket: continues one word deeper -> shift the cache
+                Rec o;
+                o.h = r.h;
+                o.w[0] = r.w[1];
+                o.w[1] = r.w[2];
+                o.w[2] = 0;
+                recY[pos] = o;
             } else {
-                hY[pos] = h;
-                kY[pos] = kX[e];
+                recY[pos] = r;
             }
         }
         __syncthreads();
@@ -597,8 +609,7 @@ static int64_t small_max_of(int64_t t_medium) {
 }
 
 struct Workspace {
-    int64_t *hA, *hB;
-    uint64_t *kA, *kB;
+    Rec *recA, *recB;
     uint16_t* bid;
     uint32_t* cnt;
     uint32_t *tot, *bstart;
@@ -640,10 +651,8 @@ static size_t carve(Workspace* w, uint8_t* base, int64_t n, int64_t t_medium) {
             off += w->cls_cap[c];
         }
     }
-    w->hA = (int64_t*)take(8 * nn);
-    w->hB = (int64_t*)take(8 * nn);
-    w->kA = (uint64_t*)take(8 * nn);
-    w->kB = (uint64_t*)take(8 * nn);
+    w->recA = (Rec*)take(sizeof(Rec) * nn);
+    w->recB = (Rec*)take(sizeof(Rec) * nn);
     w->bid = (uint16_t*)take(2 * nn);
     w->cnt = (uint32_t*)take(4 * w->cnt_cap);
     w->tot = (uint32_t*)take(4 * w->bk_cap);
@@ -771,15 +780,15 @@ static int sort_impl_body(const s5g_sort_args* a) {
     for (int c = 0; c < NCLS; c++) cls_lists.off[c] = w.cls_off[c];
 
     CK(cudaMemsetAsync(w.ctr, 0, sizeof(Counters), st));
-    PROF(K_INIT, n, 32LL * n, (k_init<<<blocks_for(n, 256), 256, 0, st>>>(a->arena, a->arena_len,
-                                                                 a->handles, n, a->depth, w.hA,
-                                                                 w.kA)));
+    PROF(K_INIT, n, 56LL * n, (k_init<<<blocks_for(n, 256), 256, 0, st>>>(a->arena, a->arena_len,
+                                                                 a->handles, n, a->depth,
+                                                                 w.recA)));
     CK(cudaGetLastError());
     Counters hc{};
     hc.fetches = 0;
     int64_t n_jobs = 0;
     std::vector<SegDev> large;
-    SegDev root{0, a->depth, (int32_t)n, SEG_KEYS_VALID};
+    SegDev root{0, a->depth, (int32_t)n, NCACHE};
     if (n <= small_max) {
         const int cls = size_class(n);
         CK(cudaMemcpyAsync(w.small + w.cls_off[cls], &root, sizeof(SegDev),
@@ -823,7 +832,7 @@ static int sort_impl_body(const s5g_sort_args* a) {
                 d.count = alpha * (d.v + 1) - 1;
                 d.levels = levels_of(d.v);
                 d.nb = 2 * d.v + 1;
-                d.keys_valid = (s.flags & SEG_KEYS_VALID) ? 1 : 0;
+                d.nvalid = s.flags & SEG_NV_MASK;
                 d.ntiles = (int32_t)((s.n + TILE - 1) / TILE);
                 int64_t need_cnt = (int64_t)d.ntiles * d.nb;
                 if ((int64_t)steps.size() + 1 > w.steps_cap ||
@@ -858,38 +867,36 @@ static int sort_impl_body(const s5g_sort_args* a) {
                                cudaMemcpyHostToDevice, st));
             CK(cudaMemcpyAsync(w.tile_step + tile0, cblk_step.data(), 4 * cblk_step.size(),
                                cudaMemcpyHostToDevice, st));
-            const int64_t* hX = in_b ? w.hB : w.hA;
-            uint64_t* kX = in_b ? w.kB : w.kA;
-            int64_t* hY = in_b ? w.hA : w.hB;
-            uint64_t* kY = in_b ? w.kA : w.kB;
+            Rec* recX = in_b ? w.recB : w.recA;
+            Rec* recY = in_b ? w.recA : w.recB;
             int maxv = 1;
             long long sample_bytes = 0;
             int maxP = 1;
             for (auto& d : steps) {
                 maxv = std::max(maxv, d.v);
                 while (maxP < d.count) maxP <<= 1;
-                sample_bytes += (long long)d.count * (d.keys_valid ? 8 : 16) + 27LL * d.v;
+                sample_bytes += (long long)d.count * (d.nvalid ? 8 : 16) + 27LL * d.v;
             }
             PROF(K_SAMPLE, nsteps, sample_bytes,
                  (k_sample_tree<<<nsteps, SAMPLE_NT, smem_sample(maxP, maxv), st>>>(
-                     w.steps, a->arena, a->arena_len, hX, kX, a->seed, w.tree, w.inorder, w.tpos,
+                     w.steps, a->arena, a->arena_len, recX, a->seed, w.tree, w.inorder, w.tpos,
                      w.eqb)));
             CK(cudaGetLastError());
             const unsigned ntiles = (unsigned)tile0;
             int64_t round_elems = 0, cls_bytes = 0;
             for (auto& d : steps) {
                 round_elems += d.n;
-                cls_bytes += (d.keys_valid ? 10LL : 26LL) * d.n;
+                cls_bytes += (d.nvalid ? 10LL : 66LL) * d.n;
             }
             if (a->variant == S5G_VARIANT_UNROLL)
                 PROF(K_CLASSIFY, round_elems, cls_bytes,
                      (k_classify<S5G_VARIANT_UNROLL><<<ntiles, CLS_NT, SMEM_CLS_UNROLL, st>>>(
-                         w.steps, w.tile_step, a->arena, a->arena_len, hX, kX, w.bid, w.cnt,
+                         w.steps, w.tile_step, a->arena, a->arena_len, recX, w.bid, w.cnt,
                          w.tree, w.eqb, w.ctr)));
             else
                 PROF(K_CLASSIFY, round_elems, cls_bytes,
                      (k_classify<S5G_VARIANT_EQUAL><<<ntiles, CLS_NT, SMEM_CLS, st>>>(
-                         w.steps, w.tile_step, a->arena, a->arena_len, hX, kX, w.bid, w.cnt,
+                         w.steps, w.tile_step, a->arena, a->arena_len, recX, w.bid, w.cnt,
                          w.tree, w.eqb, w.ctr)));
             CK(cudaGetLastError());
             PROF(K_SCAN_COLS, cnt_off, 8LL * cnt_off + 4LL * bk_off,
@@ -902,9 +909,9 @@ static int sort_impl_body(const s5g_sort_args* a) {
                                                          w.small, cls_lists, w.blist, lcps,
                                                          w.ctr)));
             CK(cudaGetLastError());
-            PROF(K_SCATTER, round_elems, 34LL * round_elems,
-                 (k_scatter<<<ntiles, SC_NT, SMEM_SC, st>>>(w.steps, w.tile_step, hX, kX, w.bid,
-                                                           w.cnt, w.tot, w.bstart, w.tpos, hY, kY,
+            PROF(K_SCATTER, round_elems, 66LL * round_elems,
+                 (k_scatter<<<ntiles, SC_NT, SMEM_SC, st>>>(w.steps, w.tile_step, recX, w.bid,
+                                                           w.cnt, w.tot, w.bstart, w.tpos, recY,
                                                            a->out_handles, lcps)));
             CK(cudaGetLastError());
             if (a->step_cb) {
@@ -951,25 +958,25 @@ static int sort_impl_body(const s5g_sort_args* a) {
         const SegDev* lst = w.small + w.cls_off[c];
         switch (c) {
             case 0: PROF(K_SEG_WARP + 0, (long long)hc.cls_elems[0], 0, (k_warp_sort<1><<<grid, WS_NT, 0, st>>>(
-                        lst, cnt_c, w.hA, w.kA, w.hB, w.kB, a->arena, a->arena_len,
+                        lst, cnt_c, w.recA, w.recB, a->arena, a->arena_len,
                         a->out_handles, lcps, w.ctr))); break;
             case 1: PROF(K_SEG_WARP + 1, (long long)hc.cls_elems[1], 0, (k_warp_sort<2><<<grid, WS_NT, 0, st>>>(
-                        lst, cnt_c, w.hA, w.kA, w.hB, w.kB, a->arena, a->arena_len,
+                        lst, cnt_c, w.recA, w.recB, a->arena, a->arena_len,
                         a->out_handles, lcps, w.ctr))); break;
             case 2: PROF(K_SEG_WARP + 2, (long long)hc.cls_elems[2], 0, (k_warp_sort<4><<<grid, WS_NT, 0, st>>>(
-                        lst, cnt_c, w.hA, w.kA, w.hB, w.kB, a->arena, a->arena_len,
+                        lst, cnt_c, w.recA, w.recB, a->arena, a->arena_len,
                         a->out_handles, lcps, w.ctr))); break;
             case 3: PROF(K_SEG_WARP + 3, (long long)hc.cls_elems[3], 0, (k_warp_sort<8><<<grid, WS_NT, 0, st>>>(
-                        lst, cnt_c, w.hA, w.kA, w.hB, w.kB, a->arena, a->arena_len,
+                        lst, cnt_c, w.recA, w.recB, a->arena, a->arena_len,
                         a->out_handles, lcps, w.ctr))); break;
             case 4: PROF(K_SEG_CTA2, (long long)hc.cls_elems[4], 0, (k_cta_sort<2><<<(unsigned)cnt_c, 64,
-                        sizeof(CtaSortSmem<2>), st>>>(lst, cnt_c, w.hA, w.kA, w.hB, w.kB,
+                        sizeof(CtaSortSmem<2>), st>>>(lst, cnt_c, w.recA, w.recB,
                         a->arena, a->arena_len, a->out_handles, lcps, w.ctr))); break;
             case 5: PROF(K_SEG_CTA4, (long long)hc.cls_elems[5], 0, (k_cta_sort<4><<<(unsigned)cnt_c, 128,
-                        sizeof(CtaSortSmem<4>), st>>>(lst, cnt_c, w.hA, w.kA, w.hB, w.kB,
+                        sizeof(CtaSortSmem<4>), st>>>(lst, cnt_c, w.recA, w.recB,
                         a->arena, a->arena_len, a->out_handles, lcps, w.ctr))); break;
             default: PROF(K_SEG_CTA8, (long long)hc.cls_elems[6], 0, (k_cta_sort<8><<<(unsigned)cnt_c, 256,
-                        sizeof(CtaSortSmem<8>), st>>>(lst, cnt_c, w.hA, w.kA, w.hB, w.kB,
+                        sizeof(CtaSortSmem<8>), st>>>(lst, cnt_c, w.recA, w.recB,
                         a->arena, a->arena_len, a->out_handles, lcps, w.ctr))); break;
         }
         CK(cudaGetLastError());

@@ -70,6 +70,27 @@ __device__ __forceinline__ uint64_t load_key(const uint8_t* __restrict__ arena, 
     return mask_terminated(bswap64(load_word_le(arena, arena_len, h + d)));
 }
 
+__device__ __forceinline__ uint64_t ld8_guard(const uint8_t* __restrict__ arena, int64_t alen,
+                                              int64_t a) {
+    return a < alen ? __ldg(reinterpret_cast<const unsigned long long*>(arena + a)) : 0ull;
+}
+
+// The three words at depth d of the string at h (0 past the terminator):
+// four aligned 8-byte loads, funnel shifts, byte swaps, exact masking.
+__device__ __forceinline__ void load_words3(const uint8_t* __restrict__ arena, int64_t alen,
+                                            int64_t h, int64_t d, uint64_t (&w)[3]) {
+    const int64_t p = h + d, a = p & ~int64_t(7);
+    const int sh = (int)(p & 7);
+    const uint64_t x0 = ld8_guard(arena, alen, a), x1 = ld8_guard(arena, alen, a + 8),
+                   x2 = ld8_guard(arena, alen, a + 16), x3 = sh ? ld8_guard(arena, alen, a + 24) : 0;
+    const uint64_t l0 = sh ? (x0 >> (8 * sh)) | (x1 << (64 - 8 * sh)) : x0;
+    const uint64_t l1 = sh ? (x1 >> (8 * sh)) | (x2 << (64 - 8 * sh)) : x1;
+    const uint64_t l2 = sh ? (x2 >> (8 * sh)) | (x3 << (64 - 8 * sh)) : x2;
+    w[0] = mask_terminated(bswap64(l0));
+    w[1] = term_pos(w[0]) < WORD ? 0 : mask_terminated(bswap64(l1));
+    w[2] = term_pos(w[1]) < WORD ? 0 : mask_terminated(bswap64(l2));
+}
+
 __device__ __forceinline__ uint32_t lanemask_lt() {
     uint32_t m;
     asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));

@@ -26,11 +26,22 @@ constexpr int SC_R = 1 << SC_RB;
 constexpr uint16_t BID_SENTINEL = 0x3FFF; // > any bucket id (max 16382)
 constexpr int SAMPLE_NT = 1024;
 
-enum : int32_t { SEG_KEYS_VALID = 1, SEG_IN_B = 2 };
+// Work record of one string: its handle and the next three words from the
+// segment's depth (the paper's character cache, widened to one 32-byte
+// sector: scatters write whole sectors, and the finishers find the next two
+// words without a gather).  Words past the terminator are 0.
+struct __align__(32) Rec {
+    int64_t h;
+    uint64_t w[3];
+};
+constexpr int NCACHE = 3;
+
+// SegDev.flags: number of valid cached words (0..3) | data in buffer B
+enum : int32_t { SEG_NV_MASK = 3, SEG_IN_B = 4 };
 
 struct StepDev {
     int64_t lo, n, depth;
-    int32_t v, levels, nb, keys_valid;
+    int32_t v, levels, nb, nvalid;   // nvalid: cached words valid at depth (0 = refill)
     int64_t tile0;
     int32_t ntiles, pad0;
     int64_t cnt_off;   // first entry in the tile x bucket count matrix

@@ -60,6 +60,18 @@ __device__ __forceinline__ uint64_t pext_key(uint64_t x, const Pext& p) {
     return c;
 }
 
+// Word at `depth` of the segment's string `tag`: from its work record while
+// the cache covers that depth (depth - d0 < 8 * nv), else an arena gather.
+__device__ __forceinline__ uint64_t seg_word(const Rec* __restrict__ segrec, uint32_t tag,
+                                             int64_t d0, int nv, int64_t depth,
+                                             const uint8_t* __restrict__ arena, int64_t alen,
+                                             int64_t h, unsigned& fetches) {
+    const int64_t r = (depth - d0) >> 3;
+    if (r < nv) return segrec[tag].w[r];
+    fetches++;
+    return load_key(arena, alen, h, depth);
+}
+
 __device__ __forceinline__ void cex_u64(uint64_t& a, uint64_t& b, bool up) {
     const uint64_t lo = min(a, b), hi = max(a, b);
     a = up ? lo : hi;
@@ -152,20 +164,17 @@ __device__ __forceinline__ uint64_t warp_and64(uint64_t x) {
 // interior and the final tag order back to ord[g0 ..].
 template <int IT>
 __device__ void warp_finish(const int64_t* __restrict__ hbt, uint16_t* __restrict__ ord,
-                            uint64_t* __restrict__ kb, int g0, int gn, int64_t depth,
-                            bool have_keys, uint64_t (&key)[IT], const uint8_t* __restrict__ arena,
-                            int64_t alen, int64_t* __restrict__ lcp_seg, unsigned& fetches,
-                            int lane) {
+                            uint64_t* __restrict__ kb, const Rec* __restrict__ segrec, int64_t d0,
+                            int nv, int g0, int gn, int64_t depth, uint64_t (&key)[IT],
+                            const uint8_t* __restrict__ arena, int64_t alen,
+                            int64_t* __restrict__ lcp_seg, unsigned& fetches, int lane) {
     uint32_t meta[IT];
 #pragma unroll
     for (int e = 0; e < IT; e++) {
         const int i = lane * IT + e;
         if (i < gn) {
             const uint32_t tag = ord[g0 + i];
-            if (!have_keys) {
-                key[e] = load_key(arena, alen, hbt[tag], depth);
-                fetches++;
-            }
+            key[e] = seg_word(segrec, tag, d0, nv, depth, arena, alen, hbt[tag], fetches);
             meta[e] = (1u << 22) | tag;
         } else {
             key[e] = ~0ull;
@@ -263,8 +272,8 @@ __device__ void warp_finish(const int64_t* __restrict__ hbt, uint16_t* __restric
 #pragma unroll
         for (int e = 0; e < IT; e++)
             if (meta[e] >> 22 & 1) {
-                key[e] = load_key(arena, alen, hbt[meta[e] & 0x7ff], depth);
-                fetches++;
+                const uint32_t tag = meta[e] & 0x7ff;
+                key[e] = seg_word(segrec, tag, d0, nv, depth, arena, alen, hbt[tag], fetches);
             }
     }
 #pragma unroll
@@ -281,9 +290,8 @@ constexpr int WS_NT = 256;  // 8 warps per CTA, one segment per warp
 
 template <int ITEMS>
 __global__ void __launch_bounds__(WS_NT) k_warp_sort(
-    const SegDev* __restrict__ segs, int64_t nsegs, const int64_t* __restrict__ hA,
-    const uint64_t* __restrict__ kA, const int64_t* __restrict__ hB,
-    const uint64_t* __restrict__ kB, const uint8_t* __restrict__ arena, int64_t alen,
+    const SegDev* __restrict__ segs, int64_t nsegs, const Rec* __restrict__ recA,
+    const Rec* __restrict__ recB, const uint8_t* __restrict__ arena, int64_t alen,
     int64_t* __restrict__ out_h, int64_t* __restrict__ lcps, Counters* __restrict__ ctr) {
     constexpr int CAP = 32 * ITEMS;
     __shared__ int64_t s_h[WS_NT / 32][CAP];
@@ -295,9 +303,8 @@ __global__ void __launch_bounds__(WS_NT) k_warp_sort(
     const SegDev sg = segs[gw];
     const int m = sg.n;
     const int64_t lo = sg.lo;
-    const int64_t* sh = (sg.flags & SEG_IN_B) ? hB : hA;
-    const uint64_t* sk = (sg.flags & SEG_IN_B) ? kB : kA;
-    const bool valid = sg.flags & SEG_KEYS_VALID;
+    const Rec* segrec = ((sg.flags & SEG_IN_B) ? recB : recA) + lo;
+    const int nv = sg.flags & SEG_NV_MASK;
     int64_t* wh = s_h[w];
     uint16_t* wo = s_o[w];
     unsigned fetches = 0;
@@ -305,20 +312,13 @@ __global__ void __launch_bounds__(WS_NT) k_warp_sort(
     for (int e = 0; e < ITEMS; e++) {
         const int i = e * 32 + lane;
         if (i < m) {
-            wh[i] = sh[lo + i];
+            wh[i] = segrec[i].h;
             wo[i] = (uint16_t)i;
         }
     }
     __syncwarp();
     uint64_t key[ITEMS];
-    if (valid) {
-#pragma unroll
-        for (int e = 0; e < ITEMS; e++) {
-            const int i = lane * ITEMS + e;
-            key[e] = i < m ? sk[lo + i] : ~0ull;
-        }
-    }
-    warp_finish<ITEMS>(wh, wo, s_k[w], 0, m, sg.depth, valid, key, arena, alen,
+    warp_finish<ITEMS>(wh, wo, s_k[w], segrec, sg.depth, nv, 0, m, sg.depth, key, arena, alen,
                        lcps ? lcps + lo : nullptr, fetches, lane);
     __syncwarp();
 #pragma unroll
@@ -462,9 +462,8 @@ __device__ void cta_bitonic_generic(uint64_t (&key)[8], uint32_t (&meta)[8], int
 
 template <int W>
 __global__ void __launch_bounds__(32 * W, 24 / W) k_cta_sort(
-    const SegDev* __restrict__ segs, int64_t nsegs, const int64_t* __restrict__ hA,
-    const uint64_t* __restrict__ kA, const int64_t* __restrict__ hB,
-    const uint64_t* __restrict__ kB, const uint8_t* __restrict__ arena, int64_t alen,
+    const SegDev* __restrict__ segs, int64_t nsegs, const Rec* __restrict__ recA,
+    const Rec* __restrict__ recB, const uint8_t* __restrict__ arena, int64_t alen,
     int64_t* __restrict__ out_h, int64_t* __restrict__ lcps, Counters* __restrict__ ctr) {
     constexpr int ITEMS = 8, NT = 32 * W;
     extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -473,13 +472,13 @@ __global__ void __launch_bounds__(32 * W, 24 / W) k_cta_sort(
     const SegDev sg = segs[blockIdx.x];
     const int m = sg.n;
     const int64_t lo = sg.lo;
-    const int64_t* sh = (sg.flags & SEG_IN_B) ? hB : hA;
-    const uint64_t* sk = (sg.flags & SEG_IN_B) ? kB : kA;
-    const bool valid = sg.flags & SEG_KEYS_VALID;
+    const Rec* segrec = ((sg.flags & SEG_IN_B) ? recB : recA) + lo;
+    const int nv = sg.flags & SEG_NV_MASK;
+    const int64_t d0 = sg.depth;
     int64_t* lcp_seg = lcps ? lcps + lo : nullptr;
     int64_t depth = sg.depth;
     unsigned fetches = 0;
-    for (int i = threadIdx.x; i < m; i += NT) S.h[i] = sh[lo + i];
+    for (int i = threadIdx.x; i < m; i += NT) S.h[i] = segrec[i].h;
     __syncthreads();
     uint64_t key[ITEMS];
     uint32_t meta[ITEMS];
@@ -488,14 +487,13 @@ __global__ void __launch_bounds__(32 * W, 24 / W) k_cta_sort(
     for (int e = 0; e < ITEMS; e++) {
         const int i = base + e;
         if (i < m) {
-            key[e] = valid ? sk[lo + i] : load_key(arena, alen, S.h[i], depth);
+            key[e] = seg_word(segrec, i, d0, nv, depth, arena, alen, S.h[i], fetches);
             meta[e] = (1u << 22) | (uint32_t)i;
         } else {
             key[e] = ~0ull;
             meta[e] = ((uint32_t)i << 11) | (uint32_t)i;
         }
     }
-    if (!valid) fetches += min(ITEMS, max(0, m - base));
     bool group_mode = false;
     for (;;) {
         // ---- sort by (group, word, tag): packed u64 when the bits fit ------
@@ -663,8 +661,8 @@ __global__ void __launch_bounds__(32 * W, 24 / W) k_cta_sort(
 #pragma unroll
         for (int e = 0; e < ITEMS; e++)
             if (meta[e] >> 22 & 1) {
-                key[e] = load_key(arena, alen, S.h[meta[e] & 0x7ff], depth);
-                fetches++;
+                const uint32_t tag = meta[e] & 0x7ff;
+                key[e] = seg_word(segrec, tag, d0, nv, depth, arena, alen, S.h[tag], fetches);
             }
         __syncthreads();  // S.wmax / S.last_key / S.wcnt / S.red reuse
     }
@@ -679,16 +677,16 @@ __global__ void __launch_bounds__(32 * W, 24 / W) k_cta_sort(
             const int64_t d = depth + WORD;
             if (gn <= 32) {
                 uint64_t k1[1];
-                warp_finish<1>(S.h, S.ord, S.kb, g0, gn, d, false, k1, arena, alen, lcp_seg, fetches, lane);
+                warp_finish<1>(S.h, S.ord, S.kb, segrec, d0, nv, g0, gn, d, k1, arena, alen, lcp_seg, fetches, lane);
             } else if (gn <= 64) {
                 uint64_t k2[2];
-                warp_finish<2>(S.h, S.ord, S.kb, g0, gn, d, false, k2, arena, alen, lcp_seg, fetches, lane);
+                warp_finish<2>(S.h, S.ord, S.kb, segrec, d0, nv, g0, gn, d, k2, arena, alen, lcp_seg, fetches, lane);
             } else if (gn <= 128) {
                 uint64_t k4[4];
-                warp_finish<4>(S.h, S.ord, S.kb, g0, gn, d, false, k4, arena, alen, lcp_seg, fetches, lane);
+                warp_finish<4>(S.h, S.ord, S.kb, segrec, d0, nv, g0, gn, d, k4, arena, alen, lcp_seg, fetches, lane);
             } else {
                 uint64_t k8[8];
-                warp_finish<8>(S.h, S.ord, S.kb, g0, gn, d, false, k8, arena, alen, lcp_seg, fetches, lane);
+                warp_finish<8>(S.h, S.ord, S.kb, segrec, d0, nv, g0, gn, d, k8, arena, alen, lcp_seg, fetches, lane);
             }
         }
     }
