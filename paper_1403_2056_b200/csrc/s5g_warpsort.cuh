@@ -73,9 +73,10 @@ __device__ __forceinline__ uint64_t seg_word(const Rec* __restrict__ segrec, uin
 }
 
 __device__ __forceinline__ void cex_u64(uint64_t& a, uint64_t& b, bool up) {
-    const uint64_t lo = min(a, b), hi = max(a, b);
-    a = up ? lo : hi;
-    b = up ? hi : lo;
+    const bool sw = (b < a) == up;
+    const uint64_t x = a, y = b;
+    a = sw ? y : x;
+    b = sw ? x : y;
 }
 
 // ---------------------------------------------------------------------------
@@ -96,12 +97,12 @@ __device__ __forceinline__ void warp_bitonic_u64(uint64_t (&c)[IT], int lane) {
                 }
             } else {
                 const int lx = j / IT;
+                const int i0 = lane * IT;  // j >= IT: direction uniform over e
+                const bool keep_min = ((i0 & j) == 0) == ((i0 & k) == 0);
 #pragma unroll
                 for (int e = 0; e < IT; e++) {
                     const uint64_t o = __shfl_xor_sync(0xffffffffu, c[e], lx);
-                    const int i = lane * IT + e;
-                    const bool keep_min = ((i & j) == 0) == ((i & k) == 0);
-                    c[e] = keep_min ? min(c[e], o) : max(c[e], o);
+                    c[e] = ((o < c[e]) == keep_min) ? o : c[e];
                 }
             }
         }
@@ -287,6 +288,9 @@ __device__ void warp_finish(const int64_t* __restrict__ hbt, uint16_t* __restric
 // k_warp_sort: one warp per segment of <= 32*ITEMS strings
 
 constexpr int WS_NT = 256;  // 8 warps per CTA, one segment per warp
+#ifndef GROUP_MODE_MIN_W
+#define GROUP_MODE_MIN_W 8
+#endif
 
 template <int ITEMS>
 __global__ void __launch_bounds__(WS_NT) k_warp_sort(
@@ -351,17 +355,25 @@ struct CtaSortSmem {
     uint32_t first_brk[W], first_act[W], wmax[W], wcnt[W];
 };
 
-template <int J>
-__device__ __forceinline__ void cta_inlane(uint64_t (&c)[8], int base, int k) {
+// In-lane stage at distance J < 8.  The direction bit (slot & k) is the same
+// for all 8 slots of a thread once k >= 8; below that it varies with e.
+template <int J, typename T>
+__device__ __forceinline__ void cta_inlane(T (&c)[8], int base, int k) {
 #pragma unroll
     for (int e = 0; e < 8; e++) {
         const int f = e ^ J;
-        if (f > e) cex_u64(c[e], c[f], ((base + e) & k) == 0);
+        if (f > e) {
+            const bool up = ((base + e) & k) == 0;
+            const bool sw = (c[f] < c[e]) == up;
+            const T x = c[e], y = c[f];
+            c[e] = sw ? y : x;
+            c[f] = sw ? x : y;
+        }
     }
 }
 
-template <int W>
-__device__ void cta_bitonic_u64(uint64_t (&c)[8], int base, CtaSortSmem<W>& S) {
+template <int W, typename T>
+__device__ void cta_bitonic(T (&c)[8], int base, T* xch) {
     constexpr int P = 256 * W;
 #pragma unroll 1
     for (int k = 2; k <= P; k <<= 1) {
@@ -373,27 +385,28 @@ __device__ void cta_bitonic_u64(uint64_t (&c)[8], int base, CtaSortSmem<W>& S) {
                 cta_inlane<2>(c, base, k);
             } else if (j == 4) {
                 cta_inlane<4>(c, base, k);
-            } else if (j < 256) {
-                const int lx = j / 8;
-#pragma unroll
-                for (int e = 0; e < 8; e++) {
-                    const uint64_t o = __shfl_xor_sync(0xffffffffu, c[e], lx);
-                    const int i = base + e;
-                    const bool keep_min = ((i & j) == 0) == ((i & k) == 0);
-                    c[e] = keep_min ? min(c[e], o) : max(c[e], o);
-                }
             } else {
+                // distance >= 8: partner slot differs in a lane/warp bit, and the
+                // keep-the-smaller decision is uniform across the thread's slots
+                const bool keep_min = ((base & j) == 0) == ((base & k) == 0);
+                if (j < 256) {
+                    const int lx = j / 8;
 #pragma unroll
-                for (int e = 0; e < 8; e++) S.xk[base + e] = c[e];
-                __syncthreads();
+                    for (int e = 0; e < 8; e++) {
+                        const T o = __shfl_xor_sync(0xffffffffu, c[e], lx);
+                        c[e] = ((o < c[e]) == keep_min) ? o : c[e];
+                    }
+                } else {
 #pragma unroll
-                for (int e = 0; e < 8; e++) {
-                    const int i = base + e;
-                    const uint64_t o = S.xk[i ^ j];
-                    const bool keep_min = ((i & j) == 0) == ((i & k) == 0);
-                    c[e] = keep_min ? min(c[e], o) : max(c[e], o);
+                    for (int e = 0; e < 8; e++) xch[base + e] = c[e];
+                    __syncthreads();
+#pragma unroll
+                    for (int e = 0; e < 8; e++) {
+                        const T o = xch[(base + e) ^ j];
+                        c[e] = ((o < c[e]) == keep_min) ? o : c[e];
+                    }
+                    __syncthreads();
                 }
-                __syncthreads();
             }
         }
     }
@@ -494,9 +507,9 @@ __global__ void __launch_bounds__(32 * W, 24 / W) k_cta_sort(
             meta[e] = ((uint32_t)i << 11) | (uint32_t)i;
         }
     }
-    bool group_mode = false;
+    bool group_mode = false, first_round = true;
     for (;;) {
-        // ---- sort by (group, word, tag): packed u64 when the bits fit ------
+        // ---- sort by (group, word, tag): packed u32/u64 when the bits fit --
         {
             uint64_t o = 0, a = ~0ull;
 #pragma unroll
@@ -511,7 +524,31 @@ __global__ void __launch_bounds__(32 * W, 24 / W) k_cta_sort(
 #pragma unroll
             for (int v = 0; v < W; v++) { o |= S.red[v]; a &= S.red[W + v]; }
             const Pext px = pext_setup(o ^ a);
-            if (px.cb <= 42) {
+            if (first_round && px.cb <= 21) {
+                // one group, no finished slots yet: (word bits | tag) in 32 bits,
+                // padding slots sort last as all-ones
+                uint32_t c[ITEMS];
+#pragma unroll
+                for (int e = 0; e < ITEMS; e++) {
+                    const uint32_t tag = meta[e] & 0x7ff;
+                    if (meta[e] >> 22 & 1) {
+                        S.kb[tag] = key[e];
+                        c[e] = ((uint32_t)pext_key(key[e], px) << 11) | tag;
+                    } else {
+                        c[e] = 0xffffffffu;
+                    }
+                }
+                __syncthreads();
+                cta_bitonic<W, uint32_t>(c, base, reinterpret_cast<uint32_t*>(S.xk));
+#pragma unroll
+                for (int e = 0; e < ITEMS; e++) {
+                    if (meta[e] >> 22 & 1) {
+                        const uint32_t tag = c[e] & 0x7ff;
+                        key[e] = S.kb[tag];
+                        meta[e] = (meta[e] & ~0x7ffu) | tag;
+                    }
+                }
+            } else if (px.cb <= 42) {
                 uint64_t c[ITEMS];
 #pragma unroll
                 for (int e = 0; e < ITEMS; e++) {
@@ -524,7 +561,7 @@ __global__ void __launch_bounds__(32 * W, 24 / W) k_cta_sort(
                     }
                 }
                 __syncthreads();
-                cta_bitonic_u64<W>(c, base, S);
+                cta_bitonic<W, uint64_t>(c, base, S.xk);
 #pragma unroll
                 for (int e = 0; e < ITEMS; e++) {
                     const uint32_t tag = (uint32_t)c[e] & 0x7ff;
@@ -616,7 +653,7 @@ __global__ void __launch_bounds__(32 * W, 24 / W) k_cta_sort(
         __syncthreads();
         uint32_t lmax = 0;
         for (int v = 0; v < W; v++) lmax = max(lmax, S.wcnt[v]);
-        if (W == 8 && lmax <= 256) {
+        if (W >= GROUP_MODE_MIN_W && lmax <= 256) {
             // ---- group mode: slot order + list of the kept runs -------------
 #pragma unroll
             for (int e = 0; e < ITEMS; e++) S.ord[base + e] = (uint16_t)(meta[e] & 0x7ff);
@@ -651,6 +688,7 @@ __global__ void __launch_bounds__(32 * W, 24 / W) k_cta_sort(
             break;
         }
         depth += WORD;
+        first_round = false;
 #pragma unroll
         for (int e = 0; e < ITEMS; e++) {
             const int i = base + e;
