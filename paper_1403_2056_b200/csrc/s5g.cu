@@ -315,16 +315,23 @@ __global__ void __launch_bounds__(1024) k_scan_buckets(
 // terminator-covering equality buckets are final: their handles go straight
 // to the output and the equality bucket's interior LCPs are written
 // (ssss.py:345-357).
-__global__ void __launch_bounds__(SC_NT) k_scatter(
+__global__ void __launch_bounds__(SC_NT, 2) k_scatter(
     const StepDev* __restrict__ steps, const int32_t* __restrict__ tile_step,
     const Rec* __restrict__ recX, const uint16_t* __restrict__ bid,
     const uint32_t* __restrict__ cnt, const uint32_t* __restrict__ tot,
     const uint32_t* __restrict__ bstart, const uint8_t* __restrict__ tpos_g,
     Rec* __restrict__ recY, int64_t* __restrict__ out_h, int64_t* __restrict__ lcps) {
+    // Per 2048-string sub-tile: (1) every thread issues coalesced loads of
+    // its 4 records and bucket ids; (2) two stable 7-bit ranking passes in
+    // shared memory order the sub-tile by bucket (the record loads are in
+    // flight meanwhile); (3) run starts give each sorted slot its offset in
+    // its bucket; (4) each thread writes its own records to their ranked
+    // destinations (whole 32-byte sectors).
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ uint32_t wsum[32];
     uint32_t* run_off = reinterpret_cast<uint32_t*>(smem);                 // NBMAX+1
-    uint16_t* rcnt = reinterpret_cast<uint16_t*>(run_off + (NBMAX + 1));   // SC_R*32
+    uint32_t* dst_by_e = run_off + (NBMAX + 1);                            // SC_SUB
+    uint16_t* rcnt = reinterpret_cast<uint16_t*>(dst_by_e + SC_SUB);       // SC_R*32
     uint16_t* kA = rcnt + SC_R * 32;
     uint16_t* vA = kA + SC_SUB;
     uint16_t* kB = vA + SC_SUB;
@@ -341,8 +348,17 @@ __global__ void __launch_bounds__(SC_NT) k_scatter(
     __syncthreads();
     for (int64_t sub = beg; sub < end; sub += SC_SUB) {
         const int m = (int)min((int64_t)SC_SUB, end - sub);
-        for (int e = threadIdx.x; e < SC_SUB; e += SC_NT) {
-            kA[e] = e < m ? bid[sub + e] : BID_SENTINEL;
+        Rec rec[SC_ITEMS];
+        uint32_t myb[SC_ITEMS];
+#pragma unroll
+        for (int i = 0; i < SC_ITEMS; i++) {
+            const int e = threadIdx.x + i * SC_NT;
+            myb[i] = BID_SENTINEL;
+            if (e < m) {
+                myb[i] = bid[sub + e];
+                rec[i] = recX[sub + e];
+            }
+            kA[e] = (uint16_t)myb[i];
             vA[e] = (uint16_t)e;
         }
         __syncthreads();
@@ -363,32 +379,35 @@ __global__ void __launch_bounds__(SC_NT) k_scatter(
 #pragma unroll
         for (int i = 0; i < SC_ITEMS; i++) {
             const int q = q0 + i;
-            if (q >= m) break;
             st[i] = (st[i] ? st[i] : before) - 1;
-            const uint32_t b = bq[i];
-            const int64_t e = sub + vA[q];
-            const uint32_t rel = run_off[b] + (q - st[i]);
+            if (q < m) dst_by_e[vA[q]] = run_off[bq[i]] + (q - st[i]);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < SC_ITEMS; i++) {
+            const int e = threadIdx.x + i * SC_NT;
+            if (e >= m) break;
+            const uint32_t b = myb[i];
+            const uint32_t rel = dst_by_e[e];
             const int64_t pos = sd.lo + rel;
-            const Rec r = recX[e];
             const uint32_t size = tot[sd.bk_off + b];
             const bool odd = b & 1;
             const int tpv = odd ? tp[b >> 1] : WORD;
             if (size == 1 || (odd && tpv < WORD)) {
-                out_h[pos] = r.h;
+                out_h[pos] = rec[i].h;
                 if (lcps && size > 1 && rel != bstart[sd.bk_off + b]) lcps[pos] = sd.depth + tpv;
             } else if (odd) {
                 // equality bucket: continues one word deeper -> shift the cache
                 Rec o;
-                o.h = r.h;
-                o.w[0] = r.w[1];
-                o.w[1] = r.w[2];
+                o.h = rec[i].h;
+                o.w[0] = rec[i].w[1];
+                o.w[1] = rec[i].w[2];
                 o.w[2] = 0;
                 recY[pos] = o;
             } else {
-                recY[pos] = r;
+                recY[pos] = rec[i];
             }
         }
-        __syncthreads();
 #pragma unroll
         for (int i = 0; i < SC_ITEMS; i++) {
             const int q = q0 + i;
@@ -675,8 +694,8 @@ static size_t carve(Workspace* w, uint8_t* base, int64_t n, int64_t t_medium) {
 static size_t smem_sample(int P, int v) { return (size_t)P * 8 + (size_t)3 * (v + 1) * 2 + 16; }
 static constexpr size_t SMEM_CLS_UNROLL = (size_t)(VMAX + 1) * 8 + (size_t)(NBMAX + 1) / 2 * 4;
 static constexpr size_t SMEM_CLS = SMEM_CLS_UNROLL + (size_t)(VMAX + 1) * 2;
-static constexpr size_t SMEM_SC = (size_t)(NBMAX + 1) * 4 + (size_t)SC_R * 32 * 2 +
-                                  (size_t)4 * SC_SUB * 2;
+static constexpr size_t SMEM_SC = (size_t)(NBMAX + 1) * 4 + (size_t)SC_SUB * 4 +
+                                  (size_t)SC_R * 32 * 2 + (size_t)4 * SC_SUB * 2;
 
 static int set_smem_attrs() {
     // per device: kernel attributes + the byte-PEXT table of the finishers
