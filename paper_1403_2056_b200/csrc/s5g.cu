@@ -48,7 +48,8 @@ __global__ void k_init(const uint8_t* __restrict__ arena, int64_t alen,
     }
 }
 
-__global__ void __launch_bounds__(SAMPLE_NT) k_sample_tree(
+template <int NT, bool BIG>
+__global__ void __launch_bounds__(NT) k_sample_tree(
     const StepDev* __restrict__ steps, const uint8_t* __restrict__ arena, int64_t alen,
     const Rec* __restrict__ recX, uint64_t seed, uint64_t* __restrict__ tree_g, uint64_t* __restrict__ inorder_g, uint8_t* __restrict__ tpos_g,
     uint16_t* __restrict__ eqb_g) {
@@ -65,7 +66,7 @@ __global__ void __launch_bounds__(SAMPLE_NT) k_sample_tree(
     // stream keyed by (seed, lo, hi, depth) -- the tuple the reference seeds
     // default_rng with; the picks never influence the output.
     const uint64_t key0 = splitmix64(seed ^ splitmix64(sd.lo ^ splitmix64(sd.n ^ splitmix64(sd.depth))));
-    for (int j = threadIdx.x; j < P; j += SAMPLE_NT) {
+    for (int j = threadIdx.x; j < P; j += NT) {
         uint64_t x = ~0ull;
         if (j < count) {
             int64_t idx = (int64_t)(splitmix64(key0 + j) % (uint64_t)sd.n);
@@ -75,8 +76,11 @@ __global__ void __launch_bounds__(SAMPLE_NT) k_sample_tree(
         s[j] = x;
     }
     __syncthreads();
-    bitonic_u64<SAMPLE_NT>(s, P);
-    select_tree<SAMPLE_NT>(s, count, v, sd.levels, sa, sb, sp, tree_g + sd.tree_off,
+    if (BIG && P == 16 * NT)
+        sort_sample16<NT>(s);  // top-level samples (16 per thread): registers + shuffles
+    else
+        bitonic_u64<NT>(s, P);  // smaller samples: shared-memory network
+    select_tree<NT>(s, count, v, sd.levels, sa, sb, sp, tree_g + sd.tree_off,
                            inorder_g + sd.tree_off, tpos_g + sd.tree_off, eqb_g + sd.tree_off);
 }
 
@@ -362,8 +366,19 @@ __global__ void __launch_bounds__(SC_NT, 2) k_scatter(
             vA[e] = (uint16_t)e;
         }
         __syncthreads();
-        rank_pass(kA, vA, kB, vB, 0, rcnt, wsum);
-        rank_pass(kB, vB, kA, vA, SC_RB, rcnt, wsum);
+        if (nb <= SC_R - 1) {
+            // few buckets (steps on small segments): one 7-bit pass suffices
+            // (the sentinel 0x3FFF has low digit 127 > any bucket id)
+            rank_pass(kA, vA, kB, vB, 0, rcnt, wsum);
+            for (int e = threadIdx.x; e < SC_SUB; e += SC_NT) {
+                kA[e] = kB[e];
+                vA[e] = vB[e];
+            }
+            __syncthreads();
+        } else {
+            rank_pass(kA, vA, kB, vB, 0, rcnt, wsum);
+            rank_pass(kB, vB, kA, vA, SC_RB, rcnt, wsum);
+        }
         // run starts in the sorted sub-tile: thread owns q = 4t .. 4t+3
         const int q0 = threadIdx.x * SC_ITEMS;
         uint32_t bq[SC_ITEMS], st[SC_ITEMS], mx = 0;
@@ -534,12 +549,25 @@ struct Profiler {
     std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev;
     std::vector<long long> units, bytes;
     explicit Profiler(cudaStream_t s) : st(s) {}
+    static std::vector<cudaEvent_t>& pool() {
+        static std::vector<cudaEvent_t> p;
+        return p;
+    }
+    static cudaEvent_t take() {
+        auto& p = pool();
+        if (p.empty()) {
+            cudaEvent_t e;
+            cudaEventCreate(&e);
+            return e;
+        }
+        cudaEvent_t e = p.back();
+        p.pop_back();
+        return e;
+    }
     int begin() {
         g_launches++;
         if (!g_prof) return -1;
-        cudaEvent_t a, b;
-        cudaEventCreate(&a);
-        cudaEventCreate(&b);
+        cudaEvent_t a = take(), b = take();
         cudaEventRecord(a, st);
         ev.push_back({-1, {a, b}});
         units.push_back(0);
@@ -568,8 +596,8 @@ struct Profiler {
                 g_prof_tab[ev[i].first].units += units[i];
                 g_prof_tab[ev[i].first].bytes += bytes[i];
             }
-            cudaEventDestroy(ev[i].second.first);
-            cudaEventDestroy(ev[i].second.second);
+            pool().push_back(ev[i].second.first);
+            pool().push_back(ev[i].second.second);
         }
         ev.clear();
         units.clear();
@@ -714,7 +742,9 @@ static int set_smem_attrs() {
             }
         CK(cudaMemcpyToSymbol(g_pext8, lut, sizeof(lut)));
     }
-    CK(cudaFuncSetAttribute(k_sample_tree, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CK(cudaFuncSetAttribute(k_sample_tree<SAMPLE_NT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)smem_sample(2 * (VMAX + 1), VMAX)));
+    CK(cudaFuncSetAttribute(k_sample_tree<256, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)smem_sample(2 * (VMAX + 1), VMAX)));
     CK(cudaFuncSetAttribute(k_select_only, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)smem_sample(2 * (VMAX + 1), VMAX)));
@@ -752,6 +782,25 @@ struct L2Granularity {
         cudaGetLastError();
     }
 };
+
+// Pinned host staging for the per-round descriptor uploads and counter /
+// segment-list downloads (async copies, one sync per round).
+struct Staging {
+    void* p = nullptr;
+    size_t cap = 0;
+    void* get(size_t bytes) {
+        if (bytes > cap) {
+            if (p) cudaFreeHost(p);
+            cap = std::max(bytes, cap * 2);
+            if (cudaMallocHost(&p, cap) != cudaSuccess) {
+                p = nullptr;
+                cap = 0;
+            }
+        }
+        return p;
+    }
+};
+static Staging g_stage_up, g_stage_down;
 
 static int sort_impl_body(const s5g_sort_args* a);
 
@@ -880,12 +929,19 @@ static int sort_impl_body(const s5g_sort_args* a) {
                 for (int b = 0; b < steps[si].nb; b += 32) cblk_step.push_back(si);
             }
             n_jobs += nsteps;
-            CK(cudaMemcpyAsync(w.steps, steps.data(), sizeof(StepDev) * nsteps,
-                               cudaMemcpyHostToDevice, st));
-            CK(cudaMemcpyAsync(w.tile_step, tile_step.data(), 4 * tile_step.size(),
-                               cudaMemcpyHostToDevice, st));
-            CK(cudaMemcpyAsync(w.tile_step + tile0, cblk_step.data(), 4 * cblk_step.size(),
-                               cudaMemcpyHostToDevice, st));
+            {
+                // previous round's uploads are complete: this round began after
+                // a stream sync, so the staging buffer can be reused
+                const size_t b1 = sizeof(StepDev) * nsteps, b2 = 4 * tile_step.size(),
+                             b3 = 4 * cblk_step.size();
+                uint8_t* up = (uint8_t*)g_stage_up.get(b1 + b2 + b3);
+                if (!up) return fail(S5G_E_CUDA, "cudaMallocHost failed");
+                memcpy(up, steps.data(), b1);
+                memcpy(up + b1, tile_step.data(), b2);
+                memcpy(up + b1 + b2, cblk_step.data(), b3);
+                CK(cudaMemcpyAsync(w.steps, up, b1, cudaMemcpyHostToDevice, st));
+                CK(cudaMemcpyAsync(w.tile_step, up + b1, b2 + b3, cudaMemcpyHostToDevice, st));
+            }
             Rec* recX = in_b ? w.recB : w.recA;
             Rec* recY = in_b ? w.recA : w.recB;
             int maxv = 1;
@@ -896,10 +952,16 @@ static int sort_impl_body(const s5g_sort_args* a) {
                 while (maxP < d.count) maxP <<= 1;
                 sample_bytes += (long long)d.count * (d.nvalid ? 8 : 16) + 27LL * d.v;
             }
-            PROF(K_SAMPLE, nsteps, sample_bytes,
-                 (k_sample_tree<<<nsteps, SAMPLE_NT, smem_sample(maxP, maxv), st>>>(
-                     w.steps, a->arena, a->arena_len, recX, a->seed, w.tree, w.inorder, w.tpos,
-                     w.eqb)));
+            if (maxP == 16 * SAMPLE_NT)
+                PROF(K_SAMPLE, nsteps, sample_bytes,
+                     (k_sample_tree<SAMPLE_NT, true><<<nsteps, SAMPLE_NT, smem_sample(maxP, maxv), st>>>(
+                         w.steps, a->arena, a->arena_len, recX, a->seed, w.tree, w.inorder, w.tpos,
+                         w.eqb)));
+            else
+                PROF(K_SAMPLE, nsteps, sample_bytes,
+                     (k_sample_tree<256, false><<<nsteps, 256, smem_sample(maxP, maxv), st>>>(
+                         w.steps, a->arena, a->arena_len, recX, a->seed, w.tree, w.inorder, w.tpos,
+                         w.eqb)));
             CK(cudaGetLastError());
             const unsigned ntiles = (unsigned)tile0;
             int64_t round_elems = 0, cls_bytes = 0;
@@ -953,15 +1015,27 @@ static int sort_impl_body(const s5g_sort_args* a) {
             }
         }
         // ---- next round's large segments ---------------------------------
-        CK(cudaMemcpyAsync(&hc, w.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
-        large.resize(hc.n_large);
-        if (hc.n_large) {
-            CK(cudaMemcpyAsync(large.data(), w.large[(round + 1) & 1], sizeof(SegDev) * hc.n_large,
+        {
+            // counters + a speculative prefix of the next round's list in one sync
+            const int64_t spec = std::min<int64_t>(w.steps_cap, 4096);
+            uint8_t* down = (uint8_t*)g_stage_down.get(sizeof(Counters) + sizeof(SegDev) * spec);
+            if (!down) return fail(S5G_E_CUDA, "cudaMallocHost failed");
+            SegDev* dl = reinterpret_cast<SegDev*>(down + sizeof(Counters));
+            CK(cudaMemcpyAsync(down, w.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
+            CK(cudaMemcpyAsync(dl, w.large[(round + 1) & 1], sizeof(SegDev) * spec,
                                cudaMemcpyDeviceToHost, st));
-            unsigned long long zero = 0;
-            CK(cudaMemcpyAsync(&w.ctr->n_large, &zero, 8, cudaMemcpyHostToDevice, st));
+            CK(cudaMemsetAsync(&w.ctr->n_large, 0, 8, st));
             CK(cudaStreamSynchronize(st));
+            memcpy(&hc, down, sizeof(Counters));
+            large.resize(hc.n_large);
+            const int64_t have = std::min<int64_t>((int64_t)hc.n_large, spec);
+            if (have) memcpy(large.data(), dl, sizeof(SegDev) * have);
+            if ((int64_t)hc.n_large > spec) {
+                CK(cudaMemcpyAsync(large.data() + spec, w.large[(round + 1) & 1] + spec,
+                                   sizeof(SegDev) * (hc.n_large - spec), cudaMemcpyDeviceToHost,
+                                   st));
+                CK(cudaStreamSynchronize(st));
+            }
         }
         in_b ^= 1;
         round++;

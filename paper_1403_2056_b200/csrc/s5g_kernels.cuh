@@ -95,6 +95,75 @@ __device__ void bitonic_u64(uint64_t* s, int P) {
         }
 }
 
+// Register bitonic of P = NT*IT keys (slot = threadIdx.x*IT + e): in-lane
+// stages below IT, shuffles below 32*IT, shared memory above.
+template <int J, int IT>
+__device__ __forceinline__ void rb_inlane(uint64_t (&c)[IT], int base, int k) {
+#pragma unroll
+    for (int e = 0; e < IT; e++) {
+        const int f = e ^ J;
+        if (f > e) {
+            const bool up = ((base + e) & k) == 0;
+            const bool sw = (c[f] < c[e]) == up;
+            const uint64_t x = c[e], y = c[f];
+            c[e] = sw ? y : x;
+            c[f] = sw ? x : y;
+        }
+    }
+}
+
+template <int IT>
+__device__ void reg_bitonic_keys(uint64_t (&c)[IT], int P, uint64_t* xch, bool cta) {
+    const int base = threadIdx.x * IT;
+#pragma unroll 1
+    for (int k = 2; k <= P; k <<= 1) {
+#pragma unroll 1
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j < IT) {
+                if (j == 1) rb_inlane<1, IT>(c, base, k);
+                else if (j == 2) rb_inlane<2, IT>(c, base, k);
+                else if (j == 4) rb_inlane<4, IT>(c, base, k);
+                else if (j == 8) rb_inlane<8, IT>(c, base, k);
+            } else {
+                const bool keep_min = ((base & j) == 0) == ((base & k) == 0);
+                if (j < 32 * IT) {
+                    const int lx = j / IT;
+#pragma unroll
+                    for (int e = 0; e < IT; e++) {
+                        const uint64_t o = __shfl_xor_sync(0xffffffffu, c[e], lx);
+                        c[e] = ((o < c[e]) == keep_min) ? o : c[e];
+                    }
+                } else {
+#pragma unroll
+                    for (int e = 0; e < IT; e++) xch[base + e] = c[e];
+                    if (cta) __syncthreads(); else __syncwarp();
+#pragma unroll
+                    for (int e = 0; e < IT; e++) {
+                        const uint64_t o = xch[(base + e) ^ j];
+                        c[e] = ((o < c[e]) == keep_min) ? o : c[e];
+                    }
+                    if (cta) __syncthreads(); else __syncwarp();
+                }
+            }
+        }
+    }
+}
+
+// Sort a full top-level sample s[0..16*NT) in place: 16 keys per thread in
+// registers; distances < 512 never touch shared memory.
+template <int NT>
+__device__ void sort_sample16(uint64_t* s) {
+    constexpr int IT = 16;
+    uint64_t c[IT];
+#pragma unroll
+    for (int e = 0; e < IT; e++) c[e] = s[threadIdx.x * IT + e];
+    __syncthreads();
+    reg_bitonic_keys<IT>(c, NT * IT, s, true);
+#pragma unroll
+    for (int e = 0; e < IT; e++) s[threadIdx.x * IT + e] = c[e];
+    __syncthreads();
+}
+
 // Sort (meta.group, key, meta.tag) lexicographically; meta = group<<16 | tag.
 template <int NT>
 __device__ void bitonic_pairs(uint64_t* key, uint32_t* meta, int P) {
