@@ -134,12 +134,17 @@ __device__ void reg_bitonic_keys(uint64_t (&c)[IT], int P, uint64_t* xch, bool c
                         c[e] = ((o < c[e]) == keep_min) ? o : c[e];
                     }
                 } else {
+                    // exchange through shared memory in [e][thread] layout: a
+                    // warp touches 32 consecutive words per access (no bank
+                    // conflicts); partner slot = same e, thread ^ (j / IT)
+                    const int nt = cta ? (int)blockDim.x : 32;
+                    const int pt = threadIdx.x ^ (j / IT);
 #pragma unroll
-                    for (int e = 0; e < IT; e++) xch[base + e] = c[e];
+                    for (int e = 0; e < IT; e++) xch[e * nt + threadIdx.x] = c[e];
                     if (cta) __syncthreads(); else __syncwarp();
 #pragma unroll
                     for (int e = 0; e < IT; e++) {
-                        const uint64_t o = xch[(base + e) ^ j];
+                        const uint64_t o = xch[e * nt + pt];
                         c[e] = ((o < c[e]) == keep_min) ? o : c[e];
                     }
                     if (cta) __syncthreads(); else __syncwarp();

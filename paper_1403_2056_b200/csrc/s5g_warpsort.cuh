@@ -397,12 +397,15 @@ __device__ void cta_bitonic(T (&c)[8], int base, T* xch) {
                         c[e] = ((o < c[e]) == keep_min) ? o : c[e];
                     }
                 } else {
+                    // [e][thread] layout: conflict-free; partner = thread ^ (j / 8)
+                    constexpr int NT = 32 * W;
+                    const int pt = threadIdx.x ^ (j / 8);
 #pragma unroll
-                    for (int e = 0; e < 8; e++) xch[base + e] = c[e];
+                    for (int e = 0; e < 8; e++) xch[e * NT + threadIdx.x] = c[e];
                     __syncthreads();
 #pragma unroll
                     for (int e = 0; e < 8; e++) {
-                        const T o = xch[(base + e) ^ j];
+                        const T o = xch[e * NT + pt];
                         c[e] = ((o < c[e]) == keep_min) ? o : c[e];
                     }
                     __syncthreads();
@@ -450,17 +453,19 @@ __device__ void cta_bitonic_generic(uint64_t (&key)[8], uint32_t (&meta)[8], int
                     }
                 }
             } else {
+                constexpr int NT = 32 * W;
+                const int pt = threadIdx.x ^ (j / 8);
 #pragma unroll
                 for (int e = 0; e < 8; e++) {
-                    S.xk[base + e] = key[e];
-                    S.xm[base + e] = meta[e];
+                    S.xk[e * NT + threadIdx.x] = key[e];
+                    S.xm[e * NT + threadIdx.x] = meta[e];
                 }
                 __syncthreads();
 #pragma unroll
                 for (int e = 0; e < 8; e++) {
                     const int i = base + e;
-                    const uint64_t ok = S.xk[i ^ j];
-                    const uint32_t om = S.xm[i ^ j];
+                    const uint64_t ok = S.xk[e * NT + pt];
+                    const uint32_t om = S.xm[e * NT + pt];
                     const bool up = (i & k) == 0, lower = (i & j) == 0;
                     if (cs_less(ok, om, key[e], meta[e]) == (lower == up)) {
                         key[e] = ok;
