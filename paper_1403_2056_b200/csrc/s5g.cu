@@ -143,8 +143,8 @@ __global__ void __launch_bounds__(CLS_NT) k_classify(
     const int t = blockIdx.x;
     const StepDev sd = steps[tile_step[t]];
     const int ti = t - (int)sd.tile0;
-    const int64_t beg = sd.lo + (int64_t)ti * TILE;
-    const int64_t end = min(beg + TILE, sd.lo + sd.n);
+    const int64_t beg = sd.lo + (int64_t)ti * sd.tile;
+    const int64_t end = min(beg + sd.tile, sd.lo + sd.n);
     const int v = sd.v, L = sd.levels, nb = sd.nb;
     const uint32_t tree_bytes = (uint32_t)(v + 1) * 8u;
     if (threadIdx.x == 0) {
@@ -343,8 +343,8 @@ __global__ void __launch_bounds__(SC_NT, 2) k_scatter(
     const int t = blockIdx.x;
     const StepDev sd = steps[tile_step[t]];
     const int ti = t - (int)sd.tile0;
-    const int64_t beg = sd.lo + (int64_t)ti * TILE;
-    const int64_t end = min(beg + TILE, sd.lo + sd.n);
+    const int64_t beg = sd.lo + (int64_t)ti * sd.tile;
+    const int64_t end = min(beg + sd.tile, sd.lo + sd.n);
     const int nb = sd.nb;
     const uint32_t* row = cnt + sd.cnt_off + (int64_t)ti * nb;
     const uint8_t* tp = tpos_g + sd.tree_off;
@@ -525,6 +525,7 @@ __global__ void k_single(const int64_t* __restrict__ handles, int64_t* __restric
 
 static thread_local std::string g_err;
 static size_t g_l2_fetch = 32;  // s5g_set_l2_fetch_granularity
+static int g_sms = 148;         // multiprocessors of the current device
 
 // ---- live per-kernel timing (CUDA events on the launching stream) --------
 enum KernelId { K_INIT, K_SAMPLE, K_CLASSIFY, K_SCAN_COLS, K_SCAN_BUCKETS, K_SCATTER, K_SEG_WARP,
@@ -684,8 +685,9 @@ static size_t carve(Workspace* w, uint8_t* base, int64_t n, int64_t t_medium) {
     const int64_t nn = std::max<int64_t>(n, 1);
     const int64_t large_min = small_max_of(t_medium) + 1;
     w->steps_cap = nn / large_min + 2;
-    w->tiles_cap = nn / TILE + w->steps_cap + 1 + (nn + 2 * w->steps_cap) / 32 + w->steps_cap;
-    w->cnt_cap = nn * ((int64_t)NBMAX / TILE + 2) + w->steps_cap * 2;
+    // big steps round their tile count up to whole waves: <= 2x the tiles
+    w->tiles_cap = 2 * (nn / TILE) + w->steps_cap + 1 + (nn + 2 * w->steps_cap) / 32 + w->steps_cap;
+    w->cnt_cap = nn * (2 * (int64_t)NBMAX / TILE + 2) + w->steps_cap * 2;
     w->bk_cap = nn + 2 * w->steps_cap;
     w->tree_cap = nn / 2 + 4 * w->steps_cap + 2;
     {
@@ -730,6 +732,7 @@ static int set_smem_attrs() {
     static unsigned long long done_mask = 0;
     int dev = 0;
     CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev));
     if (dev < 64 && (done_mask >> dev & 1ull)) return 0;
     {
         static uint8_t lut[256 * 256];
@@ -902,6 +905,13 @@ static int sort_impl_body(const s5g_sort_args* a) {
                 d.nb = 2 * d.v + 1;
                 d.nvalid = s.flags & SEG_NV_MASK;
                 d.ntiles = (int32_t)((s.n + TILE - 1) / TILE);
+                if (d.ntiles >= g_sms) {
+                    // big steps: a whole number of waves of 2 CTAs per SM
+                    const int wave = 2 * g_sms;
+                    d.ntiles = (d.ntiles + wave - 1) / wave * wave;
+                }
+                d.tile = (int32_t)((s.n + d.ntiles - 1) / d.ntiles);
+                d.ntiles = (int32_t)((s.n + d.tile - 1) / d.tile);
                 int64_t need_cnt = (int64_t)d.ntiles * d.nb;
                 if ((int64_t)steps.size() + 1 > w.steps_cap ||
                     tile0 + d.ntiles + (bk_off + d.nb) / 32 + (int64_t)steps.size() + 1 > w.tiles_cap ||

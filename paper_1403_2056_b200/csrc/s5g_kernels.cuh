@@ -49,7 +49,7 @@ struct StepDev {
     int64_t tree_off;  // first entry in tree / inorder / tpos / eqb (even)
     int64_t cblk0;     // first 32-column block of k_scan_cols
     int32_t count;     // sample size (>= v)
-    int32_t pad1;
+    int32_t tile;      // strings per classify / scatter CTA (<= TILE)
 };
 
 struct SegDev {
