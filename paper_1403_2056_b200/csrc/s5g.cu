@@ -608,6 +608,12 @@ struct Profiler {
 };
 // Algorithmic bytes per launch: what the kernel must read and write at
 // minimum, not what it happens to move.
+#define SPROF(p, kid, units_, bytes_, launch)      \
+    do {                                           \
+        int slot_ = (p).begin();                   \
+        launch;                                    \
+        (p).end(slot_, kid, (units_), (bytes_));   \
+    } while (0)
 #define PROF(kid, units_, bytes_, launch)          \
     do {                                           \
         int slot_ = prof.begin();                  \
@@ -850,12 +856,64 @@ static int sort_impl_body(const s5g_sort_args* a) {
     ClassLists cls_lists;
     for (int c = 0; c < NCLS; c++) cls_lists.off[c] = w.cls_off[c];
 
+    Counters hc{};
+    // side stream (per device, created once): finishers of earlier rounds run
+    // there concurrently with the next round's device-wide step
+    static cudaStream_t s_st2[64];
+    static cudaEvent_t s_fork[64], s_join[64];
+    int dev_id = 0;
+    CK(cudaGetDevice(&dev_id));
+    if (dev_id >= 64) return fail(S5G_E_INVALID, "device id >= 64");
+    if (!s_st2[dev_id]) {
+        CK(cudaStreamCreateWithFlags(&s_st2[dev_id], cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&s_fork[dev_id], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&s_join[dev_id], cudaEventDisableTiming));
+    }
+    cudaStream_t st2 = s_st2[dev_id];
+    cudaEvent_t ev_fork = s_fork[dev_id], ev_join = s_join[dev_id];
+    Profiler prof2(st2);
+    bool fin_side_used = false;
+    unsigned long long fin_done[NCLS] = {0}, fin_done_el[NCLS] = {0};
+    // launch the finishers for list entries [fin_done[c], hc.n_cls[c])
+    auto launch_finishers = [&](cudaStream_t fs, Profiler& fp) -> cudaError_t {
+        for (int c = 0; c < NCLS; c++) {
+            const long long cnt_c = (long long)(hc.n_cls[c] - fin_done[c]);
+            const long long el_c = (long long)(hc.cls_elems[c] - fin_done_el[c]);
+            if ((long long)hc.n_cls[c] > w.cls_cap[c]) return cudaErrorMemoryAllocation;
+            if (cnt_c <= 0) continue;
+            const unsigned grid = blocks_for(cnt_c, WS_NT / 32);
+            const SegDev* lst = w.small + w.cls_off[c] + fin_done[c];
+            switch (c) {
+                case 0: SPROF(fp, K_SEG_WARP + 0, el_c, 32LL * el_c, (k_warp_sort<1><<<grid, WS_NT, 0, fs>>>(
+                            lst, cnt_c, w.recA, w.recB, a->arena, a->arena_len, a->out_handles, lcps, w.ctr))); break;
+                case 1: SPROF(fp, K_SEG_WARP + 1, el_c, 32LL * el_c, (k_warp_sort<2><<<grid, WS_NT, 0, fs>>>(
+                            lst, cnt_c, w.recA, w.recB, a->arena, a->arena_len, a->out_handles, lcps, w.ctr))); break;
+                case 2: SPROF(fp, K_SEG_WARP + 2, el_c, 32LL * el_c, (k_warp_sort<4><<<grid, WS_NT, 0, fs>>>(
+                            lst, cnt_c, w.recA, w.recB, a->arena, a->arena_len, a->out_handles, lcps, w.ctr))); break;
+                case 3: SPROF(fp, K_SEG_WARP + 3, el_c, 32LL * el_c, (k_warp_sort<8><<<grid, WS_NT, 0, fs>>>(
+                            lst, cnt_c, w.recA, w.recB, a->arena, a->arena_len, a->out_handles, lcps, w.ctr))); break;
+                case 4: SPROF(fp, K_SEG_CTA2, el_c, 32LL * el_c, (k_cta_sort<2><<<(unsigned)cnt_c, 64,
+                            sizeof(CtaSortSmem<2>), fs>>>(lst, cnt_c, w.recA, w.recB, a->arena,
+                            a->arena_len, a->out_handles, lcps, w.ctr))); break;
+                case 5: SPROF(fp, K_SEG_CTA4, el_c, 32LL * el_c, (k_cta_sort<4><<<(unsigned)cnt_c, 128,
+                            sizeof(CtaSortSmem<4>), fs>>>(lst, cnt_c, w.recA, w.recB, a->arena,
+                            a->arena_len, a->out_handles, lcps, w.ctr))); break;
+                default: SPROF(fp, K_SEG_CTA8, el_c, 32LL * el_c, (k_cta_sort<8><<<(unsigned)cnt_c, 256,
+                            sizeof(CtaSortSmem<8>), fs>>>(lst, cnt_c, w.recA, w.recB, a->arena,
+                            a->arena_len, a->out_handles, lcps, w.ctr))); break;
+            }
+            cudaError_t e = cudaGetLastError();
+            if (e != cudaSuccess) return e;
+            fin_done[c] = hc.n_cls[c];
+            fin_done_el[c] = hc.cls_elems[c];
+        }
+        return cudaSuccess;
+    };
     CK(cudaMemsetAsync(w.ctr, 0, sizeof(Counters), st));
     PROF(K_INIT, n, 56LL * n, (k_init<<<blocks_for(n, 256), 256, 0, st>>>(a->arena, a->arena_len,
                                                                  a->handles, n, a->depth,
                                                                  w.recA)));
     CK(cudaGetLastError());
-    Counters hc{};
     hc.fetches = 0;
     int64_t n_jobs = 0;
     std::vector<SegDev> large;
@@ -1047,43 +1105,27 @@ static int sort_impl_body(const s5g_sort_args* a) {
                 CK(cudaStreamSynchronize(st));
             }
         }
+        if (hc.n_large) {
+            // this round's small segments: finish them on the side stream while
+            // the next round runs (disjoint positions; the host already synced)
+            CK(cudaEventRecord(ev_fork, st));
+            CK(cudaStreamWaitEvent(st2, ev_fork, 0));
+            CK(launch_finishers(st2, prof2));
+            fin_side_used = true;
+        }
         in_b ^= 1;
         round++;
         if (round > a->arena_len / WORD + 64) return fail(S5G_E_INVALID, "no progress: corrupt input");
     }
-    long long n_small = 0;
-    for (int c = 0; c < NCLS; c++) {
-        const long long cnt_c = (long long)hc.n_cls[c];
-        n_small += cnt_c;
-        if (cnt_c > w.cls_cap[c]) return fail(S5G_E_WORKSPACE, "small list overflow");
-        if (!cnt_c) continue;
-        const unsigned grid = blocks_for(cnt_c, WS_NT / 32);
-        const SegDev* lst = w.small + w.cls_off[c];
-        switch (c) {
-            case 0: PROF(K_SEG_WARP + 0, (long long)hc.cls_elems[0], 0, (k_warp_sort<1><<<grid, WS_NT, 0, st>>>(
-                        lst, cnt_c, w.recA, w.recB, a->arena, a->arena_len,
-                        a->out_handles, lcps, w.ctr))); break;
-            case 1: PROF(K_SEG_WARP + 1, (long long)hc.cls_elems[1], 0, (k_warp_sort<2><<<grid, WS_NT, 0, st>>>(
-                        lst, cnt_c, w.recA, w.recB, a->arena, a->arena_len,
-                        a->out_handles, lcps, w.ctr))); break;
-            case 2: PROF(K_SEG_WARP + 2, (long long)hc.cls_elems[2], 0, (k_warp_sort<4><<<grid, WS_NT, 0, st>>>(
-                        lst, cnt_c, w.recA, w.recB, a->arena, a->arena_len,
-                        a->out_handles, lcps, w.ctr))); break;
-            case 3: PROF(K_SEG_WARP + 3, (long long)hc.cls_elems[3], 0, (k_warp_sort<8><<<grid, WS_NT, 0, st>>>(
-                        lst, cnt_c, w.recA, w.recB, a->arena, a->arena_len,
-                        a->out_handles, lcps, w.ctr))); break;
-            case 4: PROF(K_SEG_CTA2, (long long)hc.cls_elems[4], 0, (k_cta_sort<2><<<(unsigned)cnt_c, 64,
-                        sizeof(CtaSortSmem<2>), st>>>(lst, cnt_c, w.recA, w.recB,
-                        a->arena, a->arena_len, a->out_handles, lcps, w.ctr))); break;
-            case 5: PROF(K_SEG_CTA4, (long long)hc.cls_elems[5], 0, (k_cta_sort<4><<<(unsigned)cnt_c, 128,
-                        sizeof(CtaSortSmem<4>), st>>>(lst, cnt_c, w.recA, w.recB,
-                        a->arena, a->arena_len, a->out_handles, lcps, w.ctr))); break;
-            default: PROF(K_SEG_CTA8, (long long)hc.cls_elems[6], 0, (k_cta_sort<8><<<(unsigned)cnt_c, 256,
-                        sizeof(CtaSortSmem<8>), st>>>(lst, cnt_c, w.recA, w.recB,
-                        a->arena, a->arena_len, a->out_handles, lcps, w.ctr))); break;
-        }
-        CK(cudaGetLastError());
+    // finishers for whatever the last round produced (earlier rounds' small
+    // segments were launched on the side stream while later rounds ran)
+    CK(launch_finishers(st, prof));
+    if (fin_side_used) {
+        CK(cudaEventRecord(ev_join, st2));
+        CK(cudaStreamWaitEvent(st, ev_join, 0));
     }
+    long long n_small = 0;
+    for (int c = 0; c < NCLS; c++) n_small += (long long)hc.n_cls[c];
     if (lcps) {
         if (hc.n_bound)
             PROF(K_BOUNDARY, (long long)hc.n_bound, 56LL * (long long)hc.n_bound,
@@ -1101,9 +1143,8 @@ static int sort_impl_body(const s5g_sort_args* a) {
     CK(cudaStreamSynchronize(st));
     // k_seg_sort: (h, key) in, (handle, lcp) out per element; (handle, word)
     // per re-keyed element
-    // register finishers: (handle, word) in, (handle, lcp) out per string, plus
-    // (handle, word) per re-keyed string; attributed to the <8> CTA class
-    prof.set_bytes(K_SEG_CTA8, 32LL * (long long)hc.small_elems + 16LL * (long long)hc.seg_fetches);
+    // register finishers: record (32 B) in per string, handle + lcp (16 B) out;
+    // modelled as 32 B/string in the launches above
     if (a->stats) {
         a->stats->word_fetches += n + (int64_t)hc.fetches + (int64_t)hc.seg_fetches;
         a->stats->jobs_enqueued += n_jobs + n_small;
