@@ -35,6 +35,22 @@ PEAKS = ROOT / "MEASURED_PEAKS.json"
 FALLBACK_HBM = 6650.0  # GB/s, B200_PROFILING.md fallback
 
 
+TRAFFIC = ROOT / "profiles" / "r01_traffic.json"
+
+
+def ncu_traffic(kernel: str):
+    """dram bytes per launch of `kernel` from the committed ncu --set full
+    capture (profiles/r01_traffic.json), or None."""
+    try:
+        d = json.loads(TRAFFIC.read_text())["kernels"]
+    except Exception:
+        return None
+    k = d.get(kernel) or d.get(kernel.replace("<", "<").strip())
+    if k is None:  # ncu names templates with their argument values
+        k = next((v for n, v in d.items() if n.split("<")[0] == kernel.split("<")[0]), None)
+    return k["dram_bytes_per_launch"] if k else None
+
+
 def hbm_peak():
     try:
         d = json.loads(PEAKS.read_text())
@@ -364,7 +380,8 @@ def run_ours(args):
                    "l2": "inputs larger than L2 (arena > 126 MB), no flush"},
         "d_bytes_per_s": D * world / (ms_step / 1000.0),
         "roofline": {"bound": "hbm", "kernel": top, "achieved": ach, "peak": peak,
-                     "unit": "GB/s", "frac": ach / peak, "traffic": None,
+                     "unit": "GB/s", "frac": ach / peak, "traffic": ncu_traffic(top),
+                     "algorithmic_bytes_per_launch": kt["bytes"] / max(1, kt["launches"]),
                      "peak_source": peak_src,
                      "share_of_step": kt["ms"] / args.steps / ms_step},
         "sort_roofline": {"b_alg_bytes": b_alg(n, D), "achieved": sort_gbs,
