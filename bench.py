@@ -190,19 +190,10 @@ def run_reference(args):
 
 
 def dist_stats_device(ds, out_h, lcps):
-    """(D, L) of the sorted set on the GPU (strset.py:290-309 convention)."""
-    import torch
+    """(D, L) of the sorted set on the GPU (s5g_dist_stats, strset.py:290-309)."""
+    from paper_1403_2056_b200 import device as DV
 
-    n = out_h.numel()
-    zeros = torch.nonzero(ds.arena[: ds.arena_len] == 0).squeeze(1)
-    ends = zeros[torch.searchsorted(zeros, out_h)]
-    lens = ends - out_h
-    h = torch.zeros(n + 1, dtype=torch.int64, device=out_h.device)
-    h[1:n] = lcps[1:]
-    neighbor = torch.maximum(h[:n], h[1:])
-    D = int(torch.minimum(lens + 1, neighbor + 1).sum())
-    L = int(lcps[1:].sum())
-    return D, L
+    return DV.dist_stats(lcps)
 
 
 def run_dist(args):

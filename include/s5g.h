@@ -135,6 +135,21 @@ int s5g_pack(const uint8_t *arena, int64_t arena_len, const int64_t *handles,
              const int64_t *lengths, const int64_t *dst_off, int64_t n, uint8_t *dst,
              void *stream);
 
+/* load_delimited (strset.py:113-134) on the device: `data` (device, len
+ * bytes, writable, readable for S5G_ARENA_PAD bytes past len with the byte at
+ * data[len] set to 0 by the caller) becomes the arena in place -- the
+ * delimiter is remapped to 0 (error if data holds a 0 byte while delimiter !=
+ * 0) -- and out_handles (device, room for len + 1 entries) receives the
+ * string starts; *out_n their count.  A trailing terminator is the caller's
+ * data[len] = 0 (the reference appends one).  Workspace: 16 + 4*ceil(len /
+ * 16384) bytes. */
+int s5g_load_delimited(uint8_t *data, int64_t len, int32_t delimiter, int64_t *out_handles,
+                       int64_t *out_n, void *workspace, size_t workspace_bytes, void *stream);
+
+/* dist_stats (strset.py:290-309) of a sorted set from its exact LCP array
+ * (device): D and L. */
+int s5g_dist_stats(const int64_t *lcps, int64_t n, int64_t *out_D, int64_t *out_L, void *stream);
+
 /* fill_dchar (basecase.py:36-42). */
 int s5g_fill_dchar(const uint8_t *arena, const int64_t *handles, const int64_t *lcps, int64_t n,
                    uint8_t *out_dchar, void *stream);

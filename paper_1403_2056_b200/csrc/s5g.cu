@@ -516,6 +516,93 @@ __global__ void k_pack(const uint8_t* __restrict__ arena, int64_t alen,
     for (int64_t b = lane; b < L; b += 32) dst[o + b] = b < L - 1 && h + b < alen ? arena[h + b] : 0;
 }
 
+// ---------------------------------------------------------------------------
+// input side: load_delimited (strset.py:113-134) on the device.  Pass 1 remaps
+// the delimiter to 0 (flagging embedded zeros) and counts terminators per
+// chunk; a single CTA scans the chunk counts; pass 2 writes the string starts.
+constexpr int LD_NT = 256, LD_CHUNK = LD_NT * 64;
+
+__global__ void k_ld_count(uint8_t* __restrict__ data, int64_t len, int delim,
+                           uint32_t* __restrict__ chunk_cnt, int* __restrict__ bad) {
+    __shared__ uint32_t wsum[32];
+    const int64_t c0 = (int64_t)blockIdx.x * LD_CHUNK;
+    uint32_t cntv = 0;
+    for (int64_t i = c0 + threadIdx.x; i < min(c0 + LD_CHUNK, len); i += LD_NT) {
+        uint8_t b = data[i];
+        if (delim != 0) {
+            if (b == 0) *bad = 1;  // input contains byte 0, reserved as terminator
+            if (b == (uint8_t)delim) { b = 0; data[i] = 0; }
+        }
+        cntv += b == 0;
+    }
+    uint32_t total;
+    block_excl_sum<LD_NT>(cntv, wsum, &total);
+    if (threadIdx.x == 0) chunk_cnt[blockIdx.x] = total;
+}
+
+__global__ void k_ld_scan(uint32_t* __restrict__ chunk_cnt, int64_t nchunks, int64_t* __restrict__ n_out) {
+    __shared__ uint32_t wsum[32];
+    constexpr int NT = 1024;
+    const int64_t per = (nchunks + NT - 1) / NT;
+    const int64_t b0 = threadIdx.x * per, b1 = min(b0 + per, nchunks);
+    uint64_t s = 0;
+    for (int64_t i = b0; i < b1; i++) s += chunk_cnt[i];
+    uint32_t total;
+    uint32_t run = block_excl_sum<NT>((uint32_t)s, wsum, &total);
+    for (int64_t i = b0; i < b1; i++) {
+        const uint32_t v = chunk_cnt[i];
+        chunk_cnt[i] = run;
+        run += v;
+    }
+    if (threadIdx.x == 0) *n_out = total;
+}
+
+// string k starts right after terminator k-1 (string 0 at offset 0)
+__global__ void k_ld_write(const uint8_t* __restrict__ data, int64_t len,
+                           const uint32_t* __restrict__ chunk_off, int64_t* __restrict__ handles) {
+    __shared__ uint32_t wsum[32];
+    const int64_t c0 = (int64_t)blockIdx.x * LD_CHUNK;
+    const int64_t per = LD_CHUNK / LD_NT;  // contiguous run per thread keeps order
+    const int64_t t0 = c0 + (int64_t)threadIdx.x * per, t1 = min(t0 + per, len);
+    uint32_t cntv = 0;
+    for (int64_t i = t0; i < t1; i++) cntv += data[i] == 0;
+    uint32_t k = chunk_off[blockIdx.x] + block_excl_sum<LD_NT>(cntv, wsum, nullptr);
+    for (int64_t i = t0; i < t1; i++)
+        if (data[i] == 0) {
+            if (k == 0) handles[0] = 0;
+            handles[k + 1] = i + 1;  // start of the next string (dropped if past the end)
+            k++;
+        }
+}
+
+// dist_stats (strset.py:290-309) from an exact LCP array: since every LCP is
+// at most the length of both its strings, D_i = max(h_i, h_{i+1}) + 1 with
+// h_0 = h_n = 0, and L = sum of lcps[1:].
+__global__ void k_dist_stats(const int64_t* __restrict__ lcps, int64_t n,
+                             unsigned long long* __restrict__ out) {
+    __shared__ unsigned long long sD[32], sL[32];
+    unsigned long long d = 0, l = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t hi = i > 0 ? lcps[i] : 0, hn = i + 1 < n ? lcps[i + 1] : 0;
+        d += (unsigned long long)(max(hi, hn) + 1);
+        l += (unsigned long long)hi;
+    }
+    for (int o = 16; o; o >>= 1) {
+        d += __shfl_xor_sync(0xffffffffu, d, o);
+        l += __shfl_xor_sync(0xffffffffu, l, o);
+    }
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (lane == 0) { sD[w] = d; sL[w] = l; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        d = l = 0;
+        for (int v = 0; v < (int)(blockDim.x / 32); v++) { d += sD[v]; l += sL[v]; }
+        atomicAdd(&out[0], d);
+        atomicAdd(&out[1], l);
+    }
+}
+
 __global__ void k_single(const int64_t* __restrict__ handles, int64_t* __restrict__ out_h) {
     out_h[0] = handles[0];
 }
@@ -1358,6 +1445,56 @@ int s5g_pack(const uint8_t* arena, int64_t arena_len, const int64_t* handles,
                                                     n, dst);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(st));
+    return 0;
+}
+
+int s5g_load_delimited(uint8_t* data, int64_t len, int32_t delimiter, int64_t* out_handles,
+                       int64_t* out_n, void* workspace, size_t workspace_bytes, void* stream) {
+    if (len < 0 || delimiter < 0 || delimiter > 255) return fail(S5G_E_INVALID, "delimiter must be a byte value");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t nchunks = (len + LD_CHUNK - 1) / LD_CHUNK;
+    if (workspace_bytes < (size_t)nchunks * 4 + 16) return fail(S5G_E_WORKSPACE, "workspace too small");
+    int* bad = (int*)workspace;
+    int64_t* d_n = (int64_t*)((uint8_t*)workspace + 8);
+    uint32_t* chunk = (uint32_t*)((uint8_t*)workspace + 16);
+    CK(cudaMemsetAsync(workspace, 0, 16, st));
+    if (len == 0) {
+        *out_n = 0;
+        return 0;
+    }
+    g_launches += 3;
+    k_ld_count<<<(unsigned)nchunks, LD_NT, 0, st>>>(data, len, delimiter, chunk, bad);
+    k_ld_scan<<<1, 1024, 0, st>>>(chunk, nchunks, d_n);
+    k_ld_write<<<(unsigned)nchunks, LD_NT, 0, st>>>(data, len, chunk, out_handles);
+    CK(cudaGetLastError());
+    int hbad = 0;
+    int64_t hn = 0;
+    CK(cudaMemcpyAsync(&hbad, bad, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&hn, d_n, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (hbad) return fail(S5G_E_INVALID, "input contains byte 0, which is reserved as terminator");
+    *out_n = hn;
+    return 0;
+}
+
+int s5g_dist_stats(const int64_t* lcps, int64_t n, int64_t* out_D, int64_t* out_L, void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (n <= 0) {
+        *out_D = *out_L = 0;
+        return n < 0 ? fail(S5G_E_INVALID, "negative n") : 0;
+    }
+    unsigned long long* d_out = nullptr;
+    CK(cudaMallocAsync((void**)&d_out, 16, st));
+    CK(cudaMemsetAsync(d_out, 0, 16, st));
+    g_launches++;
+    k_dist_stats<<<(unsigned)std::min<int64_t>(blocks_for(n, 256), 4 * 148), 256, 0, st>>>(lcps, n, d_out);
+    CK(cudaGetLastError());
+    unsigned long long h[2];
+    CK(cudaMemcpyAsync(h, d_out, 16, cudaMemcpyDeviceToHost, st));
+    CK(cudaFreeAsync(d_out, st));
+    CK(cudaStreamSynchronize(st));
+    *out_D = (int64_t)h[0];
+    *out_L = (int64_t)h[1];
     return 0;
 }
 

@@ -195,3 +195,41 @@ def pack(ds: DeviceStrings, handles: torch.Tensor, lens: torch.Tensor, dst_off: 
                          dst_off.data_ptr(), handles.numel(), dst.data_ptr(),
                          torch.cuda.current_stream().cuda_stream))
     return dst
+
+
+def load_delimited(data, delimiter: int = 0, device=None) -> DeviceStrings:
+    """load_delimited (strset.py:113-134) with the scan on the GPU: the bytes
+    are copied to HBM once and become the arena in place."""
+    if not (0 <= delimiter < 256):
+        raise ValueError("delimiter must be a byte value")
+    device = device or _require_cuda()
+    arr = data if isinstance(data, np.ndarray) else np.frombuffer(data, dtype=np.uint8)
+    L = int(arr.size)
+    if L == 0:
+        return DeviceStrings(alloc_arena(0, device), 0, torch.zeros(0, dtype=torch.int64, device=device))
+    # the reference appends a terminator unless the input already ends in the
+    # delimiter (after remapping); the arena gets room for one more byte
+    ends = int(arr[-1]) == delimiter
+    alen = L if ends else L + 1
+    arena = alloc_arena(alen, device)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        arena[:L].copy_(torch.from_numpy(arr))
+    if not ends:
+        arena[L] = delimiter  # the appended terminator (remapped to 0 with the rest)
+    handles = torch.empty(alen + 1, dtype=torch.int64, device=device)
+    nchunks = (alen + 16384 - 1) // 16384
+    ws = torch.empty(16 + 4 * nchunks, dtype=torch.uint8, device=device)
+    n = C.c_int64()
+    check(lib().s5g_load_delimited(arena.data_ptr(), alen, delimiter, handles.data_ptr(),
+                                   C.byref(n), ws.data_ptr(), ws.numel(),
+                                   torch.cuda.current_stream(device).cuda_stream))
+    return DeviceStrings(arena, alen, handles[: n.value])
+
+
+def dist_stats(lcps: torch.Tensor) -> tuple[int, int]:
+    """(D, L) of a sorted set from its exact LCP array (strset.py:290-309)."""
+    D, L = C.c_int64(), C.c_int64()
+    check(lib().s5g_dist_stats(lcps.data_ptr(), lcps.numel(), C.byref(D), C.byref(L),
+                               torch.cuda.current_stream(lcps.device).cuda_stream))
+    return int(D.value), int(L.value)
