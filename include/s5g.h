@@ -169,6 +169,11 @@ typedef struct s5g_kernel_profile {
 void s5g_profile_enable(int on);
 void s5g_profile_reset(void);
 int s5g_profile_read(s5g_kernel_profile *out, int max_entries);
+/* Launch timeline of the last sort run with profiling enabled: kernel index
+ * (into s5g_profile_read's table), stream (0 = caller's, 1 = side stream of
+ * the pipelined finishers), start / end in ms from the sort's first event.
+ * Returns the number of launches (entries beyond max_entries are dropped). */
+int s5g_profile_timeline(int *kid, int *stream, float *t0, float *t1, int max_entries);
 /* Monotonic count of kernels this library has launched (all entry points). */
 unsigned long long s5g_launch_count(void);
 /* L2 fetch granularity (bytes: 32, 64 or 128) requested for the duration of

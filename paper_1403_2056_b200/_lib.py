@@ -68,6 +68,8 @@ SIGNATURES = {
     "s5g_profile_enable": (None, [C.c_int]),
     "s5g_profile_reset": (None, []),
     "s5g_profile_read": (C.c_int, [C.POINTER(KernelProfile), C.c_int]),
+    "s5g_profile_timeline": (C.c_int, [C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                       C.POINTER(C.c_float), C.POINTER(C.c_float), C.c_int]),
     "s5g_launch_count": (C.c_ulonglong, []),
     "s5g_set_l2_fetch_granularity": (None, [C.c_int]),
     "s5g_debug_arm": (C.c_int, [_p]),
@@ -121,6 +123,19 @@ def profile(enable: bool | None = None, reset: bool = False) -> dict[str, dict]:
     return {buf[i].name.decode(): {"launches": int(buf[i].launches), "units": int(buf[i].units),
                                    "ms": float(buf[i].ms),
                                    "bytes": int(buf[i].bytes)} for i in range(k)}
+
+
+def timeline() -> list[tuple[str, int, float, float]]:
+    """(kernel, stream, start ms, end ms) of every launch of the last profiled sort."""
+    L = lib()
+    names = list(profile().keys())
+    cap = 4096
+    kid = (C.c_int * cap)()
+    sid = (C.c_int * cap)()
+    t0 = (C.c_float * cap)()
+    t1 = (C.c_float * cap)()
+    k = min(cap, L.s5g_profile_timeline(kid, sid, t0, t1, cap))
+    return [(names[kid[i]], int(sid[i]), float(t0[i]), float(t1[i])) for i in range(k)]
 
 
 def launch_count() -> int:

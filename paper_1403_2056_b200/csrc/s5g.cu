@@ -630,13 +630,22 @@ struct ProfEntry {
 };
 static bool g_prof = false;
 static ProfEntry g_prof_tab[K_COUNT];
+// timeline of the last profiled sort: (kernel id, stream, start ms, end ms)
+// relative to an event recorded on the launching stream when the sort began
+struct TimelineEntry {
+    int kid, stream;
+    float t0, t1;
+};
+static std::vector<TimelineEntry> g_timeline;
+static cudaEvent_t g_tl_base = nullptr;
 static unsigned long long g_launches = 0;
 
 struct Profiler {
     cudaStream_t st;
+    int sid;
     std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev;
     std::vector<long long> units, bytes;
-    explicit Profiler(cudaStream_t s) : st(s) {}
+    explicit Profiler(cudaStream_t s, int id = 0) : st(s), sid(id) {}
     static std::vector<cudaEvent_t>& pool() {
         static std::vector<cudaEvent_t> p;
         return p;
@@ -678,6 +687,12 @@ struct Profiler {
         for (size_t i = 0; i < ev.size(); i++) {
             float ms = 0;
             cudaEventElapsedTime(&ms, ev[i].second.first, ev[i].second.second);
+            if (ev[i].first >= 0 && g_tl_base) {
+                float t0 = 0, t1 = 0;
+                cudaEventElapsedTime(&t0, g_tl_base, ev[i].second.first);
+                cudaEventElapsedTime(&t1, g_tl_base, ev[i].second.second);
+                g_timeline.push_back({ev[i].first, sid, t0, t1});
+            }
             if (ev[i].first >= 0) {
                 g_prof_tab[ev[i].first].launches++;
                 g_prof_tab[ev[i].first].ms += ms;
@@ -933,6 +948,11 @@ static int sort_impl_body(const s5g_sort_args* a) {
         CK(cudaStreamSynchronize(st));
         return 0;
     }
+    if (g_prof) {
+        if (!g_tl_base) CK(cudaEventCreate(&g_tl_base));
+        g_timeline.clear();
+        CK(cudaEventRecord(g_tl_base, st));
+    }
     Profiler prof(st);
     Workspace w;
     size_t need = carve(&w, nullptr, n, t_medium);
@@ -958,7 +978,7 @@ static int sort_impl_body(const s5g_sort_args* a) {
     }
     cudaStream_t st2 = s_st2[dev_id];
     cudaEvent_t ev_fork = s_fork[dev_id], ev_join = s_join[dev_id];
-    Profiler prof2(st2);
+    Profiler prof2(st2, 1);
     bool fin_side_used = false;
     unsigned long long fin_done[NCLS] = {0}, fin_done_el[NCLS] = {0};
     // launch the finishers for list entries [fin_done[c], hc.n_cls[c])
@@ -968,16 +988,17 @@ static int sort_impl_body(const s5g_sort_args* a) {
             const long long el_c = (long long)(hc.cls_elems[c] - fin_done_el[c]);
             if ((long long)hc.n_cls[c] > w.cls_cap[c]) return cudaErrorMemoryAllocation;
             if (cnt_c <= 0) continue;
-            const unsigned grid = blocks_for(cnt_c, WS_NT / 32);
+            const int wnt = ws_nt(c == 0 ? 1 : c == 1 ? 2 : c == 2 ? 4 : 8);
+            const unsigned grid = blocks_for(cnt_c, wnt / 32);
             const SegDev* lst = w.small + w.cls_off[c] + fin_done[c];
             switch (c) {
-                case 0: SPROF(fp, K_SEG_WARP + 0, el_c, 32LL * el_c, (k_warp_sort<1><<<grid, WS_NT, 0, fs>>>(
+                case 0: SPROF(fp, K_SEG_WARP + 0, el_c, 32LL * el_c, (k_warp_sort<1><<<grid, wnt, 0, fs>>>(
                             lst, cnt_c, w.recA, w.recB, a->arena, a->arena_len, a->out_handles, lcps, w.ctr))); break;
-                case 1: SPROF(fp, K_SEG_WARP + 1, el_c, 32LL * el_c, (k_warp_sort<2><<<grid, WS_NT, 0, fs>>>(
+                case 1: SPROF(fp, K_SEG_WARP + 1, el_c, 32LL * el_c, (k_warp_sort<2><<<grid, wnt, 0, fs>>>(
                             lst, cnt_c, w.recA, w.recB, a->arena, a->arena_len, a->out_handles, lcps, w.ctr))); break;
-                case 2: SPROF(fp, K_SEG_WARP + 2, el_c, 32LL * el_c, (k_warp_sort<4><<<grid, WS_NT, 0, fs>>>(
+                case 2: SPROF(fp, K_SEG_WARP + 2, el_c, 32LL * el_c, (k_warp_sort<4><<<grid, wnt, 0, fs>>>(
                             lst, cnt_c, w.recA, w.recB, a->arena, a->arena_len, a->out_handles, lcps, w.ctr))); break;
-                case 3: SPROF(fp, K_SEG_WARP + 3, el_c, 32LL * el_c, (k_warp_sort<8><<<grid, WS_NT, 0, fs>>>(
+                case 3: SPROF(fp, K_SEG_WARP + 3, el_c, 32LL * el_c, (k_warp_sort<8><<<grid, wnt, 0, fs>>>(
                             lst, cnt_c, w.recA, w.recB, a->arena, a->arena_len, a->out_handles, lcps, w.ctr))); break;
                 case 4: SPROF(fp, K_SEG_CTA2, el_c, 32LL * el_c, (k_cta_sort<2><<<(unsigned)cnt_c, 64,
                             sizeof(CtaSortSmem<2>), fs>>>(lst, cnt_c, w.recA, w.recB, a->arena,
@@ -1267,6 +1288,19 @@ int s5g_profile_read(s5g_kernel_profile* out, int max_entries) {
         out[k].bytes = g_prof_tab[i].bytes;
     }
     return k;
+}
+
+int s5g_profile_timeline(int* kid, int* stream, float* t0, float* t1, int max_entries) {
+    int k = 0;
+    for (const auto& e : g_timeline) {
+        if (k >= max_entries) break;
+        kid[k] = e.kid;
+        stream[k] = e.stream;
+        t0[k] = e.t0;
+        t1[k] = e.t1;
+        k++;
+    }
+    return (int)g_timeline.size();
 }
 
 unsigned long long s5g_launch_count(void) { return g_launches; }

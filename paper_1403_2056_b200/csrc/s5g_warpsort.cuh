@@ -32,32 +32,46 @@ __device__ __forceinline__ bool cs_less(uint64_t ka, uint32_t ma, uint64_t kb, u
 }
 
 struct Pext {
-    uint64_t V;
-    int cb;
-    int sh[8];
+    uint64_t V;   // varying-bit mask
+    uint64_t SH;  // 6-bit shift of byte b's extracted bits at 6b
+    int cb;       // popcount(V)
 };
 
 __device__ __forceinline__ Pext pext_setup(uint64_t V) {
     Pext p;
     p.V = V;
     p.cb = __popcll(V);
+    uint64_t sh = 0;
     int acc = 0;
 #pragma unroll
     for (int b = 0; b < 8; b++) {
-        p.sh[b] = acc;
+        sh |= (uint64_t)acc << (6 * b);
         acc += __popc((uint32_t)(V >> (8 * b)) & 255u);
     }
+    p.SH = sh;
     return p;
 }
 
+// Bit-extract of x under the CTA-uniform mask V, byte-wise through a 256x256
+// table.  Callers run it in ONE rolled loop over the slots staged in shared
+// memory: inlined per register slot it was a third of the finishers' code.
 __device__ __forceinline__ uint64_t pext_key(uint64_t x, const Pext& p) {
     uint64_t c = 0;
 #pragma unroll
     for (int b = 0; b < 8; b++) {
         const uint32_t m = (uint32_t)(p.V >> (8 * b)) & 255u;
-        if (m) c |= (uint64_t)__ldg(&g_pext8[m * 256 + ((uint32_t)(x >> (8 * b)) & 255u)]) << p.sh[b];
+        if (m)
+            c |= (uint64_t)__ldg(&g_pext8[m * 256 + ((uint32_t)(x >> (8 * b)) & 255u)])
+                 << ((p.SH >> (6 * b)) & 63);
     }
     return c;
+}
+
+// Arena gather beyond the cached words: one out-of-line copy instead of one
+// per inlined slot (instruction-cache footprint of the finishers).
+__device__ __noinline__ uint64_t load_key_far(const uint8_t* __restrict__ arena, int64_t alen,
+                                              int64_t h, int64_t depth) {
+    return load_key(arena, alen, h, depth);
 }
 
 // Word at `depth` of the segment's string `tag`: from its work record while
@@ -69,7 +83,7 @@ __device__ __forceinline__ uint64_t seg_word(const Rec* __restrict__ segrec, uin
     const int64_t r = (depth - d0) >> 3;
     if (r < nv) return segrec[tag].w[r];
     fetches++;
-    return load_key(arena, alen, h, depth);
+    return load_key_far(arena, alen, h, depth);
 }
 
 __device__ __forceinline__ void cex_u64(uint64_t& a, uint64_t& b, bool up) {
@@ -82,28 +96,42 @@ __device__ __forceinline__ void cex_u64(uint64_t& a, uint64_t& b, bool up) {
 // ---------------------------------------------------------------------------
 // warp-level networks over 32*IT slots (slot = lane*IT + e)
 
+// In-lane stage at compile-time distance J < IT (direction varies with e
+// while k < IT).  The stage loops below are NOT unrolled over (k, j): the
+// finishers inline several of these networks, and fully unrolled they
+// overflow the instruction cache (ncu: "no instruction" was the top stall).
+template <int J, int IT>
+__device__ __forceinline__ void warp_inlane_u64(uint64_t (&c)[IT], int i0, int k) {
+#pragma unroll
+    for (int e = 0; e < IT; e++) {
+        const int f = e ^ J;
+        if (f > e) cex_u64(c[e], c[f], ((i0 + e) & k) == 0);
+    }
+}
+
 template <int IT>
 __device__ __forceinline__ void warp_bitonic_u64(uint64_t (&c)[IT], int lane) {
     constexpr int P = 32 * IT;
-#pragma unroll
+    const int i0 = lane * IT;
+#pragma unroll 1
     for (int k = 2; k <= P; k <<= 1) {
-#pragma unroll
+#pragma unroll 1
         for (int j = k >> 1; j > 0; j >>= 1) {
-            if (j < IT) {
-#pragma unroll
-                for (int e = 0; e < IT; e++) {
-                    const int f = e ^ j;
-                    if (f > e) cex_u64(c[e], c[f], ((lane * IT + e) & k) == 0);
-                }
-            } else {
+            if (j >= IT) {
+                // partner in another lane; direction uniform over e
                 const int lx = j / IT;
-                const int i0 = lane * IT;  // j >= IT: direction uniform over e
                 const bool keep_min = ((i0 & j) == 0) == ((i0 & k) == 0);
 #pragma unroll
                 for (int e = 0; e < IT; e++) {
                     const uint64_t o = __shfl_xor_sync(0xffffffffu, c[e], lx);
                     c[e] = ((o < c[e]) == keep_min) ? o : c[e];
                 }
+            } else if (j == 1) {
+                if constexpr (IT > 1) warp_inlane_u64<1, IT>(c, i0, k);
+            } else if (j == 2) {
+                if constexpr (IT > 2) warp_inlane_u64<2, IT>(c, i0, k);
+            } else {
+                if constexpr (IT > 4) warp_inlane_u64<4, IT>(c, i0, k);
             }
         }
     }
@@ -113,19 +141,23 @@ template <int IT>
 __device__ __forceinline__ void warp_bitonic_generic(uint64_t (&key)[IT], uint32_t (&meta)[IT],
                                                      int lane) {
     constexpr int P = 32 * IT;
-#pragma unroll
+#pragma unroll 1
     for (int k = 2; k <= P; k <<= 1) {
-#pragma unroll
+#pragma unroll 1
         for (int j = k >> 1; j > 0; j >>= 1) {
             if (j < IT) {
 #pragma unroll
                 for (int e = 0; e < IT; e++) {
-                    const int f = e ^ j;
-                    if (f > e) {
-                        const bool up = ((lane * IT + e) & k) == 0;
-                        if (cs_less(key[f], meta[f], key[e], meta[e]) == up) {
-                            uint64_t tk = key[e]; key[e] = key[f]; key[f] = tk;
-                            uint32_t tm = meta[e]; meta[e] = meta[f]; meta[f] = tm;
+#pragma unroll
+                    for (int jj = 1; jj < IT; jj <<= 1) {
+                        if (jj != j) continue;
+                        const int f = e ^ jj;
+                        if (f > e) {
+                            const bool up = ((lane * IT + e) & k) == 0;
+                            if (cs_less(key[f], meta[f], key[e], meta[e]) == up) {
+                                uint64_t tk = key[e]; key[e] = key[f]; key[f] = tk;
+                                uint32_t tm = meta[e]; meta[e] = meta[f]; meta[f] = tm;
+                            }
                         }
                     }
                 }
@@ -165,7 +197,8 @@ __device__ __forceinline__ uint64_t warp_and64(uint64_t x) {
 // interior and the final tag order back to ord[g0 ..].
 template <int IT>
 __device__ void warp_finish(const int64_t* __restrict__ hbt, uint16_t* __restrict__ ord,
-                            uint64_t* __restrict__ kb, const Rec* __restrict__ segrec, int64_t d0,
+                            uint64_t* __restrict__ kb, uint64_t* __restrict__ xs,
+                            const Rec* __restrict__ segrec, int64_t d0,
                             int nv, int g0, int gn, int64_t depth, uint64_t (&key)[IT],
                             const uint8_t* __restrict__ arena, int64_t alen,
                             int64_t* __restrict__ lcp_seg, unsigned& fetches, int lane) {
@@ -190,16 +223,24 @@ __device__ void warp_finish(const int64_t* __restrict__ hbt, uint16_t* __restric
             if (meta[e] >> 22 & 1) { o |= key[e]; a &= key[e]; }
         const Pext px = pext_setup(warp_or64(o) ^ warp_and64(a));
         if (px.cb <= 45) {
+            // words by tag (kb) and by slot (xs, packed in one rolled loop)
+#pragma unroll
+            for (int e = 0; e < IT; e++) {
+                const int i = lane * IT + e;
+                if (meta[e] >> 22 & 1) kb[meta[e] & 0x7ff] = key[e];
+                if (i < gn) xs[g0 + i] = key[e];
+            }
+            __syncwarp();
+            for (int q = lane; q < gn; q += 32) xs[g0 + q] = pext_key(xs[g0 + q], px);
+            __syncwarp();
             uint64_t c[IT];
 #pragma unroll
             for (int e = 0; e < IT; e++) {
                 const uint32_t tag = meta[e] & 0x7ff;
-                if (meta[e] >> 22 & 1) {
-                    kb[tag] = key[e];
-                    c[e] = ((uint64_t)(meta[e] >> 11 & 0xff) << 56) | (pext_key(key[e], px) << 11) | tag;
-                } else {
+                if (meta[e] >> 22 & 1)
+                    c[e] = ((uint64_t)(meta[e] >> 11 & 0xff) << 56) | (xs[g0 + lane * IT + e] << 11) | tag;
+                else
                     c[e] = ((uint64_t)(lane * IT + e) << 56) | tag;
-                }
             }
             __syncwarp();
             warp_bitonic_u64<IT>(c, lane);
@@ -287,20 +328,23 @@ __device__ void warp_finish(const int64_t* __restrict__ hbt, uint16_t* __restric
 // ---------------------------------------------------------------------------
 // k_warp_sort: one warp per segment of <= 32*ITEMS strings
 
-constexpr int WS_NT = 256;  // 8 warps per CTA, one segment per warp
+// one segment per warp; 8 warps per CTA (4 for 256-string segments, whose
+// per-warp staging would exceed the 48 KB of static shared memory)
+__host__ __device__ constexpr int ws_nt(int items) { return items >= 8 ? 128 : 256; }
 #ifndef GROUP_MODE_MIN_W
 #define GROUP_MODE_MIN_W 8
 #endif
 
 template <int ITEMS>
-__global__ void __launch_bounds__(WS_NT) k_warp_sort(
+__global__ void __launch_bounds__(ws_nt(ITEMS)) k_warp_sort(
     const SegDev* __restrict__ segs, int64_t nsegs, const Rec* __restrict__ recA,
     const Rec* __restrict__ recB, const uint8_t* __restrict__ arena, int64_t alen,
     int64_t* __restrict__ out_h, int64_t* __restrict__ lcps, Counters* __restrict__ ctr) {
-    constexpr int CAP = 32 * ITEMS;
+    constexpr int CAP = 32 * ITEMS, WS_NT = ws_nt(ITEMS);
     __shared__ int64_t s_h[WS_NT / 32][CAP];
     __shared__ uint64_t s_k[WS_NT / 32][CAP];
     __shared__ uint16_t s_o[WS_NT / 32][CAP];
+    __shared__ uint64_t s_x[WS_NT / 32][CAP];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int64_t gw = (int64_t)blockIdx.x * (WS_NT / 32) + w;
     if (gw >= nsegs) return;  // whole warp
@@ -322,7 +366,7 @@ __global__ void __launch_bounds__(WS_NT) k_warp_sort(
     }
     __syncwarp();
     uint64_t key[ITEMS];
-    warp_finish<ITEMS>(wh, wo, s_k[w], segrec, sg.depth, nv, 0, m, sg.depth, key, arena, alen,
+    warp_finish<ITEMS>(wh, wo, s_k[w], s_x[w], segrec, sg.depth, nv, 0, m, sg.depth, key, arena, alen,
                        lcps ? lcps + lo : nullptr, fetches, lane);
     __syncwarp();
 #pragma unroll
@@ -347,11 +391,18 @@ struct CtaSortSmem {
     int64_t h[256 * W];           // handle by tag
     uint64_t kb[256 * W];         // word by tag (composite rounds, warp runs)
     uint64_t xk[256 * W];         // cross-warp exchange
-    uint32_t xm[256 * W];
-    uint16_t ord[256 * W];        // tag at slot
-    uint16_t gs[128 * W], ge[128 * W];  // first / last slot of each remaining run
-    uint64_t red[2 * W];
-    uint64_t last_key[W];
+    union {
+        // the two-word first round keeps the second word by tag here; the
+        // generic exchange, the slot order and the run list come later
+        uint64_t kb1[256 * W];
+        struct {
+            uint32_t xm[256 * W];
+            uint16_t ord[256 * W];        // tag at slot
+            uint16_t gs[128 * W], ge[128 * W];  // first / last slot of each remaining run
+        };
+    };
+    uint64_t red[4 * W];
+    uint64_t last_key[W], last_key1[W];
     uint32_t first_brk[W], first_act[W], wmax[W], wcnt[W];
 };
 
@@ -513,90 +564,167 @@ __global__ void __launch_bounds__(32 * W, 24 / W) k_cta_sort(
         }
     }
     bool group_mode = false, first_round = true;
+    uint64_t k1[ITEMS];  // second word of the slot in a two-word round
     for (;;) {
         // ---- sort by (group, word, tag): packed u32/u64 when the bits fit --
+        bool two = false;  // this round sorts by the words at depth and depth + 8
         {
-            uint64_t o = 0, a = ~0ull;
+            // the first round may take the record's second cached word along
+            // when both words' varying bits fit one u64 beside the tag: one
+            // round instead of two for low-entropy keys (DNA: 4 bits/char)
+            const bool try_two = first_round && nv >= 2;
+            uint64_t o = 0, a = ~0ull, o1 = 0, a1 = ~0ull;
 #pragma unroll
-            for (int e = 0; e < ITEMS; e++)
-                if (meta[e] >> 22 & 1) { o |= key[e]; a &= key[e]; }
+            for (int e = 0; e < ITEMS; e++) {
+                k1[e] = 0;
+                if (meta[e] >> 22 & 1) {
+                    o |= key[e];
+                    a &= key[e];
+                    if (try_two) {
+                        k1[e] = segrec[base + e].w[1];
+                        o1 |= k1[e];
+                        a1 &= k1[e];
+                    }
+                }
+            }
             o = warp_or64(o);
             a = warp_and64(a);
-            if (lane == 0) { S.red[w] = o; S.red[W + w] = a; }
+            if (try_two) {
+                o1 = warp_or64(o1);
+                a1 = warp_and64(a1);
+            }
+            if (lane == 0) { S.red[w] = o; S.red[W + w] = a; S.red[2 * W + w] = o1; S.red[3 * W + w] = a1; }
             __syncthreads();
             o = 0;
             a = ~0ull;
+            o1 = 0;
+            a1 = ~0ull;
 #pragma unroll
-            for (int v = 0; v < W; v++) { o |= S.red[v]; a &= S.red[W + v]; }
+            for (int v = 0; v < W; v++) {
+                o |= S.red[v];
+                a &= S.red[W + v];
+                o1 |= S.red[2 * W + v];
+                a1 &= S.red[3 * W + v];
+            }
             const Pext px = pext_setup(o ^ a);
-            if (first_round && px.cb <= 21) {
-                // one group, no finished slots yet: (word bits | tag) in 32 bits,
-                // padding slots sort last as all-ones
-                uint32_t c[ITEMS];
+            if (try_two) {
+                const int cb1 = __popcll(o1 ^ a1);
+                // u32 single-word rounds are cheaper unless ties are likely
+                two = px.cb + cb1 <= 53 && (px.cb > 21 || (1u << px.cb) < 64u * (uint32_t)m);
+                if (!two) {
+#pragma unroll
+                    for (int e = 0; e < ITEMS; e++) k1[e] = 0;  // single-word round
+                }
+            }
+            const int mode = two ? 0 : (first_round && px.cb <= 21) ? 1 : (px.cb <= 42) ? 2 : 3;
+            if (mode != 3) {
+                // stage the words by tag (kb, kb1) and by slot (xk), pack the
+                // varying bits of every slot in one rolled loop, build the
+                // sort values: two-word (word0 bits | word1 bits | tag), u32
+                // (word bits | tag) on the first round, else (group | bits | tag)
+                const Pext px1 = pext_setup(o1 ^ a1);
 #pragma unroll
                 for (int e = 0; e < ITEMS; e++) {
                     const uint32_t tag = meta[e] & 0x7ff;
                     if (meta[e] >> 22 & 1) {
                         S.kb[tag] = key[e];
-                        c[e] = ((uint32_t)pext_key(key[e], px) << 11) | tag;
-                    } else {
-                        c[e] = 0xffffffffu;
+                        if (two) S.kb1[tag] = k1[e];  // tag == slot in the first round
                     }
+                    S.xk[base + e] = key[e];
                 }
                 __syncthreads();
-                cta_bitonic<W, uint32_t>(c, base, reinterpret_cast<uint32_t*>(S.xk));
-#pragma unroll
-                for (int e = 0; e < ITEMS; e++) {
-                    if (meta[e] >> 22 & 1) {
-                        const uint32_t tag = c[e] & 0x7ff;
-                        key[e] = S.kb[tag];
-                        meta[e] = (meta[e] & ~0x7ffu) | tag;
-                    }
-                }
-            } else if (px.cb <= 42) {
-                uint64_t c[ITEMS];
-#pragma unroll
-                for (int e = 0; e < ITEMS; e++) {
-                    const uint32_t tag = meta[e] & 0x7ff;
-                    if (meta[e] >> 22 & 1) {
-                        S.kb[tag] = key[e];
-                        c[e] = ((uint64_t)(meta[e] >> 11 & 0x7ff) << 53) | (pext_key(key[e], px) << 11) | tag;
-                    } else {
-                        c[e] = ((uint64_t)(base + e) << 53) | tag;
-                    }
+                const int lim = first_round ? m : 256 * W;
+                for (int q = threadIdx.x; q < lim; q += NT) {
+                    uint64_t v = pext_key(S.xk[q], px);
+                    if (two) v = (v << px1.cb) | pext_key(S.kb1[q], px1);
+                    S.xk[q] = v;
                 }
                 __syncthreads();
-                cta_bitonic<W, uint64_t>(c, base, S.xk);
+                if (mode == 1) {
+                    uint32_t c[ITEMS];
 #pragma unroll
-                for (int e = 0; e < ITEMS; e++) {
-                    const uint32_t tag = (uint32_t)c[e] & 0x7ff;
-                    if (meta[e] >> 22 & 1) key[e] = S.kb[tag];
-                    meta[e] = (meta[e] & ~0x7ffu) | tag;
+                    for (int e = 0; e < ITEMS; e++) {
+                        const uint32_t tag = meta[e] & 0x7ff;
+                        c[e] = (meta[e] >> 22 & 1) ? (((uint32_t)S.xk[base + e] << 11) | tag) : 0xffffffffu;
+                    }
+                    __syncthreads();  // xk becomes the exchange buffer
+                    cta_bitonic<W, uint32_t>(c, base, reinterpret_cast<uint32_t*>(S.xk));
+#pragma unroll
+                    for (int e = 0; e < ITEMS; e++) {
+                        if (meta[e] >> 22 & 1) {
+                            const uint32_t tag = c[e] & 0x7ff;
+                            key[e] = S.kb[tag];
+                            meta[e] = (meta[e] & ~0x7ffu) | tag;
+                        }
+                    }
+                } else {
+                    uint64_t c[ITEMS];
+#pragma unroll
+                    for (int e = 0; e < ITEMS; e++) {
+                        const uint32_t tag = meta[e] & 0x7ff;
+                        if (mode == 0)
+                            c[e] = (meta[e] >> 22 & 1) ? ((S.xk[base + e] << 11) | tag) : ~0ull;
+                        else
+                            c[e] = (meta[e] >> 22 & 1)
+                                       ? (((uint64_t)(meta[e] >> 11 & 0x7ff) << 53) | (S.xk[base + e] << 11) | tag)
+                                       : (((uint64_t)(base + e) << 53) | tag);
+                    }
+                    __syncthreads();  // xk becomes the exchange buffer
+                    cta_bitonic<W, uint64_t>(c, base, S.xk);
+#pragma unroll
+                    for (int e = 0; e < ITEMS; e++) {
+                        const uint32_t tag = (uint32_t)c[e] & 0x7ff;
+                        if (meta[e] >> 22 & 1) {
+                            key[e] = S.kb[tag];
+                            if (two) k1[e] = S.kb1[tag];
+                        }
+                        if (mode == 0) {
+                            if (meta[e] >> 22 & 1) meta[e] = (meta[e] & ~0x7ffu) | tag;
+                        } else {
+                            meta[e] = (meta[e] & ~0x7ffu) | tag;
+                        }
+                    }
                 }
             } else {
                 cta_bitonic_generic<W>(key, meta, base, S);
             }
         }
         // ---- LCPs at word changes, run breaks -------------------------------
+        // (a two-word round compares (word, word1); a string whose first word
+        // holds its terminator has word1 = 0, so pair equality is string
+        // equality within the 16-character window)
+        const int step = two ? 2 * WORD : WORD;
         uint64_t prev_last = __shfl_up_sync(0xffffffffu, key[ITEMS - 1], 1);
-        if (lane == 31) S.last_key[w] = key[ITEMS - 1];
+        uint64_t prev_last1 = __shfl_up_sync(0xffffffffu, k1[ITEMS - 1], 1);
+        if (lane == 31) {
+            S.last_key[w] = key[ITEMS - 1];
+            S.last_key1[w] = k1[ITEMS - 1];
+        }
         __syncthreads();
-        if (lane == 0 && w > 0) prev_last = S.last_key[w - 1];
+        if (lane == 0 && w > 0) {
+            prev_last = S.last_key[w - 1];
+            prev_last1 = S.last_key1[w - 1];
+        }
         bool brk[ITEMS];
+        int tw[ITEMS];  // terminator position in the round's window (step if none)
 #pragma unroll
         for (int e = 0; e < ITEMS; e++) {
             const int i = base + e;
             const bool act = meta[e] >> 22 & 1;
             const int grp = meta[e] >> 11 & 0x7ff;
             brk[e] = true;
+            tw[e] = term_pos(key[e]);
+            if (two && tw[e] == WORD) tw[e] = WORD + term_pos(k1[e]);
             if (act && i != grp) {
                 const uint64_t pk = e ? key[e - 1] : prev_last;
+                const uint64_t pk1 = e ? k1[e - 1] : prev_last1;
                 if (pk != key[e]) {
                     if (lcp_seg) lcp_seg[i] = depth + (__clzll(pk ^ key[e]) >> 3);
+                } else if (pk1 != k1[e]) {  // two-word round only
+                    if (lcp_seg) lcp_seg[i] = depth + WORD + (__clzll(pk1 ^ k1[e]) >> 3);
                 } else {
                     brk[e] = false;
-                    const int tpv = term_pos(key[e]);
-                    if (lcp_seg && tpv < WORD) lcp_seg[i] = depth + tpv;
+                    if (lcp_seg && tw[e] < step) lcp_seg[i] = depth + tw[e];
                 }
             }
         }
@@ -626,7 +754,7 @@ __global__ void __launch_bounds__(32 * W, 24 / W) k_cta_sort(
                 nb = next_brk0;
                 na = next_act0;
             }
-            keep[e] = act && term_pos(key[e]) == WORD && (!brk[e] || (na && !nb));
+            keep[e] = act && tw[e] == step && (!brk[e] || (na && !nb));
             kend[e] = keep[e] && (!na || nb);  // last slot of a kept run
             any |= keep[e];
             if (keep[e] && brk[e]) { run = i + 1; nstart++; }
@@ -690,9 +818,10 @@ __global__ void __launch_bounds__(32 * W, 24 / W) k_cta_sort(
             if (threadIdx.x == 0) S.wcnt[0] = tot2 & 0xffff;
             __syncthreads();
             group_mode = true;
+            depth += step;
             break;
         }
-        depth += WORD;
+        depth += step;
         first_round = false;
 #pragma unroll
         for (int e = 0; e < ITEMS; e++) {
@@ -717,19 +846,19 @@ __global__ void __launch_bounds__(32 * W, 24 / W) k_cta_sort(
         const uint32_t ngroups = S.wcnt[0];
         for (uint32_t g = w; g < ngroups; g += W) {
             const int g0 = S.gs[g], gn = S.ge[g] - g0 + 1;
-            const int64_t d = depth + WORD;
+            const int64_t d = depth;
             if (gn <= 32) {
                 uint64_t k1[1];
-                warp_finish<1>(S.h, S.ord, S.kb, segrec, d0, nv, g0, gn, d, k1, arena, alen, lcp_seg, fetches, lane);
+                warp_finish<1>(S.h, S.ord, S.kb, S.xk, segrec, d0, nv, g0, gn, d, k1, arena, alen, lcp_seg, fetches, lane);
             } else if (gn <= 64) {
                 uint64_t k2[2];
-                warp_finish<2>(S.h, S.ord, S.kb, segrec, d0, nv, g0, gn, d, k2, arena, alen, lcp_seg, fetches, lane);
+                warp_finish<2>(S.h, S.ord, S.kb, S.xk, segrec, d0, nv, g0, gn, d, k2, arena, alen, lcp_seg, fetches, lane);
             } else if (gn <= 128) {
                 uint64_t k4[4];
-                warp_finish<4>(S.h, S.ord, S.kb, segrec, d0, nv, g0, gn, d, k4, arena, alen, lcp_seg, fetches, lane);
+                warp_finish<4>(S.h, S.ord, S.kb, S.xk, segrec, d0, nv, g0, gn, d, k4, arena, alen, lcp_seg, fetches, lane);
             } else {
                 uint64_t k8[8];
-                warp_finish<8>(S.h, S.ord, S.kb, segrec, d0, nv, g0, gn, d, k8, arena, alen, lcp_seg, fetches, lane);
+                warp_finish<8>(S.h, S.ord, S.kb, S.xk, segrec, d0, nv, g0, gn, d, k8, arena, alen, lcp_seg, fetches, lane);
             }
         }
     }
