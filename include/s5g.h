@@ -180,10 +180,11 @@ unsigned long long s5g_launch_count(void);
  * each sort (cudaLimitMaxL2FetchGranularity; restored afterwards).  Default 32:
  * the sort is dominated by random 8-byte gathers and stores. */
 void s5g_set_l2_fetch_granularity(int bytes);
-/* Debug: per-CTA trace of the small-segment sorter (5 x uint64 per CTA:
- * cycles, size, rounds, active elements over rounds, radix passes) into a
- * device buffer; NULL disarms. */
-int s5g_debug_arm(void *dev_buf);
+/* Finisher counters accumulated over all sorts on the current device since
+ * the last reset: for k_cta_sort<2>, <4>, <8> (entries 4c .. 4c+3 for c =
+ * 0, 1, 2): CTAs, CTA-wide rounds, two-word first rounds, group-mode exits.
+ * Copies min(n, 12) entries to out; reset != 0 zeroes them afterwards. */
+int s5g_finisher_counters(unsigned long long *out, int n, int reset);
 
 const char *s5g_last_error(void);
 int s5g_version(void);

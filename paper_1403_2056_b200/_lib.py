@@ -72,7 +72,7 @@ SIGNATURES = {
                                        C.POINTER(C.c_float), C.POINTER(C.c_float), C.c_int]),
     "s5g_launch_count": (C.c_ulonglong, []),
     "s5g_set_l2_fetch_granularity": (None, [C.c_int]),
-    "s5g_debug_arm": (C.c_int, [_p]),
+    "s5g_finisher_counters": (C.c_int, [C.POINTER(C.c_ulonglong), C.c_int, C.c_int]),
     "s5g_last_error": (C.c_char_p, []),
     "s5g_version": (C.c_int, []),
 }
@@ -136,6 +136,15 @@ def timeline() -> list[tuple[str, int, float, float]]:
     t1 = (C.c_float * cap)()
     k = min(cap, L.s5g_profile_timeline(kid, sid, t0, t1, cap))
     return [(names[kid[i]], int(sid[i]), float(t0[i]), float(t1[i])) for i in range(k)]
+
+
+def finisher_counters(reset: bool = False) -> dict[str, dict[str, int]]:
+    """CTAs / rounds / two-word rounds / group-mode exits per k_cta_sort<W>."""
+    buf = (C.c_ulonglong * 12)()
+    check(lib().s5g_finisher_counters(buf, 12, 1 if reset else 0))
+    return {f"k_cta_sort<{W}>": {"ctas": buf[4 * c], "rounds": buf[4 * c + 1],
+                                  "two_word": buf[4 * c + 2], "group_mode": buf[4 * c + 3]}
+            for c, W in enumerate((2, 4, 8))}
 
 
 def launch_count() -> int:

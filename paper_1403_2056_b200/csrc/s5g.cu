@@ -52,7 +52,7 @@ template <int NT, bool BIG>
 __global__ void __launch_bounds__(NT) k_sample_tree(
     const StepDev* __restrict__ steps, const uint8_t* __restrict__ arena, int64_t alen,
     const Rec* __restrict__ recX, uint64_t seed, uint64_t* __restrict__ tree_g, uint64_t* __restrict__ inorder_g, uint8_t* __restrict__ tpos_g,
-    uint16_t* __restrict__ eqb_g) {
+    uint16_t* __restrict__ eqb_g, const int64_t* __restrict__ hroot) {
     extern __shared__ __align__(16) uint8_t smem[];
     const StepDev sd = steps[blockIdx.x];
     const int v = sd.v, count = sd.count;
@@ -70,8 +70,12 @@ __global__ void __launch_bounds__(NT) k_sample_tree(
         uint64_t x = ~0ull;
         if (j < count) {
             int64_t idx = (int64_t)(splitmix64(key0 + j) % (uint64_t)sd.n);
-            const Rec* r = recX + sd.lo + idx;
-            x = sd.nvalid ? r->w[0] : load_key(arena, alen, r->h, sd.depth);
+            if (hroot) {  // the root step, sampled from the input while k_init runs
+                x = load_key(arena, alen, hroot[sd.lo + idx], sd.depth);
+            } else {
+                const Rec* r = recX + sd.lo + idx;
+                x = sd.nvalid ? r->w[0] : load_key(arena, alen, r->h, sd.depth);
+            }
         }
         s[j] = x;
     }
@@ -267,52 +271,83 @@ __global__ void __launch_bounds__(1024) k_scan_cols(const StepDev* __restrict__ 
     }
 }
 
-// Bucket-major exclusive scan (bounds), child segments, boundary records.
+// Append `item` to a device list at *counter, one atomic per warp and list
+// (a top-level step emits ~16K children; per-thread atomics on the same
+// counters serialised).  Every lane of the warp must call it.
+template <typename T>
+__device__ __forceinline__ void warp_append(bool want, const T& item, T* list,
+                                            unsigned long long* counter) {
+    const uint32_t m = __ballot_sync(0xffffffffu, want);
+    if (!m) return;
+    const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+    unsigned long long base = 0;
+    if (lane == leader) base = atomicAdd(counter, (unsigned long long)__popc(m));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (want) list[base + __popc(m & lanemask_lt())] = item;
+}
+
+// Bucket-major exclusive scan (bounds), child segments, boundary records:
+// one CTA per 1024 buckets of a step; its offset is the sum of the step's
+// earlier bucket totals (read from L2), so the top step's 16K buckets take
+// 16 CTAs instead of one CTA's sequential chunks.
 __global__ void __launch_bounds__(1024) k_scan_buckets(
-    const StepDev* __restrict__ steps, const uint32_t* __restrict__ tot,
+    const StepDev* __restrict__ steps, const int32_t* __restrict__ sblk_step,
+    const uint32_t* __restrict__ tot,
     uint32_t* __restrict__ bstart, const uint8_t* __restrict__ tpos_g, int dst_in_b,
     int64_t small_max, SegDev* __restrict__ large_out, SegDev* __restrict__ small_out,
     ClassLists cls,
     int64_t* __restrict__ blist, int64_t* __restrict__ lcps, Counters* __restrict__ ctr) {
     __shared__ uint32_t wsum[32];
-    const StepDev sd = steps[blockIdx.x];
+    __shared__ unsigned long long cls_el[NCLS];
+    const StepDev sd = steps[sblk_step[blockIdx.x]];
     const int nb = sd.nb;
     constexpr int NT = 1024;
-    const int per = (nb + NT - 1) / NT;
-    const int beg = threadIdx.x * per, end = min(beg + per, nb);
-    uint32_t s = 0;
-    for (int b = beg; b < end; b++) s += tot[sd.bk_off + b];
-    uint32_t run = block_excl_sum<NT>(s, wsum, nullptr);
-    for (int b = beg; b < end; b++) {
-        uint32_t size = tot[sd.bk_off + b];
-        bstart[sd.bk_off + b] = run;
-        if (size) {
-            if (lcps && run > 0) {  // boundary to the previous non-empty bucket
-                int64_t pos = sd.lo + run;
-                lcps[pos] = sd.depth;  // resolved by k_boundary
-                blist[atomicAdd(&ctr->n_bound, 1ull)] = pos;
-            }
-            bool odd = b & 1;
-            int tp = odd ? tpos_g[sd.tree_off + (b >> 1)] : WORD;
-            bool final_bucket = size == 1 || (odd && tp < WORD);
-            if (!final_bucket) {
-                SegDev c;
-                c.lo = sd.lo + run;
-                c.depth = sd.depth + (odd ? WORD : 0);
-                c.n = (int32_t)size;
-                const int nv = sd.nvalid ? sd.nvalid : NCACHE;  // classify refilled
-                c.flags = (odd ? nv - 1 : nv) | (dst_in_b ? SEG_IN_B : 0);
-                if ((int64_t)size <= small_max) {
-                    const int ci = size_class(size);
-                    small_out[cls.off[ci] + atomicAdd(&ctr->n_cls[ci], 1ull)] = c;
-                    atomicAdd(&ctr->cls_elems[ci], (unsigned long long)size);
+    const int nv = sd.nvalid ? sd.nvalid : NCACHE;  // classify refilled
+    if (threadIdx.x < NCLS) cls_el[threadIdx.x] = 0;
+    const int base = (blockIdx.x - sd.sblk0) * NT;
+    uint32_t carry = 0;
+    {
+        uint32_t part = 0;
+        for (int b = threadIdx.x; b < base; b += NT) part += tot[sd.bk_off + b];
+        block_excl_sum<NT>(part, wsum, &carry);  // total of the earlier buckets
+    }
+    {
+        const int b = base + threadIdx.x;
+        const uint32_t size = b < nb ? tot[sd.bk_off + b] : 0;
+        uint32_t total;
+        const uint32_t run = carry + block_excl_sum<NT>(size, wsum, &total);
+        bool bound = false, child = false;
+        SegDev c{};
+        int ci = -1;
+        if (b < nb) {
+            bstart[sd.bk_off + b] = run;
+            if (size) {
+                bound = lcps && run > 0;  // boundary to the previous non-empty bucket
+                if (bound) lcps[sd.lo + run] = sd.depth;  // resolved by k_boundary
+                const bool odd = b & 1;
+                const int tp = odd ? tpos_g[sd.tree_off + (b >> 1)] : WORD;
+                child = !(size == 1 || (odd && tp < WORD));
+                if (child) {
+                    c.lo = sd.lo + run;
+                    c.depth = sd.depth + (odd ? WORD : 0);
+                    c.n = (int32_t)size;
+                    c.flags = (odd ? nv - 1 : nv) | (dst_in_b ? SEG_IN_B : 0);
+                    ci = (int64_t)size <= small_max ? size_class(size) : -1;
                 }
-                else
-                    large_out[atomicAdd(&ctr->n_large, 1ull)] = c;
             }
         }
-        run += size;
+        warp_append<int64_t>(bound, sd.lo + run, blist, &ctr->n_bound);
+        warp_append<SegDev>(child && ci < 0, c, large_out, &ctr->n_large);
+#pragma unroll 1
+        for (int k = 0; k < NCLS; k++) {
+            warp_append<SegDev>(child && ci == k, c, small_out + cls.off[k], &ctr->n_cls[k]);
+            const uint32_t el = __reduce_add_sync(0xffffffffu, (child && ci == k) ? size : 0u);
+            if ((threadIdx.x & 31) == 0 && el) atomicAdd(&cls_el[k], (unsigned long long)el);
+        }
     }
+    __syncthreads();
+    if (threadIdx.x < NCLS && cls_el[threadIdx.x])
+        atomicAdd(&ctr->cls_elems[threadIdx.x], cls_el[threadIdx.x]);
 }
 
 // Stable scatter of (handle, key) into bucket order.  Singleton and
@@ -430,6 +465,205 @@ __global__ void __launch_bounds__(SC_NT, 2) k_scatter(
         }
         __syncthreads();
     }
+}
+
+// A whole S^5 step of one segment of at most MED_MAX strings in one CTA
+// (sample + select_splitters + classify + counts + stable scatter +
+// children), so the many small steps of later rounds cost one launch
+// instead of five and never round-trip their counts through global memory.
+// Bucket ids are recomputed in the scatter pass (<= 5 tree levels) instead of
+// being stored.  Same outputs as the device-wide step (ssss.py:281-358).
+struct StepCtaSmem {
+    uint64_t s[16 * (MED_VMAX + 1)];       // sorted sample
+    uint64_t tree[MED_VMAX + 1], inorder[MED_VMAX + 1];
+    uint32_t hist[SC_R], bst[SC_R], run_off[SC_R];
+    uint32_t dst_by_e[SC_SUB];
+    uint16_t rcnt[SC_R * (SC_NT / 32)];
+    uint16_t kA[SC_SUB], vA[SC_SUB], kB[SC_SUB], vB[SC_SUB];
+    uint16_t eqb[MED_VMAX + 1];
+    int16_t sa[MED_VMAX + 1], sb[MED_VMAX + 1], sp[MED_VMAX + 1];
+    uint8_t tpos[MED_VMAX + 1];
+    uint32_t wsum[32];
+    unsigned fetched;
+};
+
+template <int VARIANT>
+__global__ void __launch_bounds__(SC_NT, 2) k_step_cta(
+    const SegDev* __restrict__ segs, Rec* __restrict__ recA, Rec* __restrict__ recB,
+    const uint8_t* __restrict__ arena, int64_t alen, uint64_t seed, int64_t vcap,
+    int64_t small_max, SegDev* __restrict__ large_out, SegDev* __restrict__ small_out,
+    ClassLists cls, int64_t* __restrict__ blist, int64_t* __restrict__ out_h,
+    int64_t* __restrict__ lcps, Counters* __restrict__ ctr) {
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    StepCtaSmem& S = *reinterpret_cast<StepCtaSmem*>(smem_raw);
+    const SegDev sg = segs[blockIdx.x];
+    if (sg.n > MED_MAX) return;  // device-wide path
+    const int n = sg.n;
+    const int64_t lo = sg.lo, depth = sg.depth;
+    const bool in_b = sg.flags & SEG_IN_B;
+    Rec* X = (in_b ? recB : recA) + lo;
+    Rec* Y = (in_b ? recA : recB) + lo;
+    const int nvalid = sg.flags & SEG_NV_MASK;
+    const int v = (int)gpu_tree_capacity(n, vcap), L = levels_of(v), nb = 2 * v + 1;
+    const int count = sample_count(v);
+    int P = 1;
+    while (P < count) P <<= 1;
+    const int lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) S.fetched = 0;
+    unsigned my_fetch = 0;
+    // ---- refill the cached words when the segment ran out of them --------
+    if (!nvalid) {
+        for (int i = threadIdx.x; i < n; i += SC_NT) {
+            uint64_t wv[3];
+            load_words3(arena, alen, X[i].h, depth, wv);
+            X[i].w[0] = wv[0];
+            X[i].w[1] = wv[1];
+            X[i].w[2] = wv[2];
+            my_fetch += 3;
+        }
+        __syncthreads();  // the CTA's own record writes are visible after this
+    }
+    // ---- draw_sample + select_splitters (ssss.py:76-146) -----------------
+    const uint64_t key0 = splitmix64(seed ^ splitmix64(lo ^ splitmix64((uint64_t)n ^ splitmix64(depth))));
+    for (int j = threadIdx.x; j < P; j += SC_NT)
+        S.s[j] = j < count ? X[splitmix64(key0 + j) % (uint64_t)n].w[0] : ~0ull;
+    for (int b = threadIdx.x; b < SC_R; b += SC_NT) S.hist[b] = 0;
+    __syncthreads();
+    bitonic_u64<SC_NT>(S.s, P);
+    select_tree<SC_NT>(S.s, count, v, L, S.sa, S.sb, S.sp, S.tree, S.inorder, S.tpos, S.eqb);
+    __syncthreads();
+    // ---- classify + bucket counts (ssss.py:149-181, 292) -----------------
+    for (int base = 0; base < n; base += SC_NT) {
+        const int i = base + threadIdx.x;
+        const bool ok = i < n;
+        const uint32_t b = ok ? classify_one<VARIANT>(X[i].w[0], S.tree, S.eqb, v, L) : 0;
+        const uint32_t mask = __ballot_sync(0xffffffffu, ok);
+        if (ok) {
+            const uint32_t peers = __match_any_sync(mask, b);
+            if (lane == __ffs(peers) - 1) atomicAdd(&S.hist[b], (uint32_t)__popc(peers));
+        }
+    }
+    __syncthreads();
+    // ---- bucket starts, children, boundary records (one warp) -----------
+    if (threadIdx.x < 32) {
+        uint32_t sz[2], run = 0;
+#pragma unroll
+        for (int k = 0; k < 2; k++) {
+            const int b = lane * 2 + k;
+            sz[k] = b < nb ? S.hist[b] : 0;
+        }
+        const uint32_t mine = sz[0] + sz[1];
+        uint32_t incl = mine;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        run = incl - mine;
+        const int nv = nvalid ? nvalid : NCACHE;
+#pragma unroll
+        for (int k = 0; k < 2; k++) {
+            const int b = lane * 2 + k;
+            if (b < nb) {
+                S.bst[b] = run;
+                S.run_off[b] = run;
+                const uint32_t size = sz[k];
+                if (size) {
+                    if (lcps && run > 0) {
+                        lcps[lo + run] = depth;  // resolved by k_boundary
+                        blist[atomicAdd(&ctr->n_bound, 1ull)] = lo + run;
+                    }
+                    const bool odd = b & 1;
+                    const int tp = odd ? S.tpos[b >> 1] : WORD;
+                    if (!(size == 1 || (odd && tp < WORD))) {
+                        SegDev c;
+                        c.lo = lo + run;
+                        c.depth = depth + (odd ? WORD : 0);
+                        c.n = (int32_t)size;
+                        c.flags = (odd ? nv - 1 : nv) | (in_b ? 0 : SEG_IN_B);
+                        if ((int64_t)size <= small_max) {
+                            const int ci = size_class(size);
+                            small_out[cls.off[ci] + atomicAdd(&ctr->n_cls[ci], 1ull)] = c;
+                            atomicAdd(&ctr->cls_elems[ci], (unsigned long long)size);
+                        } else {
+                            large_out[atomicAdd(&ctr->n_large, 1ull)] = c;
+                        }
+                    }
+                }
+                run += sz[k];
+            }
+        }
+    }
+    __syncthreads();
+    // ---- stable scatter per SC_SUB sub-tile (one 7-bit ranking pass) -----
+    for (int sub = 0; sub < n; sub += SC_SUB) {
+        const int m = min(SC_SUB, n - sub);
+        Rec rec[SC_ITEMS];
+        uint32_t myb[SC_ITEMS];
+#pragma unroll
+        for (int it = 0; it < SC_ITEMS; it++) {
+            const int e = threadIdx.x + it * SC_NT;
+            myb[it] = BID_SENTINEL;
+            if (e < m) {
+                rec[it] = X[sub + e];
+                myb[it] = classify_one<VARIANT>(rec[it].w[0], S.tree, S.eqb, v, L);
+            }
+            S.kA[e] = (uint16_t)myb[it];
+            S.vA[e] = (uint16_t)e;
+        }
+        __syncthreads();
+        rank_pass(S.kA, S.vA, S.kB, S.vB, 0, S.rcnt, S.wsum);
+        const int q0 = threadIdx.x * SC_ITEMS;
+        uint32_t bq[SC_ITEMS], st[SC_ITEMS], mx = 0;
+#pragma unroll
+        for (int it = 0; it < SC_ITEMS; it++) {
+            const int q = q0 + it;
+            bq[it] = S.kB[q];
+            const bool start = q < m && (q == 0 || S.kB[q - 1] != bq[it]);
+            if (start) mx = q + 1;
+            st[it] = mx;
+        }
+        const uint32_t before = block_excl_max<SC_NT>(mx, S.wsum);
+#pragma unroll
+        for (int it = 0; it < SC_ITEMS; it++) {
+            const int q = q0 + it;
+            st[it] = (st[it] ? st[it] : before) - 1;
+            if (q < m) S.dst_by_e[S.vB[q]] = S.run_off[bq[it]] + (q - st[it]);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int it = 0; it < SC_ITEMS; it++) {
+            const int e = threadIdx.x + it * SC_NT;
+            if (e >= m) break;
+            const uint32_t b = myb[it];
+            const uint32_t rel = S.dst_by_e[e];
+            const uint32_t size = S.hist[b];
+            const bool odd = b & 1;
+            const int tpv = odd ? S.tpos[b >> 1] : WORD;
+            if (size == 1 || (odd && tpv < WORD)) {
+                out_h[lo + rel] = rec[it].h;
+                if (lcps && size > 1 && rel != S.bst[b]) lcps[lo + rel] = depth + tpv;
+            } else if (odd) {
+                Rec o;
+                o.h = rec[it].h;
+                o.w[0] = rec[it].w[1];
+                o.w[1] = rec[it].w[2];
+                o.w[2] = 0;
+                Y[rel] = o;
+            } else {
+                Y[rel] = rec[it];
+            }
+        }
+#pragma unroll
+        for (int it = 0; it < SC_ITEMS; it++) {
+            const int q = q0 + it;
+            if (q < m && (q == m - 1 || S.kB[q + 1] != bq[it])) S.run_off[bq[it]] += q - st[it] + 1;
+        }
+        __syncthreads();
+    }
+    if (my_fetch) atomicAdd(&S.fetched, my_fetch);
+    __syncthreads();
+    if (threadIdx.x == 0 && S.fetched) atomicAdd(&ctr->fetches, (unsigned long long)S.fetched);
 }
 
 // LCP at a bucket boundary of a device-wide step at depth d: both strings
@@ -617,13 +851,13 @@ static int g_sms = 148;         // multiprocessors of the current device
 // ---- live per-kernel timing (CUDA events on the launching stream) --------
 enum KernelId { K_INIT, K_SAMPLE, K_CLASSIFY, K_SCAN_COLS, K_SCAN_BUCKETS, K_SCATTER, K_SEG_WARP,
                 K_SEG_WARP2, K_SEG_WARP4, K_SEG_WARP8, K_SEG_CTA2, K_SEG_CTA4, K_SEG_CTA8,
-                K_BOUNDARY, K_DCHAR, K_COUNT };
+                K_BOUNDARY, K_DCHAR, K_STEP_CTA, K_COUNT };
 static const char* kKernelNames[K_COUNT] = {"k_init", "k_sample_tree", "k_classify",
                                             "k_scan_cols", "k_scan_buckets", "k_scatter",
                                             "k_warp_sort<1>", "k_warp_sort<2>",
                                             "k_warp_sort<4>", "k_warp_sort<8>", "k_cta_sort<2>",
                                             "k_cta_sort<4>", "k_cta_sort<8>", "k_boundary",
-                                            "k_dchar"};
+                                            "k_dchar", "k_step_cta"};
 struct ProfEntry {
     long long launches = 0, units = 0, bytes = 0;
     double ms = 0;
@@ -735,28 +969,6 @@ static int fail(int code, const std::string& msg) {
             return fail(S5G_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
     } while (0)
 
-static int levels_of(int64_t v) {
-    int l = 0;
-    while ((1LL << l) < v + 1) l++;
-    return l;
-}
-
-// tree_capacity (ssss.py:67-73)
-static int64_t tree_capacity(int64_t n, int64_t v) {
-    int64_t limit = std::min<int64_t>(v, std::max<int64_t>(1, n / 2));
-    int d = 0;
-    while ((1LL << (d + 1)) - 1 <= limit) d++;
-    return std::max<int64_t>(1, (1LL << d) - 1);
-}
-
-// Splitters for a device-wide step: v+1 range buckets of about SEG_TARGET
-// strings each (the reference's tree_capacity, ssss.py:67-73, caps it; v
-// and the sample size never change the output, only the bucket sizes).
-static int64_t gpu_tree_capacity(int64_t n, int64_t vcap) {
-    int64_t want = 1;
-    while (want < VMAX && (want + 1) * SEG_TARGET < n) want = 2 * want + 1;
-    return std::min(want, tree_capacity(n, vcap));
-}
 
 static int64_t small_max_of(int64_t t_medium) {
     // segments of size <= small_max finish in one CTA; the reference
@@ -773,6 +985,7 @@ struct Workspace {
     uint8_t* tpos;
     uint16_t* eqb;
     StepDev* steps;
+    StepDev* root_step;
     int32_t* tile_step;
     SegDev* large[2];
     SegDev* small;   // NCLS lists; class c holds cls_cap[c] entries at cls_off[c]
@@ -794,7 +1007,8 @@ static size_t carve(Workspace* w, uint8_t* base, int64_t n, int64_t t_medium) {
     const int64_t large_min = small_max_of(t_medium) + 1;
     w->steps_cap = nn / large_min + 2;
     // big steps round their tile count up to whole waves: <= 2x the tiles
-    w->tiles_cap = 2 * (nn / TILE) + w->steps_cap + 1 + (nn + 2 * w->steps_cap) / 32 + w->steps_cap;
+    w->tiles_cap = 2 * (nn / TILE) + w->steps_cap + 1 + (nn + 2 * w->steps_cap) / 32 +
+                   (nn + 2 * w->steps_cap) / 1024 + 2 * w->steps_cap + 2;
     w->cnt_cap = nn * (2 * (int64_t)NBMAX / TILE + 2) + w->steps_cap * 2;
     w->bk_cap = nn + 2 * w->steps_cap;
     w->tree_cap = nn / 2 + 4 * w->steps_cap + 2;
@@ -819,6 +1033,7 @@ static size_t carve(Workspace* w, uint8_t* base, int64_t n, int64_t t_medium) {
     w->tpos = (uint8_t*)take(w->tree_cap);
     w->eqb = (uint16_t*)take(2 * w->tree_cap);
     w->steps = (StepDev*)take(sizeof(StepDev) * w->steps_cap);
+    w->root_step = (StepDev*)take(sizeof(StepDev));
     w->tile_step = (int32_t*)take(4 * w->tiles_cap);
     w->large[0] = (SegDev*)take(sizeof(SegDev) * w->steps_cap);
     w->large[1] = (SegDev*)take(sizeof(SegDev) * w->steps_cap);
@@ -864,6 +1079,10 @@ static int set_smem_attrs() {
     CK(cudaFuncSetAttribute(k_classify<S5G_VARIANT_EQUAL>,
                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_CLS));
     CK(cudaFuncSetAttribute(k_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_SC));
+    CK(cudaFuncSetAttribute(k_step_cta<S5G_VARIANT_UNROLL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)sizeof(StepCtaSmem)));
+    CK(cudaFuncSetAttribute(k_step_cta<S5G_VARIANT_EQUAL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)sizeof(StepCtaSmem)));
     CK(cudaFuncSetAttribute(k_cta_sort<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)sizeof(CtaSortSmem<2>)));
     CK(cudaFuncSetAttribute(k_cta_sort<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -966,19 +1185,25 @@ static int sort_impl_body(const s5g_sort_args* a) {
     Counters hc{};
     // side stream (per device, created once): finishers of earlier rounds run
     // there concurrently with the next round's device-wide step
-    static cudaStream_t s_st2[64];
-    static cudaEvent_t s_fork[64], s_join[64];
+    // and a high-priority stream for the root step's sample, drawn from the
+    // input while k_init copies it (its one CTA is scheduled first)
+    static cudaStream_t s_st2[64], s_hi[64];
+    static cudaEvent_t s_fork[64], s_join[64], s_samp[64];
     int dev_id = 0;
     CK(cudaGetDevice(&dev_id));
     if (dev_id >= 64) return fail(S5G_E_INVALID, "device id >= 64");
     if (!s_st2[dev_id]) {
+        int lo_prio = 0, hi_prio = 0;
+        CK(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
         CK(cudaStreamCreateWithFlags(&s_st2[dev_id], cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithPriority(&s_hi[dev_id], cudaStreamNonBlocking, hi_prio));
         CK(cudaEventCreateWithFlags(&s_fork[dev_id], cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&s_join[dev_id], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&s_samp[dev_id], cudaEventDisableTiming));
     }
-    cudaStream_t st2 = s_st2[dev_id];
-    cudaEvent_t ev_fork = s_fork[dev_id], ev_join = s_join[dev_id];
-    Profiler prof2(st2, 1);
+    cudaStream_t st2 = s_st2[dev_id], st_hi = s_hi[dev_id];
+    cudaEvent_t ev_fork = s_fork[dev_id], ev_join = s_join[dev_id], ev_samp = s_samp[dev_id];
+    Profiler prof2(st2, 1), prof_hi(st_hi, 2);
     bool fin_side_used = false;
     unsigned long long fin_done[NCLS] = {0}, fin_done_el[NCLS] = {0};
     // launch the finishers for list entries [fin_done[c], hc.n_cls[c])
@@ -1018,6 +1243,41 @@ static int sort_impl_body(const s5g_sort_args* a) {
         return cudaSuccess;
     };
     CK(cudaMemsetAsync(w.ctr, 0, sizeof(Counters), st));
+    // segments of <= MED_MAX strings take their step in one CTA (k_step_cta);
+    // the step hook wants every step's bounds, so it keeps the device-wide path
+    const bool fused = !a->step_cb;
+    // root step sampled early (device-wide root only): same StepDev fields
+    // the round loop plans for it (lo, n, depth, v, count, levels, tree_off 0)
+    const bool early_root = n > small_max && !(fused && n <= MED_MAX);
+    if (early_root) {
+        StepDev d{};
+        d.lo = 0;
+        d.n = n;
+        d.depth = a->depth;
+        d.v = (int32_t)gpu_tree_capacity(n, vcap);
+        d.count = sample_count(d.v);
+        d.levels = levels_of(d.v);
+        d.nb = 2 * d.v + 1;
+        d.nvalid = NCACHE;
+        CK(cudaEventRecord(ev_fork, st));  // the caller's stream order (handles ready)
+        CK(cudaStreamWaitEvent(st_hi, ev_fork, 0));
+        CK(cudaMemcpyAsync(w.root_step, &d, sizeof(StepDev), cudaMemcpyHostToDevice, st_hi));
+        int P = 1;
+        while (P < d.count) P <<= 1;
+        const long long sb = (long long)d.count * 16 + 27LL * d.v;
+        if (P == 16 * SAMPLE_NT)
+            SPROF(prof_hi, K_SAMPLE, 1, sb,
+                  (k_sample_tree<SAMPLE_NT, true><<<1, SAMPLE_NT, smem_sample(P, d.v), st_hi>>>(
+                      w.root_step, a->arena, a->arena_len, w.recA, a->seed, w.tree, w.inorder,
+                      w.tpos, w.eqb, a->handles)));
+        else
+            SPROF(prof_hi, K_SAMPLE, 1, sb,
+                  (k_sample_tree<256, false><<<1, 256, smem_sample(P, d.v), st_hi>>>(
+                      w.root_step, a->arena, a->arena_len, w.recA, a->seed, w.tree, w.inorder,
+                      w.tpos, w.eqb, a->handles)));
+        CK(cudaGetLastError());
+        CK(cudaEventRecord(ev_samp, st_hi));
+    }
     PROF(K_INIT, n, 56LL * n, (k_init<<<blocks_for(n, 256), 256, 0, st>>>(a->arena, a->arena_len,
                                                                  a->handles, n, a->depth,
                                                                  w.recA)));
@@ -1026,6 +1286,7 @@ static int sort_impl_body(const s5g_sort_args* a) {
     int64_t n_jobs = 0;
     std::vector<SegDev> large;
     SegDev root{0, a->depth, (int32_t)n, NCACHE};
+
     if (n <= small_max) {
         const int cls = size_class(n);
         CK(cudaMemcpyAsync(w.small + w.cls_off[cls], &root, sizeof(SegDev),
@@ -1036,16 +1297,53 @@ static int sort_impl_body(const s5g_sort_args* a) {
         CK(cudaMemcpyAsync(&w.ctr->cls_elems[cls], &hc.cls_elems[cls], 8, cudaMemcpyHostToDevice, st));
     } else {
         large.push_back(root);
+        // the round's device list is w.large[round & 1] (k_step_cta reads it)
+        if (fused && n <= MED_MAX)
+            CK(cudaMemcpyAsync(w.large[0], &root, sizeof(SegDev), cudaMemcpyHostToDevice, st));
     }
     int in_b = 0;  // data of this round's segments lives in buffer B
     int round = 0;
     std::vector<StepDev> steps;
-    std::vector<int32_t> tile_step, cblk_step;
+    std::vector<int32_t> tile_step, cblk_step, sblk_step;
     std::vector<uint32_t> h_tot, h_bstart;
     std::vector<uint64_t> h_inorder;
     std::vector<int64_t> h_bounds;
+    bool side_pending = false;
+    auto launch_side = [&]() -> int {
+        if (!side_pending) return 0;
+        side_pending = false;
+        CK(cudaStreamWaitEvent(st2, ev_fork, 0));
+        CK(launch_finishers(st2, prof2));
+        fin_side_used = true;
+        return 0;
+    };
     while (!large.empty()) {
-        // ---- plan the round's steps (host) -------------------------------
+        // ---- medium segments: a whole step per CTA ------------------------
+        int64_t n_med = 0, med_elems = 0;
+        if (fused)
+            for (const auto& sgm : large)
+                if (sgm.n <= MED_MAX) {
+                    n_med++;
+                    med_elems += sgm.n;
+                }
+        if (n_med) {
+            n_jobs += n_med;
+            if (a->variant == S5G_VARIANT_UNROLL)
+                PROF(K_STEP_CTA, med_elems, 66LL * med_elems,
+                     (k_step_cta<S5G_VARIANT_UNROLL><<<(unsigned)large.size(), SC_NT, sizeof(StepCtaSmem), st>>>(
+                         w.large[round & 1], w.recA, w.recB, a->arena, a->arena_len, a->seed, vcap,
+                         small_max, w.large[(round + 1) & 1], w.small, cls_lists, w.blist,
+                         a->out_handles, lcps, w.ctr)));
+            else
+                PROF(K_STEP_CTA, med_elems, 66LL * med_elems,
+                     (k_step_cta<S5G_VARIANT_EQUAL><<<(unsigned)large.size(), SC_NT, sizeof(StepCtaSmem), st>>>(
+                         w.large[round & 1], w.recA, w.recB, a->arena, a->arena_len, a->seed, vcap,
+                         small_max, w.large[(round + 1) & 1], w.small, cls_lists, w.blist,
+                         a->out_handles, lcps, w.ctr)));
+            CK(cudaGetLastError());
+        }
+        if (int rc = launch_side()) return rc;
+        // ---- plan the round's device-wide steps (host) --------------------
         steps.clear();
         tile_step.clear();
         int64_t cnt_off = 0, bk_off = 0, tree_off = 0, tile0 = 0;
@@ -1058,15 +1356,13 @@ static int sort_impl_body(const s5g_sort_args* a) {
             size_t i = i0;
             for (; i < large.size(); i++) {
                 const SegDev& s = large[i];
+                if (fused && s.n <= MED_MAX) continue;  // k_step_cta did it
                 StepDev d{};
                 d.lo = s.lo;
                 d.n = s.n;
                 d.depth = s.depth;
                 d.v = (int32_t)gpu_tree_capacity(s.n, vcap);
-                // oversampling: the reference's alpha = 2 for big trees, up to
-                // 16 for small ones (tighter buckets, same output)
-                const int alpha = std::max(OVERSAMPLE, std::min(16, 1024 / (d.v + 1)));
-                d.count = alpha * (d.v + 1) - 1;
+                d.count = sample_count(d.v);
                 d.levels = levels_of(d.v);
                 d.nb = 2 * d.v + 1;
                 d.nvalid = s.flags & SEG_NV_MASK;
@@ -1080,7 +1376,8 @@ static int sort_impl_body(const s5g_sort_args* a) {
                 d.ntiles = (int32_t)((s.n + d.tile - 1) / d.tile);
                 int64_t need_cnt = (int64_t)d.ntiles * d.nb;
                 if ((int64_t)steps.size() + 1 > w.steps_cap ||
-                    tile0 + d.ntiles + (bk_off + d.nb) / 32 + (int64_t)steps.size() + 1 > w.tiles_cap ||
+                    tile0 + d.ntiles + (bk_off + d.nb) / 32 + (bk_off + d.nb) / 1024 +
+                            2 * ((int64_t)steps.size() + 1) > w.tiles_cap ||
                     cnt_off + need_cnt > w.cnt_cap || bk_off + d.nb > w.bk_cap ||
                     tree_off + d.v + 2 > w.tree_cap) {
                     if (steps.empty()) return fail(S5G_E_WORKSPACE, "step exceeds capacity");
@@ -1099,24 +1396,29 @@ static int sort_impl_body(const s5g_sort_args* a) {
             }
             i0 = i;
             const int nsteps = (int)steps.size();
+            if (!nsteps) break;
             cblk_step.clear();
+            sblk_step.clear();
             for (int si = 0; si < nsteps; si++) {
                 steps[si].cblk0 = (int64_t)cblk_step.size();
                 for (int b = 0; b < steps[si].nb; b += 32) cblk_step.push_back(si);
+                steps[si].sblk0 = (int32_t)sblk_step.size();
+                for (int b = 0; b < steps[si].nb; b += 1024) sblk_step.push_back(si);
             }
             n_jobs += nsteps;
             {
                 // previous round's uploads are complete: this round began after
                 // a stream sync, so the staging buffer can be reused
                 const size_t b1 = sizeof(StepDev) * nsteps, b2 = 4 * tile_step.size(),
-                             b3 = 4 * cblk_step.size();
-                uint8_t* up = (uint8_t*)g_stage_up.get(b1 + b2 + b3);
+                             b3 = 4 * cblk_step.size(), b4 = 4 * sblk_step.size();
+                uint8_t* up = (uint8_t*)g_stage_up.get(b1 + b2 + b3 + b4);
                 if (!up) return fail(S5G_E_CUDA, "cudaMallocHost failed");
                 memcpy(up, steps.data(), b1);
                 memcpy(up + b1, tile_step.data(), b2);
                 memcpy(up + b1 + b2, cblk_step.data(), b3);
+                memcpy(up + b1 + b2 + b3, sblk_step.data(), b4);
                 CK(cudaMemcpyAsync(w.steps, up, b1, cudaMemcpyHostToDevice, st));
-                CK(cudaMemcpyAsync(w.tile_step, up + b1, b2 + b3, cudaMemcpyHostToDevice, st));
+                CK(cudaMemcpyAsync(w.tile_step, up + b1, b2 + b3 + b4, cudaMemcpyHostToDevice, st));
             }
             Rec* recX = in_b ? w.recB : w.recA;
             Rec* recY = in_b ? w.recA : w.recB;
@@ -1128,16 +1430,18 @@ static int sort_impl_body(const s5g_sort_args* a) {
                 while (maxP < d.count) maxP <<= 1;
                 sample_bytes += (long long)d.count * (d.nvalid ? 8 : 16) + 27LL * d.v;
             }
-            if (maxP == 16 * SAMPLE_NT)
+            if (round == 0 && early_root) {
+                CK(cudaStreamWaitEvent(st, ev_samp, 0));  // root tree drawn on st_hi
+            } else if (maxP == 16 * SAMPLE_NT)
                 PROF(K_SAMPLE, nsteps, sample_bytes,
                      (k_sample_tree<SAMPLE_NT, true><<<nsteps, SAMPLE_NT, smem_sample(maxP, maxv), st>>>(
                          w.steps, a->arena, a->arena_len, recX, a->seed, w.tree, w.inorder, w.tpos,
-                         w.eqb)));
+                         w.eqb, nullptr)));
             else
                 PROF(K_SAMPLE, nsteps, sample_bytes,
                      (k_sample_tree<256, false><<<nsteps, 256, smem_sample(maxP, maxv), st>>>(
                          w.steps, a->arena, a->arena_len, recX, a->seed, w.tree, w.inorder, w.tpos,
-                         w.eqb)));
+                         w.eqb, nullptr)));
             CK(cudaGetLastError());
             const unsigned ntiles = (unsigned)tile0;
             int64_t round_elems = 0, cls_bytes = 0;
@@ -1161,7 +1465,8 @@ static int sort_impl_body(const s5g_sort_args* a) {
                      w.steps, w.tile_step + tile0, w.cnt, w.tot)));
             CK(cudaGetLastError());
             PROF(K_SCAN_BUCKETS, bk_off, 8LL * bk_off,
-                 (k_scan_buckets<<<nsteps, 1024, 0, st>>>(w.steps, w.tot, w.bstart, w.tpos, !in_b,
+                 (k_scan_buckets<<<(unsigned)sblk_step.size(), 1024, 0, st>>>(
+                     w.steps, w.tile_step + tile0 + cblk_step.size(), w.tot, w.bstart, w.tpos, !in_b,
                                                          small_max, w.large[(round + 1) & 1],
                                                          w.small, cls_lists, w.blist, lcps,
                                                          w.ctr)));
@@ -1215,11 +1520,10 @@ static int sort_impl_body(const s5g_sort_args* a) {
         }
         if (hc.n_large) {
             // this round's small segments: finish them on the side stream while
-            // the next round runs (disjoint positions; the host already synced)
+            // the next round runs (disjoint positions; the host already synced).
+            // Launched after the next round's first kernel is queued.
             CK(cudaEventRecord(ev_fork, st));
-            CK(cudaStreamWaitEvent(st2, ev_fork, 0));
-            CK(launch_finishers(st2, prof2));
-            fin_side_used = true;
+            side_pending = true;
         }
         in_b ^= 1;
         round++;
@@ -1307,8 +1611,14 @@ unsigned long long s5g_launch_count(void) { return g_launches; }
 
 void s5g_set_l2_fetch_granularity(int bytes) { g_l2_fetch = bytes > 0 ? (size_t)bytes : 32; }
 
-int s5g_debug_arm(void* dev_buf) {
-    (void)dev_buf;  // no traced kernel in this build
+int s5g_finisher_counters(unsigned long long* out, int n, int reset) {
+    unsigned long long h[12];
+    CK(cudaMemcpyFromSymbol(h, g_fin_ctr, sizeof(h)));
+    for (int i = 0; i < n && i < 12; i++) out[i] = h[i];
+    if (reset) {
+        std::memset(h, 0, sizeof(h));
+        CK(cudaMemcpyToSymbol(g_fin_ctr, h, sizeof(h)));
+    }
     return 0;
 }
 

@@ -43,7 +43,7 @@ struct StepDev {
     int64_t lo, n, depth;
     int32_t v, levels, nb, nvalid;   // nvalid: cached words valid at depth (0 = refill)
     int64_t tile0;
-    int32_t ntiles, pad0;
+    int32_t ntiles, sblk0;  // sblk0: first 1024-bucket block of k_scan_buckets
     int64_t cnt_off;   // first entry in the tile x bucket count matrix
     int64_t bk_off;    // first entry in tot / bstart
     int64_t tree_off;  // first entry in tree / inorder / tpos / eqb (even)
@@ -73,6 +73,44 @@ struct Counters {
 struct ClassLists {
     int64_t off[NCLS];
 };
+
+// tree_capacity (ssss.py:67-73)
+__host__ __device__ inline int64_t tree_capacity(int64_t n, int64_t v) {
+    int64_t limit = v < (n / 2 > 1 ? n / 2 : 1) ? v : (n / 2 > 1 ? n / 2 : 1);
+    int d = 0;
+    while ((1LL << (d + 1)) - 1 <= limit) d++;
+    const int64_t t = (1LL << d) - 1;
+    return t > 1 ? t : 1;
+}
+
+// Splitters for a GPU step: v+1 range buckets of about SEG_TARGET strings
+// each (the reference's tree_capacity caps it; v and the sample size never
+// change the output, only the bucket sizes).
+__host__ __device__ inline int64_t gpu_tree_capacity(int64_t n, int64_t vcap) {
+    int64_t want = 1;
+    while (want < VMAX && (want + 1) * SEG_TARGET < n) want = 2 * want + 1;
+    const int64_t t = tree_capacity(n, vcap);
+    return want < t ? want : t;
+}
+
+__host__ __device__ inline int levels_of(int64_t v) {
+    int l = 0;
+    while ((1LL << l) < v + 1) l++;
+    return l;
+}
+
+// oversampling: the reference's alpha = 2 for big trees, up to 16 for small
+// ones (tighter buckets, same output)
+__host__ __device__ inline int sample_count(int64_t v) {
+    int a = (int)(1024 / (v + 1));
+    a = a < 16 ? a : 16;
+    a = a > OVERSAMPLE ? a : OVERSAMPLE;
+    return a * (int)(v + 1) - 1;
+}
+
+// segments a single CTA takes through a whole S^5 step (k_step_cta)
+constexpr int MED_MAX = TILE;
+constexpr int MED_VMAX = 31;   // gpu_tree_capacity(MED_MAX) -> <= 63 buckets
 
 __host__ __device__ inline int size_class(int64_t n) {
     return n <= 32 ? 0 : n <= 64 ? 1 : n <= 128 ? 2 : n <= 256 ? 3 : n <= 512 ? 4 : n <= 1024 ? 5 : 6;

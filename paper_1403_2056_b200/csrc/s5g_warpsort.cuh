@@ -22,6 +22,7 @@
 namespace s5g {
 
 __device__ uint8_t g_pext8[256 * 256];  // [mask * 256 + byte] = pext(byte, mask)
+__device__ unsigned long long g_fin_ctr[12];  // s5g_finisher_counters
 
 // meta = active << 22 | group << 11 | tag   (11-bit slots and tags)
 __device__ __forceinline__ bool cs_less(uint64_t ka, uint32_t ma, uint64_t kb, uint32_t mb) {
@@ -67,23 +68,51 @@ __device__ __forceinline__ uint64_t pext_key(uint64_t x, const Pext& p) {
     return c;
 }
 
-// Arena gather beyond the cached words: one out-of-line copy instead of one
-// per inlined slot (instruction-cache footprint of the finishers).
-__device__ __noinline__ uint64_t load_key_far(const uint8_t* __restrict__ arena, int64_t alen,
-                                              int64_t h, int64_t depth) {
-    return load_key(arena, alen, h, depth);
-}
-
-// Word at `depth` of the segment's string `tag`: from its work record while
-// the cache covers that depth (depth - d0 < 8 * nv), else an arena gather.
-__device__ __forceinline__ uint64_t seg_word(const Rec* __restrict__ segrec, uint32_t tag,
-                                             int64_t d0, int nv, int64_t depth,
-                                             const uint8_t* __restrict__ arena, int64_t alen,
-                                             int64_t h, unsigned& fetches) {
-    const int64_t r = (depth - d0) >> 3;
-    if (r < nv) return segrec[tag].w[r];
-    fetches++;
-    return load_key_far(arena, alen, h, depth);
+// Words at `depth` of the active slots, from the work records while `depth`
+// is inside their cache (cd: depth of w[0], cnv: valid words), else every
+// active record is refilled with its next three words (one gather round trip
+// for up to three rounds; duplicate-heavy runs advance a word per round).
+// cd / cnv / depth are uniform over the caller (one warp, or the CTA when
+// CTA), and each tag is in one slot, so the record writes never conflict.
+// The refill walks the slots (tags staged in `scratch[0 .. nslots)`) in one
+// rolled loop: inlined per register slot, the gather code would double the
+// finishers' instruction footprint.
+template <int N, bool CTA>
+__device__ __forceinline__ void rekey(uint64_t (&key)[N], const uint32_t (&meta)[N],
+                                      Rec* __restrict__ segrec, const int64_t* __restrict__ hbt,
+                                      int64_t& cd, int& cnv, int64_t depth,
+                                      const uint8_t* __restrict__ arena, int64_t alen,
+                                      unsigned& fetches, uint64_t* __restrict__ scratch,
+                                      int slot0, int nslots, int tid, int nthreads) {
+    const int64_t off = depth - cd;
+    if ((off & 7) == 0 && (off >> 3) < cnv) {
+        const int r = (int)(off >> 3);
+#pragma unroll
+        for (int e = 0; e < N; e++)
+            if (meta[e] >> 22 & 1) key[e] = segrec[meta[e] & 0x7ff].w[r];
+        return;
+    }
+#pragma unroll
+    for (int e = 0; e < N; e++)
+        if (slot0 + e < nslots) scratch[slot0 + e] = (meta[e] >> 22 & 1) ? (meta[e] & 0x7ff) : ~0ull;
+    if (CTA) __syncthreads(); else __syncwarp();
+    for (int q = tid; q < nslots; q += nthreads) {
+        const uint64_t t = scratch[q];
+        if (t != ~0ull) {
+            uint64_t w3[3];
+            load_words3(arena, alen, hbt[t], depth, w3);
+            segrec[t].w[0] = w3[0];
+            segrec[t].w[1] = w3[1];
+            segrec[t].w[2] = w3[2];
+            fetches += 3;
+        }
+    }
+    if (CTA) __syncthreads(); else __syncwarp();
+#pragma unroll
+    for (int e = 0; e < N; e++)
+        if (meta[e] >> 22 & 1) key[e] = segrec[meta[e] & 0x7ff].w[0];
+    cd = depth;
+    cnv = NCACHE;
 }
 
 __device__ __forceinline__ void cex_u64(uint64_t& a, uint64_t& b, bool up) {
@@ -198,23 +227,19 @@ __device__ __forceinline__ uint64_t warp_and64(uint64_t x) {
 template <int IT>
 __device__ void warp_finish(const int64_t* __restrict__ hbt, uint16_t* __restrict__ ord,
                             uint64_t* __restrict__ kb, uint64_t* __restrict__ xs,
-                            const Rec* __restrict__ segrec, int64_t d0,
-                            int nv, int g0, int gn, int64_t depth, uint64_t (&key)[IT],
+                            Rec* __restrict__ segrec, int64_t cd,
+                            int cnv, int g0, int gn, int64_t depth, uint64_t (&key)[IT],
                             const uint8_t* __restrict__ arena, int64_t alen,
                             int64_t* __restrict__ lcp_seg, unsigned& fetches, int lane) {
     uint32_t meta[IT];
 #pragma unroll
     for (int e = 0; e < IT; e++) {
         const int i = lane * IT + e;
-        if (i < gn) {
-            const uint32_t tag = ord[g0 + i];
-            key[e] = seg_word(segrec, tag, d0, nv, depth, arena, alen, hbt[tag], fetches);
-            meta[e] = (1u << 22) | tag;
-        } else {
-            key[e] = ~0ull;
-            meta[e] = (uint32_t)i << 11;
-        }
+        key[e] = ~0ull;
+        meta[e] = i < gn ? (1u << 22) | ord[g0 + i] : (uint32_t)i << 11;
     }
+    rekey<IT, false>(key, meta, segrec, hbt, cd, cnv, depth, arena, alen, fetches, xs + g0,
+                     lane * IT, gn, lane, 32);
     for (;;) {
         // ---- sort the active slots by (group, word, tag) ------------------
         uint64_t o = 0, a = ~0ull;
@@ -222,7 +247,10 @@ __device__ void warp_finish(const int64_t* __restrict__ hbt, uint16_t* __restric
         for (int e = 0; e < IT; e++)
             if (meta[e] >> 22 & 1) { o |= key[e]; a &= key[e]; }
         const Pext px = pext_setup(warp_or64(o) ^ warp_and64(a));
-        if (px.cb <= 45) {
+        if (px.cb == 0) {
+            // all active words equal: the slots are already in (group, tag)
+            // order (duplicate-heavy inputs spend most rounds here)
+        } else if (px.cb <= 45) {
             // words by tag (kb) and by slot (xs, packed in one rolled loop)
 #pragma unroll
             for (int e = 0; e < IT; e++) {
@@ -311,12 +339,8 @@ __device__ void warp_finish(const int64_t* __restrict__ hbt, uint16_t* __restric
             const uint32_t tag = meta[e] & 0x7ff;
             meta[e] = keep[e] ? ((1u << 22) | ((cur - 1) << 11) | tag) : (((uint32_t)i << 11) | tag);
         }
-#pragma unroll
-        for (int e = 0; e < IT; e++)
-            if (meta[e] >> 22 & 1) {
-                const uint32_t tag = meta[e] & 0x7ff;
-                key[e] = seg_word(segrec, tag, d0, nv, depth, arena, alen, hbt[tag], fetches);
-            }
+        rekey<IT, false>(key, meta, segrec, hbt, cd, cnv, depth, arena, alen, fetches, xs + g0,
+                     lane * IT, gn, lane, 32);
     }
 #pragma unroll
     for (int e = 0; e < IT; e++) {
@@ -337,8 +361,8 @@ __host__ __device__ constexpr int ws_nt(int items) { return items >= 8 ? 128 : 2
 
 template <int ITEMS>
 __global__ void __launch_bounds__(ws_nt(ITEMS)) k_warp_sort(
-    const SegDev* __restrict__ segs, int64_t nsegs, const Rec* __restrict__ recA,
-    const Rec* __restrict__ recB, const uint8_t* __restrict__ arena, int64_t alen,
+    const SegDev* __restrict__ segs, int64_t nsegs, Rec* __restrict__ recA,
+    Rec* __restrict__ recB, const uint8_t* __restrict__ arena, int64_t alen,
     int64_t* __restrict__ out_h, int64_t* __restrict__ lcps, Counters* __restrict__ ctr) {
     constexpr int CAP = 32 * ITEMS, WS_NT = ws_nt(ITEMS);
     __shared__ int64_t s_h[WS_NT / 32][CAP];
@@ -351,7 +375,7 @@ __global__ void __launch_bounds__(ws_nt(ITEMS)) k_warp_sort(
     const SegDev sg = segs[gw];
     const int m = sg.n;
     const int64_t lo = sg.lo;
-    const Rec* segrec = ((sg.flags & SEG_IN_B) ? recB : recA) + lo;
+    Rec* segrec = ((sg.flags & SEG_IN_B) ? recB : recA) + lo;
     const int nv = sg.flags & SEG_NV_MASK;
     int64_t* wh = s_h[w];
     uint16_t* wo = s_o[w];
@@ -531,8 +555,8 @@ __device__ void cta_bitonic_generic(uint64_t (&key)[8], uint32_t (&meta)[8], int
 
 template <int W>
 __global__ void __launch_bounds__(32 * W, 24 / W) k_cta_sort(
-    const SegDev* __restrict__ segs, int64_t nsegs, const Rec* __restrict__ recA,
-    const Rec* __restrict__ recB, const uint8_t* __restrict__ arena, int64_t alen,
+    const SegDev* __restrict__ segs, int64_t nsegs, Rec* __restrict__ recA,
+    Rec* __restrict__ recB, const uint8_t* __restrict__ arena, int64_t alen,
     int64_t* __restrict__ out_h, int64_t* __restrict__ lcps, Counters* __restrict__ ctr) {
     constexpr int ITEMS = 8, NT = 32 * W;
     extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -541,7 +565,7 @@ __global__ void __launch_bounds__(32 * W, 24 / W) k_cta_sort(
     const SegDev sg = segs[blockIdx.x];
     const int m = sg.n;
     const int64_t lo = sg.lo;
-    const Rec* segrec = ((sg.flags & SEG_IN_B) ? recB : recA) + lo;
+    Rec* segrec = ((sg.flags & SEG_IN_B) ? recB : recA) + lo;
     const int nv = sg.flags & SEG_NV_MASK;
     const int64_t d0 = sg.depth;
     int64_t* lcp_seg = lcps ? lcps + lo : nullptr;
@@ -552,27 +576,28 @@ __global__ void __launch_bounds__(32 * W, 24 / W) k_cta_sort(
     uint64_t key[ITEMS];
     uint32_t meta[ITEMS];
     const int base = threadIdx.x * ITEMS;  // first slot of this thread
+    int64_t cd = d0;  // record cache: words from depth cd, cnv of them valid
+    int cnv = nv;
 #pragma unroll
     for (int e = 0; e < ITEMS; e++) {
         const int i = base + e;
-        if (i < m) {
-            key[e] = seg_word(segrec, i, d0, nv, depth, arena, alen, S.h[i], fetches);
-            meta[e] = (1u << 22) | (uint32_t)i;
-        } else {
-            key[e] = ~0ull;
-            meta[e] = ((uint32_t)i << 11) | (uint32_t)i;
-        }
+        key[e] = ~0ull;
+        meta[e] = i < m ? (1u << 22) | (uint32_t)i : ((uint32_t)i << 11) | (uint32_t)i;
     }
-    bool group_mode = false, first_round = true;
+    rekey<ITEMS, true>(key, meta, segrec, S.h, cd, cnv, depth, arena, alen, fetches, S.xk, base,
+                       256 * W, threadIdx.x, NT);
+    bool group_mode = false, first_round = true, used_two = false;
+    int rounds = 0;
     uint64_t k1[ITEMS];  // second word of the slot in a two-word round
     for (;;) {
         // ---- sort by (group, word, tag): packed u32/u64 when the bits fit --
         bool two = false;  // this round sorts by the words at depth and depth + 8
+        int jb = 0;        // ... the leading jb characters of the second one
         {
             // the first round may take the record's second cached word along
             // when both words' varying bits fit one u64 beside the tag: one
             // round instead of two for low-entropy keys (DNA: 4 bits/char)
-            const bool try_two = first_round && nv >= 2;
+            const bool try_two = first_round && cnv >= 2;  // (first round: depth == cd)
             uint64_t o = 0, a = ~0ull, o1 = 0, a1 = ~0ull;
 #pragma unroll
             for (int e = 0; e < ITEMS; e++) {
@@ -608,16 +633,27 @@ __global__ void __launch_bounds__(32 * W, 24 / W) k_cta_sort(
             }
             const Pext px = pext_setup(o ^ a);
             if (try_two) {
-                const int cb1 = __popcll(o1 ^ a1);
-                // u32 single-word rounds are cheaper unless ties are likely
-                two = px.cb + cb1 <= 53 && (px.cb > 21 || (1u << px.cb) < 64u * (uint32_t)m);
-                if (!two) {
+                // as many leading characters of word1 as fit beside word0's
+                // varying bits in 53 bits; u32 single-word rounds are cheaper
+                // when ties after word0 are unlikely (m^2 <= 2^cb0)
+                const uint64_t V1 = o1 ^ a1;
+                int bits = px.cb;
+                while (jb < WORD && bits + __popc((uint32_t)(V1 >> (56 - 8 * jb)) & 255u) <= 53)
+                    bits += __popc((uint32_t)(V1 >> (56 - 8 * jb)) & 255u), jb++;
+                const bool u32_ok = px.cb <= 21 && (uint64_t)m * (uint64_t)m <= (1ull << px.cb);
+                two = jb > 0 && !u32_ok;
+                if (!two) jb = 0;
+                const uint64_t keep1 = jb == WORD ? ~0ull : ~(~0ull >> (8 * jb));
 #pragma unroll
-                    for (int e = 0; e < ITEMS; e++) k1[e] = 0;  // single-word round
-                }
+                for (int e = 0; e < ITEMS; e++) k1[e] &= keep1;  // window of jb chars (0: none)
+                o1 &= keep1;
+                a1 &= keep1;
             }
             const int mode = two ? 0 : (first_round && px.cb <= 21) ? 1 : (px.cb <= 42) ? 2 : 3;
-            if (mode != 3) {
+            if (px.cb == 0 && (!two || (o1 ^ a1) == 0)) {
+                // every active slot has the same window: already in (group,
+                // tag) order, nothing to sort
+            } else if (mode != 3) {
                 // stage the words by tag (kb, kb1) and by slot (xk), pack the
                 // varying bits of every slot in one rolled loop, build the
                 // sort values: two-word (word0 bits | word1 bits | tag), u32
@@ -689,11 +725,13 @@ __global__ void __launch_bounds__(32 * W, 24 / W) k_cta_sort(
                 cta_bitonic_generic<W>(key, meta, base, S);
             }
         }
+        rounds++;
+        used_two |= two;
         // ---- LCPs at word changes, run breaks -------------------------------
         // (a two-word round compares (word, word1); a string whose first word
         // holds its terminator has word1 = 0, so pair equality is string
         // equality within the 16-character window)
-        const int step = two ? 2 * WORD : WORD;
+        const int step = WORD + jb;
         uint64_t prev_last = __shfl_up_sync(0xffffffffu, key[ITEMS - 1], 1);
         uint64_t prev_last1 = __shfl_up_sync(0xffffffffu, k1[ITEMS - 1], 1);
         if (lane == 31) {
@@ -714,7 +752,8 @@ __global__ void __launch_bounds__(32 * W, 24 / W) k_cta_sort(
             const int grp = meta[e] >> 11 & 0x7ff;
             brk[e] = true;
             tw[e] = term_pos(key[e]);
-            if (two && tw[e] == WORD) tw[e] = WORD + term_pos(k1[e]);
+            // masked word1: a zero byte at jb marks the window end (tw == step)
+            if (two && tw[e] == WORD) tw[e] = WORD + min(term_pos(k1[e]), jb);
             if (act && i != grp) {
                 const uint64_t pk = e ? key[e - 1] : prev_last;
                 const uint64_t pk1 = e ? k1[e - 1] : prev_last1;
@@ -786,7 +825,7 @@ __global__ void __launch_bounds__(32 * W, 24 / W) k_cta_sort(
         __syncthreads();
         uint32_t lmax = 0;
         for (int v = 0; v < W; v++) lmax = max(lmax, S.wcnt[v]);
-        if (W >= GROUP_MODE_MIN_W && lmax <= 256) {
+        if (lmax <= (W >= GROUP_MODE_MIN_W ? 256u : 64u)) {
             // ---- group mode: slot order + list of the kept runs -------------
 #pragma unroll
             for (int e = 0; e < ITEMS; e++) S.ord[base + e] = (uint16_t)(meta[e] & 0x7ff);
@@ -830,12 +869,8 @@ __global__ void __launch_bounds__(32 * W, 24 / W) k_cta_sort(
             const uint32_t tag = meta[e] & 0x7ff;
             meta[e] = keep[e] ? ((1u << 22) | ((cur - 1) << 11) | tag) : (((uint32_t)i << 11) | tag);
         }
-#pragma unroll
-        for (int e = 0; e < ITEMS; e++)
-            if (meta[e] >> 22 & 1) {
-                const uint32_t tag = meta[e] & 0x7ff;
-                key[e] = seg_word(segrec, tag, d0, nv, depth, arena, alen, S.h[tag], fetches);
-            }
+        rekey<ITEMS, true>(key, meta, segrec, S.h, cd, cnv, depth, arena, alen, fetches, S.xk, base,
+                       256 * W, threadIdx.x, NT);
         __syncthreads();  // S.wmax / S.last_key / S.wcnt / S.red reuse
     }
     if (!group_mode) {
@@ -848,17 +883,20 @@ __global__ void __launch_bounds__(32 * W, 24 / W) k_cta_sort(
             const int g0 = S.gs[g], gn = S.ge[g] - g0 + 1;
             const int64_t d = depth;
             if (gn <= 32) {
-                uint64_t k1[1];
-                warp_finish<1>(S.h, S.ord, S.kb, S.xk, segrec, d0, nv, g0, gn, d, k1, arena, alen, lcp_seg, fetches, lane);
+                uint64_t r1[1];
+                warp_finish<1>(S.h, S.ord, S.kb, S.xk, segrec, cd, cnv, g0, gn, d, r1, arena, alen, lcp_seg, fetches, lane);
             } else if (gn <= 64) {
-                uint64_t k2[2];
-                warp_finish<2>(S.h, S.ord, S.kb, S.xk, segrec, d0, nv, g0, gn, d, k2, arena, alen, lcp_seg, fetches, lane);
-            } else if (gn <= 128) {
-                uint64_t k4[4];
-                warp_finish<4>(S.h, S.ord, S.kb, S.xk, segrec, d0, nv, g0, gn, d, k4, arena, alen, lcp_seg, fetches, lane);
-            } else {
-                uint64_t k8[8];
-                warp_finish<8>(S.h, S.ord, S.kb, S.xk, segrec, d0, nv, g0, gn, d, k8, arena, alen, lcp_seg, fetches, lane);
+                uint64_t r2[2];
+                warp_finish<2>(S.h, S.ord, S.kb, S.xk, segrec, cd, cnv, g0, gn, d, r2, arena, alen, lcp_seg, fetches, lane);
+            } else if constexpr (W >= GROUP_MODE_MIN_W) {
+                // (smaller CTAs enter group mode only with runs <= 64)
+                if (gn <= 128) {
+                    uint64_t r4[4];
+                    warp_finish<4>(S.h, S.ord, S.kb, S.xk, segrec, cd, cnv, g0, gn, d, r4, arena, alen, lcp_seg, fetches, lane);
+                } else {
+                    uint64_t r8[8];
+                    warp_finish<8>(S.h, S.ord, S.kb, S.xk, segrec, cd, cnv, g0, gn, d, r8, arena, alen, lcp_seg, fetches, lane);
+                }
             }
         }
     }
@@ -866,7 +904,14 @@ __global__ void __launch_bounds__(32 * W, 24 / W) k_cta_sort(
     for (int i = threadIdx.x; i < m; i += NT) out_h[lo + i] = S.h[S.ord[i]];
     fetches = __reduce_add_sync(0xffffffffu, fetches);
     if (lane == 0 && fetches) atomicAdd(&ctr->seg_fetches, (unsigned long long)fetches);
-    if (threadIdx.x == 0) atomicAdd(&ctr->small_elems, (unsigned long long)m);
+    if (threadIdx.x == 0) {
+        atomicAdd(&ctr->small_elems, (unsigned long long)m);
+        unsigned long long* fc = g_fin_ctr + 4 * (W == 2 ? 0 : W == 4 ? 1 : 2);
+        atomicAdd(fc + 0, 1ull);
+        atomicAdd(fc + 1, (unsigned long long)rounds);
+        atomicAdd(fc + 2, used_two ? 1ull : 0ull);
+        atomicAdd(fc + 3, group_mode ? 1ull : 0ull);
+    }
 }
 
 }  // namespace s5g

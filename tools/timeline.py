@@ -25,8 +25,13 @@ e1.record()
 torch.cuda.synchronize()
 _lib.profile(enable=False)
 print(f"sort total (torch events): {e0.elapsed_time(e1):.3f} ms")
-last = {0: 0.0, 1: 0.0}
+last = {0: 0.0, 1: 0.0, 2: 0.0}
 for name, s, t0, t1 in _lib.timeline():
     gap = t0 - last[s]
     last[s] = t1
-    print(f"{'  ' * s}{name:18s} s{s} {t0:8.3f} {t1:8.3f}  dur {t1 - t0:7.3f}  gap {gap:7.3f}")
+    print(f"{"  " * s}{name:18s} s{s} {t0:8.3f} {t1:8.3f}  dur {t1 - t0:7.3f}  gap {gap:7.3f}")
+_lib.finisher_counters(reset=True)
+D.sort(ds, want_lcps=True)
+torch.cuda.synchronize()
+for k, v in _lib.finisher_counters().items():
+    print(k, v)
