@@ -138,31 +138,49 @@ __device__ __forceinline__ void warp_inlane_u64(uint64_t (&c)[IT], int i0, int k
     }
 }
 
+template <int J, int IT>
+__device__ __forceinline__ void warp_inlane_u(uint64_t (&c)[IT], bool up) {
+#pragma unroll
+    for (int e = 0; e < IT; e++) {
+        const int f = e ^ J;
+        if (f > e) cex_u64(c[e], c[f], up);
+    }
+}
+
 template <int IT>
 __device__ __forceinline__ void warp_bitonic_u64(uint64_t (&c)[IT], int lane) {
     constexpr int P = 32 * IT;
     const int i0 = lane * IT;
+    // k < IT (only when IT = 4, 8): directions vary inside the thread
+    if constexpr (IT >= 4) {
+        warp_inlane_u64<1, IT>(c, i0, 2);
+        warp_inlane_u64<2, IT>(c, i0, 4);
+        warp_inlane_u64<1, IT>(c, i0, 4);
+    } else if constexpr (IT == 2) {
+        warp_inlane_u64<1, IT>(c, i0, 2);
+    }
+    if constexpr (IT >= 8) {
+        warp_inlane_u64<4, IT>(c, i0, 8);
+        warp_inlane_u64<2, IT>(c, i0, 8);
+        warp_inlane_u64<1, IT>(c, i0, 8);
+    }
 #pragma unroll 1
-    for (int k = 2; k <= P; k <<= 1) {
+    for (int k = 2 * IT; k <= P; k <<= 1) {
+        const bool upk = (i0 & k) == 0;
+        // partner in another lane; direction uniform over e
 #pragma unroll 1
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            if (j >= IT) {
-                // partner in another lane; direction uniform over e
-                const int lx = j / IT;
-                const bool keep_min = ((i0 & j) == 0) == ((i0 & k) == 0);
+        for (int j = k >> 1; j >= IT; j >>= 1) {
+            const int lx = j / IT;
+            const bool keep_min = ((i0 & j) == 0) == upk;
 #pragma unroll
-                for (int e = 0; e < IT; e++) {
-                    const uint64_t o = __shfl_xor_sync(0xffffffffu, c[e], lx);
-                    c[e] = ((o < c[e]) == keep_min) ? o : c[e];
-                }
-            } else if (j == 1) {
-                if constexpr (IT > 1) warp_inlane_u64<1, IT>(c, i0, k);
-            } else if (j == 2) {
-                if constexpr (IT > 2) warp_inlane_u64<2, IT>(c, i0, k);
-            } else {
-                if constexpr (IT > 4) warp_inlane_u64<4, IT>(c, i0, k);
+            for (int e = 0; e < IT; e++) {
+                const uint64_t o = __shfl_xor_sync(0xffffffffu, c[e], lx);
+                c[e] = ((o < c[e]) == keep_min) ? o : c[e];
             }
         }
+        if constexpr (IT >= 8) warp_inlane_u<4, IT>(c, upk);
+        if constexpr (IT >= 4) warp_inlane_u<2, IT>(c, upk);
+        if constexpr (IT >= 2) warp_inlane_u<1, IT>(c, upk);
     }
 }
 
@@ -428,6 +446,7 @@ struct CtaSortSmem {
     uint64_t red[4 * W];
     uint64_t last_key[W], last_key1[W];
     uint32_t first_brk[W], first_act[W], wmax[W], wcnt[W];
+    Pext px[2];  // the round's bit-extract plans (read in the packing loop)
 };
 
 // In-lane stage at distance J < 8.  The direction bit (slot & k) is the same
@@ -447,46 +466,61 @@ __device__ __forceinline__ void cta_inlane(T (&c)[8], int base, int k) {
     }
 }
 
+// In-lane stage at distance J < 8 once k >= 8: one direction for all 8
+// slots of the thread (base is a multiple of 8).
+template <int J, typename T>
+__device__ __forceinline__ void cta_inlane_u(T (&c)[8], bool up) {
+#pragma unroll
+    for (int e = 0; e < 8; e++) {
+        const int f = e ^ J;
+        if (f > e) {
+            const bool sw = (c[f] < c[e]) == up;
+            const T x = c[e], y = c[f];
+            c[e] = sw ? y : x;
+            c[f] = sw ? x : y;
+        }
+    }
+}
+
 template <int W, typename T>
 __device__ void cta_bitonic(T (&c)[8], int base, T* xch) {
-    constexpr int P = 256 * W;
+    constexpr int P = 256 * W, NT = 32 * W;
+    // k = 2, 4: directions vary inside the thread
+    cta_inlane<1>(c, base, 2);
+    cta_inlane<2>(c, base, 4);
+    cta_inlane<1>(c, base, 4);
 #pragma unroll 1
-    for (int k = 2; k <= P; k <<= 1) {
+    for (int k = 8; k <= P; k <<= 1) {
+        const bool upk = (base & k) == 0;
+        // distances >= 8: partner slot differs in a lane/warp bit, and the
+        // keep-the-smaller decision is uniform across the thread's slots
 #pragma unroll 1
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            if (j == 1) {
-                cta_inlane<1>(c, base, k);
-            } else if (j == 2) {
-                cta_inlane<2>(c, base, k);
-            } else if (j == 4) {
-                cta_inlane<4>(c, base, k);
-            } else {
-                // distance >= 8: partner slot differs in a lane/warp bit, and the
-                // keep-the-smaller decision is uniform across the thread's slots
-                const bool keep_min = ((base & j) == 0) == ((base & k) == 0);
-                if (j < 256) {
-                    const int lx = j / 8;
+        for (int j = k >> 1; j >= 8; j >>= 1) {
+            const bool keep_min = ((base & j) == 0) == upk;
+            if (j < 256) {
+                const int lx = j / 8;
 #pragma unroll
-                    for (int e = 0; e < 8; e++) {
-                        const T o = __shfl_xor_sync(0xffffffffu, c[e], lx);
-                        c[e] = ((o < c[e]) == keep_min) ? o : c[e];
-                    }
-                } else {
-                    // [e][thread] layout: conflict-free; partner = thread ^ (j / 8)
-                    constexpr int NT = 32 * W;
-                    const int pt = threadIdx.x ^ (j / 8);
-#pragma unroll
-                    for (int e = 0; e < 8; e++) xch[e * NT + threadIdx.x] = c[e];
-                    __syncthreads();
-#pragma unroll
-                    for (int e = 0; e < 8; e++) {
-                        const T o = xch[e * NT + pt];
-                        c[e] = ((o < c[e]) == keep_min) ? o : c[e];
-                    }
-                    __syncthreads();
+                for (int e = 0; e < 8; e++) {
+                    const T o = __shfl_xor_sync(0xffffffffu, c[e], lx);
+                    c[e] = ((o < c[e]) == keep_min) ? o : c[e];
                 }
+            } else {
+                // [e][thread] layout: conflict-free; partner = thread ^ (j / 8)
+                const int pt = threadIdx.x ^ (j / 8);
+#pragma unroll
+                for (int e = 0; e < 8; e++) xch[e * NT + threadIdx.x] = c[e];
+                __syncthreads();
+#pragma unroll
+                for (int e = 0; e < 8; e++) {
+                    const T o = xch[e * NT + pt];
+                    c[e] = ((o < c[e]) == keep_min) ? o : c[e];
+                }
+                __syncthreads();
             }
         }
+        cta_inlane_u<4>(c, upk);
+        cta_inlane_u<2>(c, upk);
+        cta_inlane_u<1>(c, upk);
     }
 }
 
@@ -658,7 +692,10 @@ __global__ void __launch_bounds__(32 * W, 24 / W) k_cta_sort(
                 // varying bits of every slot in one rolled loop, build the
                 // sort values: two-word (word0 bits | word1 bits | tag), u32
                 // (word bits | tag) on the first round, else (group | bits | tag)
-                const Pext px1 = pext_setup(o1 ^ a1);
+                if (threadIdx.x == 0) {
+                    S.px[0] = px;
+                    S.px[1] = pext_setup(o1 ^ a1);
+                }
 #pragma unroll
                 for (int e = 0; e < ITEMS; e++) {
                     const uint32_t tag = meta[e] & 0x7ff;
@@ -671,8 +708,8 @@ __global__ void __launch_bounds__(32 * W, 24 / W) k_cta_sort(
                 __syncthreads();
                 const int lim = first_round ? m : 256 * W;
                 for (int q = threadIdx.x; q < lim; q += NT) {
-                    uint64_t v = pext_key(S.xk[q], px);
-                    if (two) v = (v << px1.cb) | pext_key(S.kb1[q], px1);
+                    uint64_t v = pext_key(S.xk[q], S.px[0]);
+                    if (two) v = (v << S.px[1].cb) | pext_key(S.kb1[q], S.px[1]);
                     S.xk[q] = v;
                 }
                 __syncthreads();
