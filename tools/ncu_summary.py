@@ -1,0 +1,54 @@
+"""Summarise an `ncu --set full` capture of one sort (bench.py --steps 1
+--warmup 0): per-kernel launches, time, DRAM bytes and occupancy/issue, as
+the committed profiles/<round>_ncu_kernels.csv and the traffic JSON that
+bench.py's roofline.traffic reads.
+
+usage: python tools/ncu_summary.py REPORT.ncu-rep OUT_PREFIX
+"""
+import csv
+import io
+import json
+import re
+import subprocess
+import sys
+
+rep, prefix = sys.argv[1], sys.argv[2]
+raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                     text=True, check=True).stdout
+rows = list(csv.reader(io.StringIO(raw)))
+h, units, data = rows[0], rows[1], rows[2:]
+col = {k: i for i, k in enumerate(h)}
+keep = ["Kernel Name", "Grid Size", "Block Size", "gpu__time_duration.sum",
+        "dram__bytes_read.sum", "dram__bytes_write.sum", "launch__registers_per_thread",
+        "sm__warps_active.avg.pct_of_peak_sustained_active",
+        "smsp__issue_active.avg.pct_of_peak_sustained_active",
+        "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"]
+scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "usecond": 1e-3, "msecond": 1.0,
+         "nsecond": 1e-6, "us": 1e-3, "ms": 1.0, "ns": 1e-6}
+
+
+def val(r, k):
+    v = float(r[col[k]].replace(",", ""))
+    return v * scale.get(units[col[k]], 1.0)
+
+
+with open(prefix + "_ncu_kernels.csv", "w", newline="") as f:
+    w = csv.writer(f)
+    w.writerow(keep)
+    w.writerow([units[col[k]] for k in keep])
+    for r in data:
+        w.writerow([r[col[k]] for k in keep])
+kern = {}
+for r in data:
+    name = re.sub(r"\(.*", "", r[col["Kernel Name"]]).replace("void ", "").replace("s5g::", "")
+    name = re.sub(r"\(int\)|\(bool\)", "", name)
+    e = kern.setdefault(name, {"launches": 0, "dram_bytes": 0.0, "ms": 0.0})
+    e["launches"] += 1
+    e["dram_bytes"] += val(r, "dram__bytes_read.sum") + val(r, "dram__bytes_write.sum")
+    e["ms"] += val(r, "gpu__time_duration.sum")
+for e in kern.values():
+    e["dram_bytes_per_launch"] = e["dram_bytes"] / e["launches"]
+json.dump({"source": f"ncu --set full, one C2 sort (bench.py --steps 1 --warmup 0), {prefix}_ncu_kernels.csv",
+           "kernels": kern}, open(prefix + "_traffic.json", "w"), indent=1)
+for k, e in sorted(kern.items(), key=lambda x: -x[1]["ms"]):
+    print(f"{k:28s} {e['launches']:3d} {e['ms']:8.3f} ms {e['dram_bytes'] / 1e9:8.3f} GB")
