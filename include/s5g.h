@@ -150,6 +150,22 @@ int s5g_load_delimited(uint8_t *data, int64_t len, int32_t delimiter, int64_t *o
  * (device): D and L. */
 int s5g_dist_stats(const int64_t *lcps, int64_t n, int64_t *out_D, int64_t *out_L, void *stream);
 
+/* K-way LCP merge of k <= 16 sorted runs (lcpmerge.kway_lcp_merge,
+ * lcpmerge.py:385-424, and the merge phase of parallel.partitioned_merge_sort,
+ * parallel.py:885-994).  Run j is handles[run_offsets[j] .. run_offsets[j+1])
+ * with its LCP array in lcps at the same positions (lcps[run start] is not
+ * read) and, when dchar != NULL, its distinguishing characters (fill_dchar
+ * convention; the cached comparisons of lcp_compare_cached).  run_offsets is
+ * a HOST array of k + 1 entries; everything else is device memory.  All
+ * strings share their first `shared` characters.  Output: the stable merge
+ * (ties to the earlier run) and its LCP array with out_lcps[0] = shared.
+ * Workspace: s5g_merge_workspace_bytes(n, k). */
+size_t s5g_merge_workspace_bytes(int64_t n, int32_t k);
+int s5g_kway_merge(const uint8_t *arena, int64_t arena_len, int32_t k, const int64_t *run_offsets,
+                   const int64_t *handles, const int64_t *lcps, const uint8_t *dchar,
+                   int64_t shared, int64_t *out_handles, int64_t *out_lcps, void *workspace,
+                   size_t workspace_bytes, void *stream, s5g_stats *stats);
+
 /* fill_dchar (basecase.py:36-42). */
 int s5g_fill_dchar(const uint8_t *arena, const int64_t *handles, const int64_t *lcps, int64_t n,
                    uint8_t *out_dchar, void *stream);

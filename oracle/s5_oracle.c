@@ -887,3 +887,103 @@ void s5o_dist_stats(const int64_t *lcps, const int64_t *lens, int64_t n, int64_t
     *D = d;
     *L = l;
 }
+
+/* ------------------------------------------------------------------ */
+/* K-way LCP merge: lcp_compare / lcp_compare_cached (lcpmerge.py:57-140)
+ * and the LoserTree tournament (lcpmerge.py:250-340), sequential.         */
+
+typedef struct { int64_t s, h; int c; } mplayer;  /* handle (-1 = done), lcp, cached char */
+
+/* game between players a < b; returns the winner, updates the loser */
+static int m_game(const uint8_t *buf, mplayer *P, int a, int b, int cached, s5o_stats *st)
+{
+    mplayer *A = &P[a], *B = &P[b];
+    if (A->s < 0) { A->h = 0; return b; }          /* lcpmerge.py:72-75 */
+    if (B->s < 0) { B->h = 0; return a; }
+    if (A->h < B->h) return b;                       /* lcpmerge.py:91-94 */
+    if (A->h > B->h) return a;
+    int64_t h = A->h;
+    int xa, xb;
+    if (cached) {                                    /* lcpmerge.py:117-135 */
+        xa = A->c; xb = B->c;
+        st->char_cmps++;
+        if (xa != 0 && xa == xb) {
+            h++;
+            for (;;) {
+                xa = buf[A->s + h]; xb = buf[B->s + h];
+                st->char_cmps++; st->merge_buffer_cmps++;
+                if (xa != 0 && xa == xb) { h++; continue; }
+                break;
+            }
+        }
+    } else {                                         /* lcpmerge.py:76-89 */
+        for (;;) {
+            xa = buf[A->s + h]; xb = buf[B->s + h];
+            st->char_cmps++; st->merge_buffer_cmps++;
+            if (xa != 0 && xa == xb) { h++; continue; }
+            break;
+        }
+    }
+    if (xa <= xb) { B->h = h; B->c = xb; return a; }
+    A->h = h; A->c = xa;
+    return b;
+}
+
+/* Merge k sorted runs (handles/lcps/dchar laid end to end, run j =
+ * [run_off[j], run_off[j+1])) into out_h / out_l; out_l[0] = shared. */
+void s5o_kway_merge(const uint8_t *buf, int k, const int64_t *run_off, const int64_t *handles,
+                    const int64_t *lcps, const uint8_t *dchar, int64_t shared, int64_t *out_h,
+                    int64_t *out_l, s5o_stats *st)
+{
+    int K = 1;
+    while (K < k) K *= 2;
+    mplayer *P = calloc((size_t)K, sizeof(mplayer));
+    int64_t *cur = calloc((size_t)K, sizeof(int64_t)), *end = calloc((size_t)K, sizeof(int64_t));
+    int *node = calloc((size_t)2 * K, sizeof(int));
+    int cached = dchar != NULL;
+    for (int j = 0; j < K; j++) {
+        P[j].s = -1;
+        if (j < k && run_off[j] < run_off[j + 1]) {
+            cur[j] = run_off[j];
+            end[j] = run_off[j + 1];
+            P[j].s = handles[cur[j]];
+            P[j].h = shared;
+            P[j].c = cached ? buf[P[j].s + shared] : 0;
+        }
+    }
+    /* bottom-up tournament: node[K + j] = j, inner nodes keep the loser */
+    int *win = calloc((size_t)2 * K, sizeof(int));
+    for (int j = 0; j < K; j++) win[K + j] = j;
+    for (int v = K - 1; v >= 1; v--) {
+        int a = win[2 * v], b = win[2 * v + 1];
+        int lo = a < b ? a : b, hi = a < b ? b : a;
+        int w = m_game(buf, P, lo, hi, cached, st);
+        win[v] = w;
+        node[v] = w == lo ? hi : lo;
+    }
+    int w = win[1];
+    int64_t n = run_off[k] - run_off[0];
+    for (int64_t pos = 0; pos < n; pos++) {
+        out_h[pos] = P[w].s;
+        out_l[pos] = P[w].h;
+        cur[w]++;
+        if (cur[w] < end[w]) {
+            P[w].s = handles[cur[w]];
+            P[w].h = lcps[cur[w]];
+            P[w].c = cached ? dchar[cur[w]] : 0;
+        } else {
+            P[w].s = -1;
+            P[w].h = 0;
+        }
+        int x = w;
+        for (int v = (K + w) / 2; v >= 1; v /= 2) {
+            int y = node[v];
+            int lo = x < y ? x : y, hi = x < y ? y : x;
+            int r = m_game(buf, P, lo, hi, cached, st);
+            node[v] = r == lo ? hi : lo;
+            x = r;
+        }
+        w = x;
+    }
+    free(P); free(cur); free(end); free(node); free(win);
+}

@@ -17,10 +17,12 @@ from .strset import (
     load_delimited,
 )
 from .ssss import SplitterTree, StepRecord, child_depths, s5_sort, tree_capacity
-from .parallel import parallel_s5
+from .parallel import parallel_s5, partitioned_merge_sort
+from .lcpmerge import LcpStream, binary_lcp_merge, kway_lcp_merge
 
 __all__ = [
-    "LCP_UNDEF", "WORD_CHARS", "SortedWithLcp", "SortStats", "SplitterTree", "StepRecord",
+    "LCP_UNDEF", "LcpStream", "WORD_CHARS", "SortedWithLcp", "binary_lcp_merge", "kway_lcp_merge",
+    "partitioned_merge_sort", "SortStats", "SplitterTree", "StepRecord",
     "StringSet", "child_depths", "from_strings", "load_delimited", "parallel_s5", "s5_sort",
     "tree_capacity",
 ]

@@ -73,6 +73,9 @@ SIGNATURES = {
     "s5g_launch_count": (C.c_ulonglong, []),
     "s5g_set_l2_fetch_granularity": (None, [C.c_int]),
     "s5g_finisher_counters": (C.c_int, [C.POINTER(C.c_ulonglong), C.c_int, C.c_int]),
+    "s5g_merge_workspace_bytes": (C.c_size_t, [_i64, _i32]),
+    "s5g_kway_merge": (C.c_int, [_p, _i64, _i32, C.POINTER(_i64), _p, _p, _p, _i64, _p, _p, _p,
+                                 C.c_size_t, _p, C.POINTER(Stats)]),
     "s5g_last_error": (C.c_char_p, []),
     "s5g_version": (C.c_int, []),
 }

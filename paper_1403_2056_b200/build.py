@@ -12,7 +12,7 @@ CSRC = PKG / "csrc"
 LIB_DIR = PKG / "_lib"
 LIB_PATH = LIB_DIR / "libs5gpu.so"
 SOURCES = [CSRC / "s5g.cu"]
-DEPS = SOURCES + [CSRC / "s5g_device.cuh", CSRC / "s5g_kernels.cuh", CSRC / "s5g_warpsort.cuh", ROOT / "include" / "s5g.h"]
+DEPS = SOURCES + [CSRC / "s5g_device.cuh", CSRC / "s5g_kernels.cuh", CSRC / "s5g_warpsort.cuh", CSRC / "s5g_merge.cuh", ROOT / "include" / "s5g.h"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

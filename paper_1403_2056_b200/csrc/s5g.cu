@@ -15,6 +15,7 @@
 #include "s5g.h"
 #include "s5g_kernels.cuh"
 #include "s5g_warpsort.cuh"
+#include "s5g_merge.cuh"
 
 namespace s5g {
 
@@ -1839,6 +1840,87 @@ int s5g_dist_stats(const int64_t* lcps, int64_t n, int64_t* out_D, int64_t* out_
     CK(cudaStreamSynchronize(st));
     *out_D = (int64_t)h[0];
     *out_L = (int64_t)h[1];
+    return 0;
+}
+
+static int64_t merge_ncand_cap(int64_t n, int32_t k) { return n / MERGE_M + k + 1; }
+
+size_t s5g_merge_workspace_bytes(int64_t n, int32_t k) {
+    const int64_t nc = merge_ncand_cap(std::max<int64_t>(n, 0), std::max(k, 1));
+    const int64_t nch = n / MC_CHUNK + 2;
+    return (size_t)(nc * (int64_t)std::max(k, 1) * 8 + nc * 8 + std::max<int64_t>(n, 1) * 4 +
+                    nc * 4 + nch * 4) + 64 + 5 * 256;
+}
+
+int s5g_kway_merge(const uint8_t* arena, int64_t arena_len, int32_t k, const int64_t* run_offsets,
+                   const int64_t* handles, const int64_t* lcps, const uint8_t* dchar,
+                   int64_t shared, int64_t* out_handles, int64_t* out_lcps, void* workspace,
+                   size_t workspace_bytes, void* stream, s5g_stats* stats) {
+    if (k < 1 || k > MERGE_KMAX) return fail(S5G_E_INVALID, "k must be in 1..16");
+    if (!run_offsets) return fail(S5G_E_INVALID, "null run_offsets");
+    if (shared < 0) return fail(S5G_E_INVALID, "negative shared prefix");
+    MergeRuns R{};
+    R.k = k;
+    int64_t ncand = 0;
+    for (int j = 0; j <= k; j++) {
+        R.off[j] = run_offsets[j] - run_offsets[0];
+        if (j && R.off[j] < R.off[j - 1]) return fail(S5G_E_INVALID, "run offsets decrease");
+    }
+    for (int j = 0; j < k; j++) {
+        R.coff[j] = ncand;
+        ncand += (R.off[j + 1] - R.off[j] + MERGE_M - 1) / MERGE_M;
+    }
+    R.coff[k] = ncand;
+    const int64_t n = R.off[k];
+    if (n == 0) return 0;
+    if (n > INT32_MAX) return fail(S5G_E_INVALID, "n exceeds 2^31-1");
+    if (!arena || !handles || !lcps || !out_handles || !out_lcps) return fail(S5G_E_INVALID, "null buffer");
+    cudaStream_t st = (cudaStream_t)stream;
+    handles += run_offsets[0];
+    lcps += run_offsets[0];
+    if (dchar) dchar += run_offsets[0];
+    if (workspace_bytes < s5g_merge_workspace_bytes(n, k) || !workspace)
+        return fail(S5G_E_WORKSPACE, "workspace too small");
+    size_t off = 0;
+    auto take = [&](size_t bytes) -> uint8_t* {
+        off = (off + 255) & ~size_t(255);
+        uint8_t* p = (uint8_t*)workspace + off;
+        off += bytes;
+        return p;
+    };
+    int64_t* cut = (int64_t*)take(8 * ncand * k);
+    int64_t* cand_out = (int64_t*)take(8 * ncand);
+    int32_t* cand_at = (int32_t*)take(4 * n);
+    int32_t* order = (int32_t*)take(4 * ncand);
+    const int64_t nch = (n + MC_CHUNK - 1) / MC_CHUNK;
+    uint32_t* chunk = (uint32_t*)take(4 * nch);
+    int64_t* d_n = (int64_t*)take(8);
+    unsigned long long* words = (unsigned long long*)take(8);
+    CK(cudaMemsetAsync(words, 0, 8, st));
+    if (k == 1) {
+        CK(cudaMemcpyAsync(out_handles, handles, 8 * n, cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemcpyAsync(out_lcps, lcps, 8 * n, cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemcpyAsync(out_lcps, &shared, 8, cudaMemcpyHostToDevice, st));
+        CK(cudaStreamSynchronize(st));
+        return 0;
+    }
+    CK(cudaMemsetAsync(cand_at, 0xff, 4 * n, st));
+    g_launches += 6;
+    k_merge_cands<<<blocks_for(ncand, 128), 128, 0, st>>>(arena, arena_len, handles, R, ncand,
+                                                          shared, cut, cand_out, cand_at, words);
+    k_mc_count<<<(unsigned)nch, MC_NT, 0, st>>>(cand_at, n, chunk);
+    k_ld_scan<<<1, 1024, 0, st>>>(chunk, nch, d_n);
+    k_mc_write<<<(unsigned)nch, MC_NT, 0, st>>>(cand_at, n, chunk, order);
+    k_merge_jobs<<<blocks_for(ncand, 128), 128, 0, st>>>(arena, arena_len, handles, lcps, dchar, R,
+                                                         order, ncand, shared, cut, cand_out,
+                                                         out_handles, out_lcps, words);
+    k_merge_fix<<<blocks_for(ncand, 256), 256, 0, st>>>(arena, arena_len, order, ncand, cand_out,
+                                                         shared, out_handles, out_lcps, words);
+    CK(cudaGetLastError());
+    unsigned long long hw = 0;
+    CK(cudaMemcpyAsync(&hw, words, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (stats) stats->word_fetches += (int64_t)hw;
     return 0;
 }
 

@@ -233,3 +233,26 @@ def dist_stats(lcps: torch.Tensor) -> tuple[int, int]:
     check(lib().s5g_dist_stats(lcps.data_ptr(), lcps.numel(), C.byref(D), C.byref(L),
                                torch.cuda.current_stream(lcps.device).cuda_stream))
     return int(D.value), int(L.value)
+
+
+def kway_merge(ds: DeviceStrings, run_offsets, handles: torch.Tensor, lcps: torch.Tensor,
+               dchar: torch.Tensor | None = None, shared: int = 0, stats: Stats | None = None):
+    """Stable K-way LCP merge of sorted runs laid end to end in handles/lcps
+    (run j = [run_offsets[j], run_offsets[j+1])); s5g_kway_merge.  Returns
+    (out_handles, out_lcps) with out_lcps[0] = shared."""
+    off = np.ascontiguousarray(run_offsets, dtype=np.int64)
+    k = len(off) - 1
+    n = int(off[-1] - off[0])
+    dev = handles.device
+    out_h = torch.empty(n, dtype=torch.int64, device=dev)
+    out_l = torch.empty(n, dtype=torch.int64, device=dev)
+    wsb = int(lib().s5g_merge_workspace_bytes(n, max(k, 1)))
+    ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
+    st = stats if stats is not None else Stats()
+    check(lib().s5g_kway_merge(ds.arena.data_ptr(), ds.arena_len, k,
+                               off.ctypes.data_as(C.POINTER(C.c_int64)), handles.data_ptr(),
+                               lcps.data_ptr(), dchar.data_ptr() if dchar is not None else None,
+                               int(shared), out_h.data_ptr(), out_l.data_ptr(), ws.data_ptr(),
+                               ws.numel(), torch.cuda.current_stream(dev).cuda_stream,
+                               C.byref(st)))
+    return out_h, out_l

@@ -120,6 +120,41 @@ def main() -> None:
                 arrays[f"{name}/keys_d{dep}"] = strset.extract_keys(sset, handles, dep)
         meta["cases"][name] = case
 
+    # K-way LCP merge (lcpmerge.py) and partitioned_merge_sort (parallel.py:885)
+    from strsort import lcpmerge  # noqa: E402
+    from strsort.parallel import partitioned_merge_sort  # noqa: E402
+    merge_cases = {}
+    for name in ("random_n17", "random_3000", "urls_2000", "dups_2000", "deep_prefix_1500",
+                 "suffixes_1800", "all_equal_700", "shuffled_dups_2500", "high_bytes_1500"):
+        buf = arrays[f"{name}/buffer"].tobytes()
+        handles = arrays[f"{name}/handles"]
+        sset = strset.StringSet(buf, handles)
+        for K in (2, 3, 5):
+            cuts = np.linspace(0, len(handles), K + 1).astype(np.int64)
+            streams, hs, ls, cs = [], [], [], []
+            for j in range(K):
+                sub = sset.with_handles(handles[cuts[j]:cuts[j + 1]])
+                r = ssss.s5_sort(sub, want_lcps=True, want_dchar=True)
+                streams.append(lcpmerge.LcpStream(sset, r.set.handles, r.lcps, r.dchar))
+                hs.append(r.set.handles), ls.append(r.lcps), cs.append(r.dchar)
+            h0, l0 = lcpmerge.kway_lcp_merge(streams, cached=False)
+            h1, l1 = lcpmerge.kway_lcp_merge(streams, cached=True)
+            assert np.array_equal(h0, h1) and np.array_equal(l0, l1), (name, K)
+            assert np.array_equal(h0, arrays[f"{name}/out_handles"]), (name, K)
+            assert np.array_equal(l0, arrays[f"{name}/lcps"]), (name, K)
+            pre = f"merge_{name}_k{K}"
+            arrays[f"{pre}/run_off"] = cuts
+            arrays[f"{pre}/run_handles"] = np.concatenate(hs)
+            arrays[f"{pre}/run_lcps"] = np.concatenate(ls)
+            arrays[f"{pre}/run_dchar"] = np.concatenate(cs)
+            arrays[f"{pre}/out_handles"] = h0
+            arrays[f"{pre}/out_lcps"] = l0
+            merge_cases[pre] = {"case": name, "K": K}
+        pm = partitioned_merge_sort(sset, K=4, p=2, want_lcps=True, t_medium=512)
+        assert np.array_equal(pm.set.handles, arrays[f"{name}/out_handles"]), name
+        assert np.array_equal(pm.lcps, arrays[f"{name}/lcps"]), name
+    meta["merge"] = merge_cases
+
     # splitter-tree / classify / distribute known answers
     rng = np.random.default_rng(7)
     kat = {}

@@ -42,3 +42,15 @@ def kat(name):
     out = {k[len(pre):]: v for k, v in arrays.items() if k.startswith(pre)}
     out.update(meta["kat"][name])
     return out
+
+
+def merges():
+    return sorted(load()[1].get("merge", {}))
+
+
+def merge(name):
+    arrays, meta = load()
+    pre = name + "/"
+    out = {k[len(pre):]: v for k, v in arrays.items() if k.startswith(pre)}
+    out.update(meta["merge"][name])
+    return out

@@ -115,3 +115,20 @@ def test_certificate_detects_faults():
     assert oracle.certify(buf, hin, bad, lcps)[0] == 3
     badl = lcps.copy(); badl[7] += 1
     assert oracle.certify(buf, hin, hout, badl)[0] == 4
+
+
+# --- K-way LCP merge (lcpmerge.py) against the reference's own merges --------
+
+@pytest.mark.parametrize("name", G.merges())
+@pytest.mark.parametrize("cached", [False, True])
+def test_oracle_kway_merge_matches_reference(name, cached):
+    m = G.merge(name)
+    c = G.case(m["case"])
+    oh, ol, st = oracle.kway_merge(c["buffer"], m["run_off"], m["run_handles"], m["run_lcps"],
+                                   m["run_dchar"] if cached else None)
+    ol[0] = -1  # the reference's LCP_UNDEF convention without output arrays
+    assert np.array_equal(oh, m["out_handles"])
+    assert np.array_equal(ol, m["out_lcps"])
+    if cached:
+        _, _, st0 = oracle.kway_merge(c["buffer"], m["run_off"], m["run_handles"], m["run_lcps"])
+        assert st["merge_buffer_cmps"] <= st0["merge_buffer_cmps"]
