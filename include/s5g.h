@@ -117,13 +117,14 @@ int s5g_classify(const uint64_t *keys, int64_t n, const uint64_t *tree,
 /* Multi-GPU partition step (the G-rank form of _phased_step's classify,
  * parallel.py:359-398): out_rank[i] = number of splitters
  * (splitters[splitter_off[j] .. splitter_off[j+1]), splitter_gidx[j]) ordered
- * before (string at handles[i], base_index + i) -- full-string comparison,
- * ties broken by global input index, so equal strings keep input order
- * across ranks.  All pointers are device pointers. */
+ * before (string at handles[i], its global input index) -- full-string
+ * comparison, ties broken by global input index, so equal strings keep input
+ * order across ranks.  The global index is string_gidx[i], or base_index + i
+ * when string_gidx is NULL.  All pointers are device pointers. */
 int s5g_partition(const uint8_t *arena, int64_t arena_len, const int64_t *handles, int64_t n,
-                  int64_t base_index, const uint8_t *splitters, const int64_t *splitter_off,
-                  const int64_t *splitter_gidx, int32_t nsplitters, int32_t *out_rank,
-                  void *stream);
+                  int64_t base_index, const int64_t *string_gidx, const uint8_t *splitters,
+                  const int64_t *splitter_off, const int64_t *splitter_gidx, int32_t nsplitters,
+                  int32_t *out_rank, void *stream);
 
 /* String lengths (StringSet.ends - handles, strset.py:64-78). */
 int s5g_lengths(const uint8_t *arena, int64_t arena_len, const int64_t *handles, int64_t n,

@@ -707,12 +707,13 @@ __device__ __forceinline__ int cmp_string_splitter(const uint8_t* __restrict__ a
 
 __global__ void k_partition(const uint8_t* __restrict__ arena, int64_t alen,
                             const int64_t* __restrict__ handles, int64_t n, int64_t base_index,
+                            const int64_t* __restrict__ str_gidx,
                             const uint8_t* __restrict__ sp_blob, const int64_t* __restrict__ sp_off,
                             const int64_t* __restrict__ sp_gidx, int nsp,
                             int32_t* __restrict__ out_rank) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const int64_t h = handles[i], g = base_index + i;
+    const int64_t h = handles[i], g = str_gidx ? str_gidx[i] : base_index + i;
     int lo = 0, hi = nsp;  // first splitter greater than (string, g)
     while (lo < hi) {
         const int mid = (lo + hi) >> 1;
@@ -1754,15 +1755,15 @@ int s5g_classify(const uint64_t* keys, int64_t n, const uint64_t* tree, const ui
 }
 
 int s5g_partition(const uint8_t* arena, int64_t arena_len, const int64_t* handles, int64_t n,
-                  int64_t base_index, const uint8_t* splitters, const int64_t* splitter_off,
-                  const int64_t* splitter_gidx, int32_t nsplitters, int32_t* out_rank,
-                  void* stream) {
+                  int64_t base_index, const int64_t* string_gidx, const uint8_t* splitters,
+                  const int64_t* splitter_off, const int64_t* splitter_gidx, int32_t nsplitters,
+                  int32_t* out_rank, void* stream) {
     if (n <= 0) return n < 0 ? fail(S5G_E_INVALID, "negative n") : 0;
     if (nsplitters < 0) return fail(S5G_E_INVALID, "negative splitter count");
     cudaStream_t st = (cudaStream_t)stream;
     g_launches++;
     k_partition<<<blocks_for(n, 256), 256, 0, st>>>(arena, arena_len, handles, n, base_index,
-                                                    splitters, splitter_off, splitter_gidx,
+                                                    string_gidx, splitters, splitter_off, splitter_gidx,
                                                     nsplitters, out_rank);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(st));

@@ -162,8 +162,10 @@ def sort_host(buffer, handles, depth: int = 0, want_lcps: bool = True, want_dcha
     return oh, ol, od
 
 
-def partition(ds: DeviceStrings, base_index: int, splitters: list[bytes], splitter_gidx) -> torch.Tensor:
-    """Destination rank of every string (s5g_partition); splitters sorted."""
+def partition(ds: DeviceStrings, base_index: int, splitters: list[bytes], splitter_gidx,
+              string_gidx: torch.Tensor | None = None) -> torch.Tensor:
+    """Destination rank of every string (s5g_partition); splitters sorted.
+    A string's global index is string_gidx[i], else base_index + i."""
     dev = ds.handles.device
     blob = b"".join(splitters)
     off = np.zeros(len(splitters) + 1, dtype=np.int64)
@@ -175,7 +177,9 @@ def partition(ds: DeviceStrings, base_index: int, splitters: list[bytes], splitt
     gidx_d = torch.as_tensor(np.asarray(splitter_gidx, dtype=np.int64), device=dev)
     out = torch.empty(ds.n, dtype=torch.int32, device=dev)
     check(lib().s5g_partition(ds.arena.data_ptr(), ds.arena_len, ds.handles.data_ptr(), ds.n,
-                              int(base_index), blob_d.data_ptr(), off_d.data_ptr(),
+                              int(base_index),
+                              string_gidx.data_ptr() if string_gidx is not None else None,
+                              blob_d.data_ptr(), off_d.data_ptr(),
                               gidx_d.data_ptr() if len(splitters) else None, len(splitters),
                               out.data_ptr(), torch.cuda.current_stream(dev).cuda_stream))
     return out

@@ -23,6 +23,11 @@ prefix sum -> scatter) lifted to G ranks:
 
 The concatenation of the ranks' outputs is the reference's output.
 
+``distributed_merge_sort`` is the other strategy (SURVEY 8f row 1,
+partitioned_merge_sort): sort first, then cut the sorted runs at sampled
+splitters, exchange the sorted pieces with their LCPs and distinguishing
+characters, and K-way LCP merge them on every rank.
+
 Compute is pluggable (``backend``): ``GpuBackend`` runs every step in the
 sm_100a library; tests substitute a CPU backend to run the collective logic
 on ``gloo`` without a GPU.
@@ -140,16 +145,84 @@ def distributed_sort(shard: Shard, backend, group=None, samples_per_rank: int = 
     sorted_g = gidx[perm]
     # 5. LCP at the rank boundary
     if want_lcps:
-        first = backend.string_bytes(arena, sorted_h[:1]) if len(sorted_h) else None
-        last = backend.string_bytes(arena, sorted_h[-1:]) if len(sorted_h) else None
-        ends: list = [None] * G
-        dist.all_gather_object(ends, last, group=group)
-        prev = next((ends[q] for q in range(r - 1, -1, -1) if ends[q] is not None), None)
-        if len(sorted_h):
-            lcps[0] = LCP_UNDEF if prev is None else _lcp_bytes(prev, first)
+        _boundary_lcp(backend, arena, sorted_h, lcps, G, r, group)
     total = torch.tensor([n_local], dtype=torch.int64, device=backend.comm_device)
     dist.all_reduce(total, group=group)
     return DistResult(sorted_g, lcps, arena, sorted_h, int(total.item()))
+
+
+def _exchange_counts(counts: list[int], device, group) -> list[int]:
+    cnt = torch.tensor(counts, dtype=torch.int64, device=device)
+    rcnt = torch.empty_like(cnt)
+    if dist.get_backend(group) == "nccl":
+        dist.all_to_all_single(rcnt, cnt, group=group)
+    else:
+        _gather_counts(cnt, rcnt, group)
+    return [int(x) for x in rcnt.tolist()]
+
+
+def _boundary_lcp(backend, arena, sorted_h, lcps, G, r, group):
+    """lcps[0] of this rank against the last string of the previous
+    non-empty rank (rank 0 keeps -1): _boundary_lcps, parallel.py:447-455."""
+    first = backend.string_bytes(arena, sorted_h[:1]) if len(sorted_h) else None
+    last = backend.string_bytes(arena, sorted_h[-1:]) if len(sorted_h) else None
+    ends: list = [None] * G
+    dist.all_gather_object(ends, last, group=group)
+    prev = next((ends[q] for q in range(r - 1, -1, -1) if ends[q] is not None), None)
+    if len(sorted_h):
+        lcps[0] = LCP_UNDEF if prev is None else _lcp_bytes(prev, first)
+
+
+def distributed_merge_sort(shard: Shard, backend, group=None, samples_per_rank: int = 1024,
+                           max_splitter_len: int = 64, use_cache: bool = True,
+                           **sort_kw) -> DistResult:
+    """partitioned_merge_sort (parallel.py:885-994) across G ranks: every rank
+    sorts its shard (S^5 with LCPs and distinguishing characters), the sorted
+    runs are cut at G-1 regularly sampled string splitters (ties by global
+    index), each rank receives one sorted piece from every rank -- strings,
+    global indices, LCPs, characters -- and K-way LCP merges them
+    (s5g_kway_merge, cached comparisons when use_cache; pieces arrive in rank
+    order = input order, so merge ties keep the stable order).  Same result
+    as distributed_sort; the exchange moves the sorted runs instead of the
+    raw shard."""
+    G = dist.get_world_size(group)
+    r = dist.get_rank(group)
+    local = backend.prepare(shard)
+    n_local = len(shard.handles)
+    hnd = backend.handles_of(local, shard)
+    perm, lcps = backend.local_sort(local, hnd, True, **sort_kw)
+    sorted_h = hnd[perm]
+    gidx = perm.to(torch.int64) + shard.base_index
+    # 1. regular samples of the sorted run -> identical splitters everywhere
+    mine = backend.sample_run(local, sorted_h, gidx, samples_per_rank, max_splitter_len)
+    gathered: list = [None] * G
+    dist.all_gather_object(gathered, mine, group=group)
+    sp, sp_g = pick_splitters([x for part in gathered for x in part], G)
+    # 2. cut the sorted run (destinations are non-decreasing along it)
+    dest = backend.partition(local, shard, sp, sp_g, handles=sorted_h, gidx=gidx)
+    counts = torch.bincount(dest.long(), minlength=G).tolist() if n_local else [0] * G
+    recv_counts = _exchange_counts(counts, backend.comm_device, group)
+    # 3. exchange the sorted pieces
+    gidx_r = _alltoallv(gidx.to(backend.comm_device), counts, recv_counts, group)
+    lcp_r = _alltoallv(lcps.to(backend.comm_device), counts, recv_counts, group)
+    dchar_r = None
+    if use_cache:
+        dchar = backend.fill_dchar(local, sorted_h, lcps)
+        dchar_r = _alltoallv(dchar.to(backend.comm_device), counts, recv_counts, group)
+    payload, byte_counts = backend.pack(local, perm, counts)
+    rbyte_counts = _exchange_counts(byte_counts, backend.comm_device, group)
+    rbytes = _alltoallv(payload, byte_counts, rbyte_counts, group)
+    arena, starts = backend.unpack(rbytes)
+    # 4. K-way LCP merge of the G received runs
+    run_off = np.r_[0, np.cumsum(recv_counts)].astype(np.int64)
+    mh, ml = backend.kway_merge(arena, run_off, starts, lcp_r, dchar_r)
+    pos = handle_positions(starts, mh)
+    out_g = gidx_r[pos]
+    # 5. LCP at the rank boundary
+    _boundary_lcp(backend, arena, mh, ml, G, r, group)
+    total = torch.tensor([n_local], dtype=torch.int64, device=backend.comm_device)
+    dist.all_reduce(total, group=group)
+    return DistResult(out_g, ml, arena, mh, int(total.item()))
 
 
 def handle_positions(handles: torch.Tensor, out_h: torch.Tensor) -> torch.Tensor:
@@ -203,10 +276,42 @@ class GpuBackend:
             out.append((row[: z[0] if len(z) else maxlen].tobytes(), int(shard.base_index + p)))
         return out
 
-    def partition(self, ds, shard: Shard, sp, sp_g):
+    def partition(self, ds, shard: Shard, sp, sp_g, handles=None, gidx=None):
         from . import device as D
 
-        return D.partition(ds, shard.base_index, sp, sp_g)
+        if handles is not None:
+            ds = D.DeviceStrings(ds.arena, ds.arena_len, handles)
+        return D.partition(ds, shard.base_index, sp, sp_g, gidx)
+
+    def handles_of(self, ds, shard: Shard):
+        return ds.handles
+
+    def sample_run(self, ds, handles, gidx, k: int, maxlen: int):
+        """Equally spaced strings of a sorted run (prefixes <= maxlen) with
+        their global indices."""
+        n = handles.numel()
+        if n == 0:
+            return []
+        pos = torch.as_tensor(np.unique(np.linspace(0, n - 1, num=min(k, n)).astype(np.int64)),
+                              device=handles.device)
+        h = handles[pos]
+        idx = (h[:, None] + torch.arange(maxlen, device=h.device)[None, :]).clamp_(max=ds.arena.numel() - 1)
+        chunk = ds.arena[idx].cpu().numpy()
+        out = []
+        for row, g in zip(chunk, gidx[pos].cpu().numpy()):
+            z = np.flatnonzero(row == 0)
+            out.append((row[: z[0] if len(z) else maxlen].tobytes(), int(g)))
+        return out
+
+    def fill_dchar(self, ds, sorted_h, lcps):
+        from . import device as D
+
+        return D.fill_dchar(ds, sorted_h, lcps)
+
+    def kway_merge(self, ds, run_off, handles, lcps, dchar):
+        from . import device as D
+
+        return D.kway_merge(ds, run_off, handles, lcps, dchar, 0)
 
     def group_by_dest(self, dest: torch.Tensor, G: int):
         order = torch.sort(dest, stable=True).indices

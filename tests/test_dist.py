@@ -15,7 +15,13 @@ import torch.multiprocessing as mp
 
 import oracle
 from paper_1403_2056_b200 import corpora
-from paper_1403_2056_b200.dist import Shard, distributed_sort, handle_positions, pick_splitters
+from paper_1403_2056_b200.dist import (
+    Shard,
+    distributed_merge_sort,
+    distributed_sort,
+    handle_positions,
+    pick_splitters,
+)
 
 
 class CpuBackend:
@@ -40,12 +46,31 @@ class CpuBackend:
         return [(self._str(buf, int(shard.handles[p]), maxlen), int(shard.base_index + p))
                 for p in pos]
 
-    def partition(self, buf, shard, sp, sp_g):
+    def partition(self, buf, shard, sp, sp_g, handles=None, gidx=None):
         import bisect
         keys = list(zip(sp, sp_g))
-        out = [bisect.bisect_right(keys, (self._str(buf, int(h)), shard.base_index + i))
-               for i, h in enumerate(shard.handles)]
+        hs = shard.handles if handles is None else np.asarray(handles)
+        gs = (shard.base_index + np.arange(len(hs))) if gidx is None else np.asarray(gidx)
+        out = [bisect.bisect_right(keys, (self._str(buf, int(h)), int(g))) for h, g in zip(hs, gs)]
         return torch.tensor(out, dtype=torch.int32)
+
+    def handles_of(self, buf, shard):
+        return torch.from_numpy(np.asarray(shard.handles, dtype=np.int64))
+
+    def sample_run(self, buf, handles, gidx, k, maxlen):
+        n = len(handles)
+        if n == 0:
+            return []
+        pos = np.unique(np.linspace(0, n - 1, num=min(k, n)).astype(np.int64))
+        return [(self._str(buf, int(handles[p]), maxlen), int(gidx[p])) for p in pos]
+
+    def fill_dchar(self, buf, sorted_h, lcps):
+        return torch.from_numpy(oracle.fill_dchar(buf, sorted_h.numpy(), lcps.numpy()))
+
+    def kway_merge(self, buf, run_off, handles, lcps, dchar):
+        h, l, _ = oracle.kway_merge(buf, run_off, handles.numpy(), lcps.numpy(),
+                                    dchar.numpy() if dchar is not None else None)
+        return torch.from_numpy(h), torch.from_numpy(l)
 
     def group_by_dest(self, dest, G):
         order = torch.sort(dest, stable=True).indices
@@ -96,7 +121,7 @@ def _worker(rank, world, port, case, q):
         buf, hnd, mode, cuts = case
         be = CpuBackend()
         lo, hi = cuts[rank], cuts[rank + 1]
-        if mode == "packed":
+        if mode in ("packed", "merge"):
             # each rank owns a self-contained buffer with its strings
             strs = [buf[h:buf.index(b"\0", h) + 1] for h in hnd[lo:hi]]
             sbuf = np.frombuffer(b"".join(strs), dtype=np.uint8).copy() if strs else np.zeros(0, np.uint8)
@@ -105,8 +130,12 @@ def _worker(rank, world, port, case, q):
             sbuf = np.frombuffer(buf, dtype=np.uint8).copy()
             shnd = np.asarray(hnd[lo:hi], dtype=np.int64)
         be._handles = shnd
-        res = distributed_sort(Shard(sbuf, shnd, lo), be, samples_per_rank=16,
-                               max_splitter_len=6, mode=mode)
+        if mode == "merge":
+            res = distributed_merge_sort(Shard(sbuf, shnd, lo), be, samples_per_rank=16,
+                                         max_splitter_len=6)
+        else:
+            res = distributed_sort(Shard(sbuf, shnd, lo), be, samples_per_rank=16,
+                                   max_splitter_len=6, mode=mode)
         parts = [None] * world
         dist.all_gather_object(parts, (res.gidx.numpy(), res.lcps.numpy(), res.n_total))
         if rank == 0:
@@ -174,3 +203,23 @@ def test_empty_rank_and_shared_prefixes():
 def test_replicated_suffixes():
     buf, hnd = corpora.gen_suffix_markov(2000, chains=4)
     _run(2, buf.tobytes(), hnd, mode="replicated")
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_merge_strategy_random(world):
+    buf, hnd = corpora.gen_random(3000, 11)
+    _run(world, buf.tobytes(), hnd, mode="merge")
+
+
+def test_merge_strategy_duplicates_and_empty_rank():
+    rng = np.random.default_rng(5)
+    items = [bytes(rng.integers(97, 99, size=int(rng.integers(0, 4)), dtype=np.uint8)) for _ in range(1200)]
+    buf, hnd = _pack(items)
+    _run(2, buf, hnd, mode="merge")
+    _run(3, buf, hnd, mode="merge", cuts=[0, 600, 600, 1200])
+
+
+def test_merge_strategy_shared_prefixes():
+    items = [b"http://same.host/" + bytes([97 + (i % 7)]) * (i % 5) for i in range(600)]
+    buf, hnd = _pack(items)
+    _run(3, buf, hnd, mode="merge")

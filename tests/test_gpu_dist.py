@@ -15,8 +15,8 @@ torch = pytest.importorskip("torch")
 
 from paper_1403_2056_b200 import corpora  # noqa: E402
 from paper_1403_2056_b200 import device as D  # noqa: E402
-from paper_1403_2056_b200.dist import (GpuBackend, Shard, distributed_sort,  # noqa: E402
-                                       handle_positions, pick_splitters)
+from paper_1403_2056_b200.dist import (GpuBackend, Shard, distributed_merge_sort,  # noqa: E402
+                                       distributed_sort, handle_positions, pick_splitters)
 from test_dist import CpuBackend  # noqa: E402
 
 
@@ -50,10 +50,33 @@ def test_distributed_sort_world1_nccl():
     try:
         for cfg in ("c1_random", "c3_urls"):
             buf, hnd = corpora.CONFIGS[cfg](1 / 64)
-            res = distributed_sort(Shard(buf, hnd, 0), GpuBackend(), samples_per_rank=64)
             h, l, _ = oracle.parallel_s5(buf, hnd)
             want = handle_positions(torch.from_numpy(hnd), torch.from_numpy(h)).numpy()
-            assert np.array_equal(res.gidx.cpu().numpy(), want)
-            assert np.array_equal(res.lcps.cpu().numpy(), l)
+            for strategy in (distributed_sort, distributed_merge_sort):
+                res = strategy(Shard(buf, hnd, 0), GpuBackend(), samples_per_rank=64)
+                assert np.array_equal(res.gidx.cpu().numpy(), want), strategy.__name__
+                assert np.array_equal(res.lcps.cpu().numpy(), l), strategy.__name__
     finally:
         dist.destroy_process_group()
+
+
+def test_merge_strategy_pieces_match_cpu_backend():
+    """sample_run / partition on a sorted run / fill_dchar / kway_merge of the
+    GPU backend equal the CPU test backend's."""
+    buf, hnd = corpora.gen_dna(20_000, 30, 5)
+    shard = Shard(buf, hnd, 123)
+    cpu, gpu = CpuBackend(), GpuBackend()
+    cpu._handles = hnd
+    ds = gpu.prepare(shard)
+    perm, lcps = gpu.local_sort(ds, ds.handles, True)
+    sh = ds.handles[perm]
+    gidx = perm + 123
+    s_gpu = gpu.sample_run(ds, sh, gidx, 50, 10)
+    s_cpu = cpu.sample_run(buf, sh.cpu().numpy(), gidx.cpu().numpy(), 50, 10)
+    assert s_gpu == s_cpu
+    sp, g = pick_splitters(s_gpu * 3, 4)
+    d_gpu = gpu.partition(ds, shard, sp, g, handles=sh, gidx=gidx).cpu().numpy()
+    d_cpu = cpu.partition(buf, shard, sp, g, handles=sh.cpu().numpy(), gidx=gidx.cpu().numpy()).numpy()
+    assert np.array_equal(d_gpu, d_cpu) and np.all(np.diff(d_gpu) >= 0)
+    dc = gpu.fill_dchar(ds, sh, lcps).cpu().numpy()
+    assert np.array_equal(dc, cpu.fill_dchar(buf, sh.cpu(), lcps.cpu()).numpy())
