@@ -207,7 +207,7 @@ def run_dist(args):
     from paper_1403_2056_b200 import _lib
     from paper_1403_2056_b200 import corpora
     from paper_1403_2056_b200 import device as DV
-    from paper_1403_2056_b200.dist import GpuBackend, Shard, distributed_sort
+    from paper_1403_2056_b200.dist import GpuBackend, Shard, distributed_merge_sort, distributed_sort
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
@@ -225,6 +225,8 @@ def run_dist(args):
     be = GpuBackend(dev)
 
     def step():
+        if args.strategy == "merge":  # partitioned_merge_sort across ranks
+            return distributed_merge_sort(shard, be)
         return distributed_sort(shard, be, want_lcps=True)
 
     for _ in range(args.warmup):
@@ -254,7 +256,10 @@ def run_dist(args):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
         "data": "synthetic",
         "config": {"workload": args.config, "n_per_rank": n, "n_total": total,
-                   "parallelism": f"dp{world} (sample-sort partition + NCCL all-to-all)",
+                   "parallelism": f"dp{world} (" + ("local S^5 + sampled cuts + NCCL all-to-all of "
+                                                     "sorted pieces + K-way LCP merge"
+                                                     if args.strategy == "merge" else
+                                                     "sample-sort partition + NCCL all-to-all") + ")",
                    "l2": "inputs larger than L2 (arena > 126 MB), no flush"},
         "roofline": {"bound": "hbm", "kernel": "whole multi-GPU sort", "achieved": None,
                      "peak": peak, "unit": "GB/s", "frac": None, "traffic": None,
@@ -407,6 +412,8 @@ def main(argv=None):
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--l2-fetch", type=int, default=32)
+    ap.add_argument("--strategy", choices=["sample", "merge"], default="sample",
+                    help="N > 1: sample-sort exchange (default) or local sort + LCP merge")
     args = ap.parse_args(argv)
     if args.impl == "reference":
         return run_reference(args)
