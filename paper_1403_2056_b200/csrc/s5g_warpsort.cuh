@@ -237,6 +237,83 @@ __device__ __forceinline__ uint64_t warp_and64(uint64_t x) {
     return x;
 }
 
+// LCP of the strings at a and b, known equal before depth d, capped at cap:
+// the warp compares 32 words (256 characters) per step.
+__device__ __forceinline__ int64_t warp_lcp_from(const uint8_t* __restrict__ arena, int64_t alen,
+                                                 int64_t a, int64_t b, int64_t d, int64_t cap,
+                                                 unsigned& fetches, int lane) {
+    for (; d < cap; d += 32 * WORD) {
+        const uint64_t wa = load_key(arena, alen, a, d + WORD * lane);
+        const uint64_t wb = load_key(arena, alen, b, d + WORD * lane);
+        fetches += 2;
+        const int tp = term_pos(wa);
+        const bool stop = wa != wb || tp < WORD;
+        const uint32_t m = __ballot_sync(0xffffffffu, stop);
+        if (m) {
+            const int f = __ffs(m) - 1;
+            const int64_t l = d + WORD * lane + (wa != wb ? (__clzll(wa ^ wb) >> 3) : tp);
+            return min(cap, __shfl_sync(0xffffffffu, l, f));
+        }
+    }
+    return cap;
+}
+
+// The kept slots form ONE run (group): all its strings share `depth`
+// characters; return their common prefix length (>= depth) so the next
+// round starts where they first differ (suffixes of texts with long copied
+// blocks otherwise advance one word per round).  lcp(s0, s1) is found by the
+// whole warp (256 characters per step); the other members, one per lane,
+// are checked against s0 only up to that bound.  Runs of more than 32
+// strings keep the word-per-round path.
+template <int IT>
+__device__ __forceinline__ int64_t run_common_prefix(const uint32_t (&meta)[IT],
+                                                     const int64_t* __restrict__ hbt, int64_t depth,
+                                                     const uint8_t* __restrict__ arena,
+                                                     int64_t alen, unsigned& fetches,
+                                                     uint64_t* __restrict__ xs, int lane) {
+    uint32_t mine = 0;
+#pragma unroll
+    for (int e = 0; e < IT; e++) mine += meta[e] >> 22 & 1;
+    uint32_t incl = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    const uint32_t r = __shfl_sync(0xffffffffu, incl, 31);
+    if (r < 2 || r > 32) return depth;
+    uint32_t k = incl - mine;  // member rank of my first active slot (slot order)
+#pragma unroll
+    for (int e = 0; e < IT; e++)
+        if (meta[e] >> 22 & 1) xs[k++] = (uint64_t)hbt[meta[e] & 0x7ff];
+    __syncwarp();
+    const int64_t h0 = (int64_t)xs[0], h1 = (int64_t)xs[1];
+    const int64_t hm = lane < (int)r ? (int64_t)xs[lane] : 0;
+    __syncwarp();
+    int64_t c = warp_lcp_from(arena, alen, h0, h1, depth, INT64_MAX, fetches, lane);
+    if (c > depth && r > 2) {
+        int64_t my = c;
+        if (lane >= 2 && lane < (int)r) {
+            for (int64_t d = depth; d < my; d += WORD) {
+                const uint64_t wa = load_key(arena, alen, h0, d), wb = load_key(arena, alen, hm, d);
+                fetches += 2;
+                if (wa != wb) {
+                    my = min(my, d + (__clzll(wa ^ wb) >> 3));
+                    break;
+                }
+                if (term_pos(wa) < WORD) {
+                    my = min(my, d + term_pos(wa));
+                    break;
+                }
+            }
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) my = min(my, __shfl_xor_sync(0xffffffffu, my, o));
+        c = my;
+    }
+    return c;
+}
+
 // One warp finishes one run of gn <= 32*IT strings that occupy slots
 // g0 .. g0+gn-1 of the segment and share `depth` characters.  On entry the
 // words at `depth` are in key[] (slot order = ord[g0 + i]) when have_keys,
@@ -258,6 +335,7 @@ __device__ void warp_finish(const int64_t* __restrict__ hbt, uint16_t* __restric
     }
     rekey<IT, false>(key, meta, segrec, hbt, cd, cnv, depth, arena, alen, fetches, xs + g0,
                      lane * IT, gn, lane, 32);
+    int wrounds = 0;
     for (;;) {
         // ---- sort the active slots by (group, word, tag) ------------------
         uint64_t o = 0, a = ~0ull;
@@ -350,13 +428,20 @@ __device__ void warp_finish(const int64_t* __restrict__ hbt, uint16_t* __restric
         uint32_t cur = __shfl_up_sync(0xffffffffu, incl, 1);
         if (lane == 0) cur = 0;
         depth += WORD;
+        uint32_t nstarts = 0;
 #pragma unroll
         for (int e = 0; e < IT; e++) {
             const int i = lane * IT + e;
-            if (keep[e] && brk[e]) cur = i + 1;
+            if (keep[e] && brk[e]) {
+                cur = i + 1;
+                nstarts++;
+            }
             const uint32_t tag = meta[e] & 0x7ff;
             meta[e] = keep[e] ? ((1u << 22) | ((cur - 1) << 11) | tag) : (((uint32_t)i << 11) | tag);
         }
+        // a single run still tied after three words: jump to its common prefix
+        if (++wrounds >= 3 && __reduce_add_sync(0xffffffffu, nstarts) == 1)
+            depth = run_common_prefix<IT>(meta, hbt, depth, arena, alen, fetches, xs + g0, lane);
         rekey<IT, false>(key, meta, segrec, hbt, cd, cnv, depth, arena, alen, fetches, xs + g0,
                      lane * IT, gn, lane, 32);
     }
