@@ -355,27 +355,29 @@ __global__ void __launch_bounds__(1024) k_scan_buckets(
 // terminator-covering equality buckets are final: their handles go straight
 // to the output and the equality bucket's interior LCPs are written
 // (ssss.py:345-357).
+constexpr int SCX_IT = 2, SCX_SUB = SC_NT * SCX_IT;  // k_scatter sub-tile: 1024 strings
+
 __global__ void __launch_bounds__(SC_NT, 2) k_scatter(
     const StepDev* __restrict__ steps, const int32_t* __restrict__ tile_step,
     const Rec* __restrict__ recX, const uint16_t* __restrict__ bid,
     const uint32_t* __restrict__ cnt, const uint32_t* __restrict__ tot,
     const uint32_t* __restrict__ bstart, const uint8_t* __restrict__ tpos_g,
     Rec* __restrict__ recY, int64_t* __restrict__ out_h, int64_t* __restrict__ lcps) {
-    // Per 2048-string sub-tile: (1) every thread issues coalesced loads of
-    // its 4 records and bucket ids; (2) two stable 7-bit ranking passes in
-    // shared memory order the sub-tile by bucket (the record loads are in
-    // flight meanwhile); (3) run starts give each sorted slot its offset in
-    // its bucket; (4) each thread writes its own records to their ranked
-    // destinations (whole 32-byte sectors).
+    // Per 1024-string sub-tile: (1) the records and bucket ids of the NEXT
+    // sub-tile are loaded (coalesced, 2 per thread, double-buffered in
+    // registers) while (2) two stable 7-bit ranking passes in shared memory
+    // order this sub-tile by bucket; (3) run starts give each sorted slot its
+    // offset in its bucket; (4) each thread writes its own records to their
+    // ranked destinations (whole 32-byte sectors).
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ uint32_t wsum[32];
     uint32_t* run_off = reinterpret_cast<uint32_t*>(smem);                 // NBMAX+1
-    uint32_t* dst_by_e = run_off + (NBMAX + 1);                            // SC_SUB
-    uint16_t* rcnt = reinterpret_cast<uint16_t*>(dst_by_e + SC_SUB);       // SC_R*32
-    uint16_t* kA = rcnt + SC_R * 32;
-    uint16_t* vA = kA + SC_SUB;
-    uint16_t* kB = vA + SC_SUB;
-    uint16_t* vB = kB + SC_SUB;
+    uint32_t* dst_by_e = run_off + (NBMAX + 1);                            // SCX_SUB
+    uint16_t* rcnt = reinterpret_cast<uint16_t*>(dst_by_e + SCX_SUB);      // SC_R*NW
+    uint16_t* kA = rcnt + SC_R * (SC_NT / 32);
+    uint16_t* vA = kA + SCX_SUB;
+    uint16_t* kB = vA + SCX_SUB;
+    uint16_t* vB = kB + SCX_SUB;
     const int t = blockIdx.x;
     const StepDev sd = steps[tile_step[t]];
     const int ti = t - (int)sd.tile0;
@@ -385,41 +387,58 @@ __global__ void __launch_bounds__(SC_NT, 2) k_scatter(
     const uint32_t* row = cnt + sd.cnt_off + (int64_t)ti * nb;
     const uint8_t* tp = tpos_g + sd.tree_off;
     for (int b = threadIdx.x; b < nb; b += SC_NT) run_off[b] = bstart[sd.bk_off + b] + row[b];
-    __syncthreads();
-    for (int64_t sub = beg; sub < end; sub += SC_SUB) {
-        const int m = (int)min((int64_t)SC_SUB, end - sub);
-        Rec rec[SC_ITEMS];
-        uint32_t myb[SC_ITEMS];
+    Rec nrec[SCX_IT];
+    uint32_t nbid[SCX_IT];
 #pragma unroll
-        for (int i = 0; i < SC_ITEMS; i++) {
+    for (int i = 0; i < SCX_IT; i++) {
+        const int64_t e = beg + threadIdx.x + i * SC_NT;
+        nbid[i] = BID_SENTINEL;
+        if (e < end) {
+            nbid[i] = bid[e];
+            nrec[i] = recX[e];
+        }
+    }
+    __syncthreads();
+    for (int64_t sub = beg; sub < end; sub += SCX_SUB) {
+        const int m = (int)min((int64_t)SCX_SUB, end - sub);
+        Rec rec[SCX_IT];
+        uint32_t myb[SCX_IT];
+#pragma unroll
+        for (int i = 0; i < SCX_IT; i++) {
             const int e = threadIdx.x + i * SC_NT;
-            myb[i] = BID_SENTINEL;
-            if (e < m) {
-                myb[i] = bid[sub + e];
-                rec[i] = recX[sub + e];
-            }
+            myb[i] = nbid[i];
+            rec[i] = nrec[i];
             kA[e] = (uint16_t)myb[i];
             vA[e] = (uint16_t)e;
+        }
+#pragma unroll
+        for (int i = 0; i < SCX_IT; i++) {  // next sub-tile, in flight during the ranking
+            const int64_t e = sub + SCX_SUB + threadIdx.x + i * SC_NT;
+            nbid[i] = BID_SENTINEL;
+            if (e < end) {
+                nbid[i] = bid[e];
+                nrec[i] = recX[e];
+            }
         }
         __syncthreads();
         if (nb <= SC_R - 1) {
             // few buckets (steps on small segments): one 7-bit pass suffices
             // (the sentinel 0x3FFF has low digit 127 > any bucket id)
-            rank_pass(kA, vA, kB, vB, 0, rcnt, wsum);
-            for (int e = threadIdx.x; e < SC_SUB; e += SC_NT) {
+            rank_pass<SCX_IT>(kA, vA, kB, vB, 0, rcnt, wsum);
+            for (int e = threadIdx.x; e < SCX_SUB; e += SC_NT) {
                 kA[e] = kB[e];
                 vA[e] = vB[e];
             }
             __syncthreads();
         } else {
-            rank_pass(kA, vA, kB, vB, 0, rcnt, wsum);
-            rank_pass(kB, vB, kA, vA, SC_RB, rcnt, wsum);
+            rank_pass<SCX_IT>(kA, vA, kB, vB, 0, rcnt, wsum);
+            rank_pass<SCX_IT>(kB, vB, kA, vA, SC_RB, rcnt, wsum);
         }
-        // run starts in the sorted sub-tile: thread owns q = 4t .. 4t+3
-        const int q0 = threadIdx.x * SC_ITEMS;
-        uint32_t bq[SC_ITEMS], st[SC_ITEMS], mx = 0;
+        // run starts in the sorted sub-tile: thread owns q = 2t .. 2t+1
+        const int q0 = threadIdx.x * SCX_IT;
+        uint32_t bq[SCX_IT], st[SCX_IT], mx = 0;
 #pragma unroll
-        for (int i = 0; i < SC_ITEMS; i++) {
+        for (int i = 0; i < SCX_IT; i++) {
             const int q = q0 + i;
             bq[i] = kA[q];
             const bool start = q < m && (q == 0 || kA[q - 1] != bq[i]);
@@ -428,14 +447,14 @@ __global__ void __launch_bounds__(SC_NT, 2) k_scatter(
         }
         const uint32_t before = block_excl_max<SC_NT>(mx, wsum);
 #pragma unroll
-        for (int i = 0; i < SC_ITEMS; i++) {
+        for (int i = 0; i < SCX_IT; i++) {
             const int q = q0 + i;
             st[i] = (st[i] ? st[i] : before) - 1;
             if (q < m) dst_by_e[vA[q]] = run_off[bq[i]] + (q - st[i]);
         }
         __syncthreads();
 #pragma unroll
-        for (int i = 0; i < SC_ITEMS; i++) {
+        for (int i = 0; i < SCX_IT; i++) {
             const int e = threadIdx.x + i * SC_NT;
             if (e >= m) break;
             const uint32_t b = myb[i];
@@ -460,7 +479,7 @@ __global__ void __launch_bounds__(SC_NT, 2) k_scatter(
             }
         }
 #pragma unroll
-        for (int i = 0; i < SC_ITEMS; i++) {
+        for (int i = 0; i < SCX_IT; i++) {
             const int q = q0 + i;
             if (q < m && (q == m - 1 || kA[q + 1] != bq[i])) run_off[bq[i]] += q - st[i] + 1;
         }
@@ -1049,8 +1068,8 @@ static size_t carve(Workspace* w, uint8_t* base, int64_t n, int64_t t_medium) {
 static size_t smem_sample(int P, int v) { return (size_t)P * 8 + (size_t)3 * (v + 1) * 2 + 16; }
 static constexpr size_t SMEM_CLS_UNROLL = (size_t)(VMAX + 1) * 8 + (size_t)(NBMAX + 1) / 2 * 4;
 static constexpr size_t SMEM_CLS = SMEM_CLS_UNROLL + (size_t)(VMAX + 1) * 2;
-static constexpr size_t SMEM_SC = (size_t)(NBMAX + 1) * 4 + (size_t)SC_SUB * 4 +
-                                  (size_t)SC_R * 32 * 2 + (size_t)4 * SC_SUB * 2;
+static constexpr size_t SMEM_SC = (size_t)(NBMAX + 1) * 4 + (size_t)SCX_SUB * 4 +
+                                  (size_t)SC_R * (SC_NT / 32) * 2 + (size_t)4 * SCX_SUB * 2;
 
 static int set_smem_attrs() {
     // per device: kernel attributes + the byte-PEXT table of the finishers

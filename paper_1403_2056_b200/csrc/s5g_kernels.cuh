@@ -234,6 +234,7 @@ __device__ void bitonic_pairs(uint64_t* key, uint32_t* meta, int P) {
 // item j / lane l is element w*128 + j*32 + l, so (digit, warp, item, lane)
 // order is input order: stability comes from warp-minor digit offsets plus
 // match_any ranks inside each warp.
+template <int ITEMS = SC_ITEMS>
 __device__ void rank_pass(const uint16_t* kin, const uint16_t* vin, uint16_t* kout,
                           uint16_t* vout, int shift, uint16_t* cnt, uint32_t* wsum) {
     constexpr int NW = SC_NT / 32;
@@ -241,12 +242,12 @@ __device__ void rank_pass(const uint16_t* kin, const uint16_t* vin, uint16_t* ko
     uint32_t* cnt32 = reinterpret_cast<uint32_t*>(cnt);
     for (int i = threadIdx.x; i < SC_R * NW / 2; i += SC_NT) cnt32[i] = 0;
     __syncthreads();
-    uint16_t kk[SC_ITEMS], vv[SC_ITEMS];
-    uint32_t loc[SC_ITEMS], dg[SC_ITEMS];
+    uint16_t kk[ITEMS], vv[ITEMS];
+    uint32_t loc[ITEMS], dg[ITEMS];
     const uint32_t lt = lanemask_lt();
 #pragma unroll
-    for (int j = 0; j < SC_ITEMS; j++) {
-        int e = w * (32 * SC_ITEMS) + j * 32 + lane;
+    for (int j = 0; j < ITEMS; j++) {
+        int e = w * (32 * ITEMS) + j * 32 + lane;
         kk[j] = kin[e];
         vv[j] = vin[e];
         uint32_t d = (kk[j] >> shift) & (SC_R - 1);
@@ -271,7 +272,7 @@ __device__ void rank_pass(const uint16_t* kin, const uint16_t* vin, uint16_t* ko
     }
     __syncthreads();
 #pragma unroll
-    for (int j = 0; j < SC_ITEMS; j++) {
+    for (int j = 0; j < ITEMS; j++) {
         uint32_t pos = cnt[dg[j] * NW + w] + loc[j];
         kout[pos] = kk[j];
         vout[pos] = vv[j];
