@@ -19,7 +19,8 @@ rows = list(csv.reader(io.StringIO(raw)))
 h, units, data = rows[0], rows[1], rows[2:]
 col = {k: i for i, k in enumerate(h)}
 keep = ["Kernel Name", "Grid Size", "Block Size", "gpu__time_duration.sum",
-        "dram__bytes_read.sum", "dram__bytes_write.sum", "launch__registers_per_thread",
+        "dram__bytes_read.sum", "dram__bytes_write.sum", "smsp__inst_executed.sum",
+        "launch__registers_per_thread",
         "sm__warps_active.avg.pct_of_peak_sustained_active",
         "smsp__issue_active.avg.pct_of_peak_sustained_active",
         "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"]
@@ -42,12 +43,14 @@ kern = {}
 for r in data:
     name = re.sub(r"\(.*", "", r[col["Kernel Name"]]).replace("void ", "").replace("s5g::", "")
     name = re.sub(r"\(int\)|\(bool\)", "", name)
-    e = kern.setdefault(name, {"launches": 0, "dram_bytes": 0.0, "ms": 0.0})
+    e = kern.setdefault(name, {"launches": 0, "dram_bytes": 0.0, "ms": 0.0, "warp_inst": 0.0})
     e["launches"] += 1
     e["dram_bytes"] += val(r, "dram__bytes_read.sum") + val(r, "dram__bytes_write.sum")
     e["ms"] += val(r, "gpu__time_duration.sum")
+    e["warp_inst"] += val(r, "smsp__inst_executed.sum")
 for e in kern.values():
     e["dram_bytes_per_launch"] = e["dram_bytes"] / e["launches"]
+    e["warp_inst_per_launch"] = e["warp_inst"] / e["launches"]
 json.dump({"source": f"ncu --set full, one C2 sort (bench.py --steps 1 --warmup 0), {prefix}_ncu_kernels.csv",
            "kernels": kern}, open(prefix + "_traffic.json", "w"), indent=1)
 for k, e in sorted(kern.items(), key=lambda x: -x[1]["ms"]):
