@@ -39,7 +39,8 @@ def build_library(force: bool = False, verbose: bool = False) -> Path:
         return LIB_PATH
     LIB_DIR.mkdir(exist_ok=True)
     tmp = LIB_PATH.with_suffix(".so.tmp")
-    cmd = [nvcc(), *NVCC_FLAGS, "-o", str(tmp), *map(str, SOURCES)]
+    extra = os.environ.get("S5G_NVCC_EXTRA", "").split()  # tuning experiments only
+    cmd = [nvcc(), *NVCC_FLAGS, *extra, "-o", str(tmp), *map(str, SOURCES)]
     if verbose:
         print(" ".join(cmd))
     subprocess.run(cmd, check=True)

@@ -314,6 +314,129 @@ __device__ __forceinline__ int64_t run_common_prefix(const uint32_t (&meta)[IT],
     return c;
 }
 
+constexpr int SMALL_RUN = 8;  // runs finished by direct comparisons
+#ifndef FSR_ROUNDS
+#define FSR_ROUNDS 4             // ... once tied for this many warp rounds (tuned on C3 / C4)
+#endif
+
+// Order two strings sharing d characters: (a <= b, their LCP); a warp-wide
+// 256-character compare per step.
+__device__ __forceinline__ bool warp_le(const uint8_t* __restrict__ arena, int64_t alen,
+                                       int64_t a, int64_t b, int64_t d, int64_t* l,
+                                       unsigned& fetches, int lane) {
+    for (;; d += 32 * WORD) {
+        const uint64_t wa = load_key(arena, alen, a, d + WORD * lane);
+        const uint64_t wb = load_key(arena, alen, b, d + WORD * lane);
+        fetches += 2;
+        const int tp = term_pos(wa);
+        const bool stop = wa != wb || tp < WORD;
+        const uint32_t m = __ballot_sync(0xffffffffu, stop);
+        if (m) {
+            const int f = __ffs(m) - 1;
+            const int64_t lf = d + WORD * lane + (wa != wb ? (__clzll(wa ^ wb) >> 3) : tp);
+            const int le = wa <= wb;
+            *l = __shfl_sync(0xffffffffu, lf, f);
+            return __shfl_sync(0xffffffffu, le, f);
+        }
+    }
+}
+
+// After a round: every kept run (slots tied on all characters before
+// `depth`) of 2..SMALL_RUN strings is sorted by direct warp-wide string
+// comparisons (stable insertion sort: ties keep tag order), its interior LCPs
+// written, and its slots retired (keep = false).  Returns whether any run was
+// finished.  xs (slot-indexed, gn entries) is scratch.
+template <int IT>
+__device__ bool finish_small_runs(bool (&keep)[IT], const bool (&brk)[IT], uint32_t (&meta)[IT],
+                                  const int64_t* __restrict__ hbt, int64_t depth,
+                                  const uint8_t* __restrict__ arena, int64_t alen,
+                                  uint64_t* __restrict__ xs, int gn,
+                                  int64_t* __restrict__ lcp_run, unsigned& fetches, int lane) {
+    // run starts and ends among the kept slots, in slot order
+    bool small_any = false;
+    uint32_t starts[IT];
+#pragma unroll
+    for (int e = 0; e < IT; e++) starts[e] = __ballot_sync(0xffffffffu, keep[e] && brk[e]);
+    // stage (handle << 11 | tag) of every kept slot
+#pragma unroll
+    for (int e = 0; e < IT; e++)
+        if (keep[e]) xs[lane * IT + e] = ((uint64_t)hbt[meta[e] & 0x7ff] << 11) | (meta[e] & 0x7ff);
+    __syncwarp();
+    // walk the runs in slot order (run start slot s = lane' * IT + e')
+    uint32_t done_mask[IT];
+#pragma unroll
+    for (int e = 0; e < IT; e++) done_mask[e] = 0;
+    for (int L = 0; L < 32; L++) {
+#pragma unroll
+        for (int e = 0; e < IT; e++) {
+            if (!(starts[e] >> L & 1)) continue;
+            const int s = L * IT + e;
+            // run length: kept slots from s while no new start / not past keep
+            int z = 1;
+            while (s + z < gn && z <= SMALL_RUN) {
+                const int q = s + z, ql = q / IT, qe = q % IT;
+                bool kq = false, bq = false;
+#pragma unroll
+                for (int f = 0; f < IT; f++)
+                    if (f == qe) {
+                        kq = __shfl_sync(0xffffffffu, keep[f], ql);
+                        bq = __shfl_sync(0xffffffffu, brk[f], ql);
+                    }
+                if (!kq || bq) break;
+                z++;
+            }
+            if (z > SMALL_RUN || z < 2) continue;
+            small_any = true;
+            // stable insertion sort of xs[s .. s+z) by string content; an
+            // element that stays put keeps the LCP its one comparison found
+            int64_t lk[SMALL_RUN];
+            bool moved = false;
+            for (int k = 1; k < z; k++) {
+                const uint64_t x = xs[s + k];
+                int j = k - 1;
+                int64_t l = 0;
+                while (j >= 0 && !warp_le(arena, alen, (int64_t)(xs[s + j] >> 11), (int64_t)(x >> 11),
+                                          depth, &l, fetches, lane)) {
+                    __syncwarp();
+                    if (lane == 0) xs[s + j + 1] = xs[s + j];
+                    __syncwarp();
+                    j--;
+                }
+                moved |= j != k - 1;
+                lk[k] = l;
+                __syncwarp();
+                if (lane == 0) xs[s + j + 1] = x;
+                __syncwarp();
+            }
+            for (int k = 1; k < z; k++) {
+                int64_t l = lk[k];
+                if (moved)
+                    warp_le(arena, alen, (int64_t)(xs[s + k - 1] >> 11), (int64_t)(xs[s + k] >> 11),
+                            depth, &l, fetches, lane);
+                if (lane == 0 && lcp_run) lcp_run[s + k] = l;
+            }
+            // retire the run's slots (lane l' owns slots l'*IT .. l'*IT+IT-1)
+            for (int k = 0; k < z; k++) {
+                const int q = s + k;
+                if (lane == q / IT) {
+#pragma unroll
+                    for (int f = 0; f < IT; f++)
+                        if (f == q % IT) done_mask[f] = 1;
+                }
+            }
+        }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int e = 0; e < IT; e++)
+        if (done_mask[e]) {
+            const int i = lane * IT + e;
+            keep[e] = false;
+            meta[e] = ((uint32_t)i << 11) | (uint32_t)(xs[i] & 0x7ff);  // finished, new tag
+        }
+    return __any_sync(0xffffffffu, small_any);
+}
+
 // One warp finishes one run of gn <= 32*IT strings that occupy slots
 // g0 .. g0+gn-1 of the segment and share `depth` characters.  On entry the
 // words at `depth` are in key[] (slot order = ord[g0 + i]) when have_keys,
@@ -416,9 +539,21 @@ __device__ void warp_finish(const int64_t* __restrict__ hbt, uint16_t* __restric
             }
             keep[e] = act && term_pos(key[e]) == WORD && (!brk[e] || (na && !nb));
             any |= keep[e];
-            if (keep[e] && brk[e]) run = i + 1;
         }
         if (!__any_sync(0xffffffffu, any) || depth > alen) break;  // alen: corrupt-input guard
+        // runs still tied after FSR_ROUNDS + 1 words: finish the small ones directly
+        // (pairs of suffixes inside copied blocks share kilobytes)
+        if (wrounds >= FSR_ROUNDS && finish_small_runs<IT>(keep, brk, meta, hbt, depth + WORD, arena, alen,
+                                                  xs + g0, gn, lcp_seg ? lcp_seg + g0 : nullptr,
+                                                  fetches, lane)) {
+            any = false;
+#pragma unroll
+            for (int e = 0; e < IT; e++) any |= keep[e];
+            if (!__any_sync(0xffffffffu, any)) break;
+        }
+#pragma unroll
+        for (int e = 0; e < IT; e++)
+            if (keep[e] && brk[e]) run = lane * IT + e + 1;
         uint32_t incl = run;
 #pragma unroll
         for (int o2 = 1; o2 < 32; o2 <<= 1) {
