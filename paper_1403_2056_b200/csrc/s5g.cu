@@ -1208,8 +1208,8 @@ static int sort_impl_body(const s5g_sort_args* a) {
     // there concurrently with the next round's device-wide step
     // and a high-priority stream for the root step's sample, drawn from the
     // input while k_init copies it (its one CTA is scheduled first)
-    static cudaStream_t s_st2[64], s_hi[64];
-    static cudaEvent_t s_fork[64], s_join[64], s_samp[64];
+    static cudaStream_t s_st2[64], s_hi[64], s_pool[64][3];
+    static cudaEvent_t s_fork[64], s_join[64], s_samp[64], s_pfork[64], s_pjoin[64][3];
     int dev_id = 0;
     CK(cudaGetDevice(&dev_id));
     if (dev_id >= 64) return fail(S5G_E_INVALID, "device id >= 64");
@@ -1221,15 +1221,31 @@ static int sort_impl_body(const s5g_sort_args* a) {
         CK(cudaEventCreateWithFlags(&s_fork[dev_id], cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&s_join[dev_id], cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&s_samp[dev_id], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&s_pfork[dev_id], cudaEventDisableTiming));
+        for (int q = 0; q < 3; q++) {
+            CK(cudaStreamCreateWithFlags(&s_pool[dev_id][q], cudaStreamNonBlocking));
+            CK(cudaEventCreateWithFlags(&s_pjoin[dev_id][q], cudaEventDisableTiming));
+        }
     }
     cudaStream_t st2 = s_st2[dev_id], st_hi = s_hi[dev_id];
     cudaEvent_t ev_fork = s_fork[dev_id], ev_join = s_join[dev_id], ev_samp = s_samp[dev_id];
     Profiler prof2(st2, 1), prof_hi(st_hi, 2);
+    // finisher size classes run side by side (their launch tails overlap):
+    // warp classes on pool 0, k_cta_sort<2> / <4> on pools 1 / 2, <8> on the
+    // caller's finisher stream
+    Profiler prof_pool[3] = {Profiler(s_pool[dev_id][0], 3), Profiler(s_pool[dev_id][1], 3),
+                             Profiler(s_pool[dev_id][2], 3)};
     bool fin_side_used = false;
     unsigned long long fin_done[NCLS] = {0}, fin_done_el[NCLS] = {0};
     // launch the finishers for list entries [fin_done[c], hc.n_cls[c])
-    auto launch_finishers = [&](cudaStream_t fs, Profiler& fp) -> cudaError_t {
+    auto launch_finishers = [&](cudaStream_t fs_main, Profiler& fp_main) -> cudaError_t {
+        cudaError_t e0 = cudaEventRecord(s_pfork[dev_id], fs_main);
+        if (e0 != cudaSuccess) return e0;
+        bool used[3] = {false, false, false};
         for (int c = 0; c < NCLS; c++) {
+            const int q = c < 4 ? 0 : c - 3;  // pool stream of this class (3 = main)
+            cudaStream_t fs = q < 3 ? s_pool[dev_id][q] : fs_main;
+            Profiler& fp = q < 3 ? prof_pool[q] : fp_main;
             const long long cnt_c = (long long)(hc.n_cls[c] - fin_done[c]);
             const long long el_c = (long long)(hc.cls_elems[c] - fin_done_el[c]);
             if ((long long)hc.n_cls[c] > w.cls_cap[c]) return cudaErrorMemoryAllocation;
@@ -1237,6 +1253,11 @@ static int sort_impl_body(const s5g_sort_args* a) {
             const int wnt = ws_nt(c == 0 ? 1 : c == 1 ? 2 : c == 2 ? 4 : 8);
             const unsigned grid = blocks_for(cnt_c, wnt / 32);
             const SegDev* lst = w.small + w.cls_off[c] + fin_done[c];
+            if (q < 3 && !used[q]) {
+                used[q] = true;
+                cudaError_t ew = cudaStreamWaitEvent(fs, s_pfork[dev_id], 0);
+                if (ew != cudaSuccess) return ew;
+            }
             switch (c) {
                 case 0: SPROF(fp, K_SEG_WARP + 0, el_c, 32LL * el_c, (k_warp_sort<1><<<grid, wnt, 0, fs>>>(
                             lst, cnt_c, w.recA, w.recB, a->arena, a->arena_len, a->out_handles, lcps, w.ctr))); break;
@@ -1261,6 +1282,12 @@ static int sort_impl_body(const s5g_sort_args* a) {
             fin_done[c] = hc.n_cls[c];
             fin_done_el[c] = hc.cls_elems[c];
         }
+        for (int q = 0; q < 3; q++)
+            if (used[q]) {
+                cudaError_t ej = cudaEventRecord(s_pjoin[dev_id][q], s_pool[dev_id][q]);
+                if (ej == cudaSuccess) ej = cudaStreamWaitEvent(fs_main, s_pjoin[dev_id][q], 0);
+                if (ej != cudaSuccess) return ej;
+            }
         return cudaSuccess;
     };
     CK(cudaMemsetAsync(w.ctr, 0, sizeof(Counters), st));

@@ -25,7 +25,7 @@ e1.record()
 torch.cuda.synchronize()
 _lib.profile(enable=False)
 print(f"sort total (torch events): {e0.elapsed_time(e1):.3f} ms")
-last = {0: 0.0, 1: 0.0, 2: 0.0}
+last = {0: 0.0, 1: 0.0, 2: 0.0, 3: 0.0}
 for name, s, t0, t1 in _lib.timeline():
     gap = t0 - last[s]
     last[s] = t1
