@@ -497,9 +497,9 @@ struct StepCtaSmem {
     uint64_t s[16 * (MED_VMAX + 1)];       // sorted sample
     uint64_t tree[MED_VMAX + 1], inorder[MED_VMAX + 1];
     uint32_t hist[SC_R], bst[SC_R], run_off[SC_R];
-    uint32_t dst_by_e[SC_SUB];
+    uint32_t dst_by_e[SCX_SUB];
     uint16_t rcnt[SC_R * (SC_NT / 32)];
-    uint16_t kA[SC_SUB], vA[SC_SUB], kB[SC_SUB], vB[SC_SUB];
+    uint16_t kA[SCX_SUB], vA[SCX_SUB], kB[SCX_SUB], vB[SCX_SUB];
     uint16_t eqb[MED_VMAX + 1];
     int16_t sa[MED_VMAX + 1], sb[MED_VMAX + 1], sp[MED_VMAX + 1];
     uint8_t tpos[MED_VMAX + 1];
@@ -553,14 +553,24 @@ __global__ void __launch_bounds__(SC_NT, 2) k_step_cta(
     select_tree<SC_NT>(S.s, count, v, L, S.sa, S.sb, S.sp, S.tree, S.inorder, S.tpos, S.eqb);
     __syncthreads();
     // ---- classify + bucket counts (ssss.py:149-181, 292) -----------------
-    for (int base = 0; base < n; base += SC_NT) {
-        const int i = base + threadIdx.x;
-        const bool ok = i < n;
-        const uint32_t b = ok ? classify_one<VARIANT>(X[i].w[0], S.tree, S.eqb, v, L) : 0;
-        const uint32_t mask = __ballot_sync(0xffffffffu, ok);
-        if (ok) {
-            const uint32_t peers = __match_any_sync(mask, b);
-            if (lane == __ffs(peers) - 1) atomicAdd(&S.hist[b], (uint32_t)__popc(peers));
+    constexpr int CU = 4;  // keys in flight per thread
+    for (int base = 0; base < n; base += SC_NT * CU) {
+        uint64_t key[CU];
+#pragma unroll
+        for (int u = 0; u < CU; u++) {
+            const int i = base + u * SC_NT + threadIdx.x;
+            key[u] = i < n ? X[i].w[0] : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < CU; u++) {
+            const int i = base + u * SC_NT + threadIdx.x;
+            const bool ok = i < n;
+            const uint32_t b = ok ? classify_one<VARIANT>(key[u], S.tree, S.eqb, v, L) : 0;
+            const uint32_t mask = __ballot_sync(0xffffffffu, ok);
+            if (ok) {
+                const uint32_t peers = __match_any_sync(mask, b);
+                if (lane == __ffs(peers) - 1) atomicAdd(&S.hist[b], (uint32_t)__popc(peers));
+            }
         }
     }
     __syncthreads();
@@ -615,13 +625,13 @@ __global__ void __launch_bounds__(SC_NT, 2) k_step_cta(
         }
     }
     __syncthreads();
-    // ---- stable scatter per SC_SUB sub-tile (one 7-bit ranking pass) -----
-    for (int sub = 0; sub < n; sub += SC_SUB) {
-        const int m = min(SC_SUB, n - sub);
-        Rec rec[SC_ITEMS];
-        uint32_t myb[SC_ITEMS];
+    // ---- stable scatter per SCX_SUB sub-tile (one 7-bit ranking pass) -----
+    for (int sub = 0; sub < n; sub += SCX_SUB) {
+        const int m = min(SCX_SUB, n - sub);
+        Rec rec[SCX_IT];
+        uint32_t myb[SCX_IT];
 #pragma unroll
-        for (int it = 0; it < SC_ITEMS; it++) {
+        for (int it = 0; it < SCX_IT; it++) {
             const int e = threadIdx.x + it * SC_NT;
             myb[it] = BID_SENTINEL;
             if (e < m) {
@@ -632,11 +642,11 @@ __global__ void __launch_bounds__(SC_NT, 2) k_step_cta(
             S.vA[e] = (uint16_t)e;
         }
         __syncthreads();
-        rank_pass(S.kA, S.vA, S.kB, S.vB, 0, S.rcnt, S.wsum);
-        const int q0 = threadIdx.x * SC_ITEMS;
-        uint32_t bq[SC_ITEMS], st[SC_ITEMS], mx = 0;
+        rank_pass<SCX_IT>(S.kA, S.vA, S.kB, S.vB, 0, S.rcnt, S.wsum);
+        const int q0 = threadIdx.x * SCX_IT;
+        uint32_t bq[SCX_IT], st[SCX_IT], mx = 0;
 #pragma unroll
-        for (int it = 0; it < SC_ITEMS; it++) {
+        for (int it = 0; it < SCX_IT; it++) {
             const int q = q0 + it;
             bq[it] = S.kB[q];
             const bool start = q < m && (q == 0 || S.kB[q - 1] != bq[it]);
@@ -645,14 +655,14 @@ __global__ void __launch_bounds__(SC_NT, 2) k_step_cta(
         }
         const uint32_t before = block_excl_max<SC_NT>(mx, S.wsum);
 #pragma unroll
-        for (int it = 0; it < SC_ITEMS; it++) {
+        for (int it = 0; it < SCX_IT; it++) {
             const int q = q0 + it;
             st[it] = (st[it] ? st[it] : before) - 1;
             if (q < m) S.dst_by_e[S.vB[q]] = S.run_off[bq[it]] + (q - st[it]);
         }
         __syncthreads();
 #pragma unroll
-        for (int it = 0; it < SC_ITEMS; it++) {
+        for (int it = 0; it < SCX_IT; it++) {
             const int e = threadIdx.x + it * SC_NT;
             if (e >= m) break;
             const uint32_t b = myb[it];
@@ -675,7 +685,7 @@ __global__ void __launch_bounds__(SC_NT, 2) k_step_cta(
             }
         }
 #pragma unroll
-        for (int it = 0; it < SC_ITEMS; it++) {
+        for (int it = 0; it < SCX_IT; it++) {
             const int q = q0 + it;
             if (q < m && (q == m - 1 || S.kB[q + 1] != bq[it])) S.run_off[bq[it]] += q - st[it] + 1;
         }
