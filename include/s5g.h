@@ -147,6 +147,20 @@ int s5g_pack(const uint8_t *arena, int64_t arena_len, const int64_t *handles,
 int s5g_load_delimited(uint8_t *data, int64_t len, int32_t delimiter, int64_t *out_handles,
                        int64_t *out_n, void *workspace, size_t workspace_bytes, void *stream);
 
+/* Stable grouping by destination rank for the all-to-all send buffer
+ * (device): out_order[k] = index of the k-th string when strings are ordered
+ * by (dest, index); out_counts[g] (device, G entries) = strings for rank g.
+ * 1 <= G <= 127.  Workspace: s5g_group_workspace_bytes(n, G). */
+size_t s5g_group_workspace_bytes(int64_t n, int32_t G);
+int s5g_group_by_dest(const int32_t *dest, int64_t n, int32_t G, int64_t *out_order,
+                      int64_t *out_counts, void *workspace, size_t workspace_bytes, void *stream);
+
+/* Positions of sorted handles in their input array, for unique handles below
+ * map_len: map (device int32[map_len], scratch) gets map[handles[i]] = i,
+ * then out_pos[j] = map[query[j]].  Device pointers. */
+int s5g_positions(const int64_t *handles, int64_t n, const int64_t *query, int64_t m,
+                  int32_t *map, int64_t map_len, int64_t *out_pos, void *stream);
+
 /* dist_stats (strset.py:290-309) of a sorted set from its exact LCP array
  * (device): D and L. */
 int s5g_dist_stats(const int64_t *lcps, int64_t n, int64_t *out_D, int64_t *out_L, void *stream);

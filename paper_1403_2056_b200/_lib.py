@@ -74,6 +74,9 @@ SIGNATURES = {
     "s5g_set_l2_fetch_granularity": (None, [C.c_int]),
     "s5g_finisher_counters": (C.c_int, [C.POINTER(C.c_ulonglong), C.c_int, C.c_int]),
     "s5g_merge_workspace_bytes": (C.c_size_t, [_i64, _i32]),
+    "s5g_group_workspace_bytes": (C.c_size_t, [_i64, _i32]),
+    "s5g_group_by_dest": (C.c_int, [_p, _i64, _i32, _p, _p, _p, C.c_size_t, _p]),
+    "s5g_positions": (C.c_int, [_p, _i64, _p, _i64, _p, _i64, _p, _p]),
     "s5g_kway_merge": (C.c_int, [_p, _i64, _i32, C.POINTER(_i64), _p, _p, _p, _i64, _p, _p, _p,
                                  C.c_size_t, _p, C.POINTER(Stats)]),
     "s5g_last_error": (C.c_char_p, []),

@@ -840,6 +840,96 @@ __global__ void k_ld_write(const uint8_t* __restrict__ data, int64_t len,
         }
 }
 
+// ---- exchange plumbing of the multi-GPU paths --------------------------
+// Stable grouping of strings by destination rank (the per-rank counts and
+// the order of the all-to-all send buffer): per 2048-string chunk a
+// histogram, a destination-major / chunk-minor exclusive scan, then one
+// stable 7-bit ranking pass per chunk writes every string's position.
+constexpr int GD_SUB = SC_SUB;  // 2048 strings per chunk (SC_NT threads x SC_ITEMS)
+
+__global__ void __launch_bounds__(SC_NT) k_gd_hist(const int32_t* __restrict__ dest, int64_t n,
+                                                   int G, uint32_t* __restrict__ hist) {
+    __shared__ uint32_t h[128];
+    const int64_t nch = (n + GD_SUB - 1) / GD_SUB;
+    for (int g = threadIdx.x; g < G; g += SC_NT) h[g] = 0;
+    __syncthreads();
+    const int64_t c0 = (int64_t)blockIdx.x * GD_SUB;
+    for (int64_t i = c0 + threadIdx.x; i < min(c0 + GD_SUB, n); i += SC_NT) atomicAdd(&h[dest[i]], 1u);
+    __syncthreads();
+    for (int g = threadIdx.x; g < G; g += SC_NT) hist[(int64_t)g * nch + blockIdx.x] = h[g];
+}
+
+__global__ void __launch_bounds__(1024) k_gd_scan(uint32_t* __restrict__ hist, int64_t len,
+                                                  int64_t nch, int G, int64_t n,
+                                                  int64_t* __restrict__ counts) {
+    __shared__ uint32_t wsum[32];
+    constexpr int NT = 1024;
+    const int64_t per = (len + NT - 1) / NT;
+    const int64_t b0 = threadIdx.x * per, b1 = min(b0 + per, len);
+    uint32_t s = 0;
+    for (int64_t i = b0; i < b1; i++) s += hist[i];
+    uint32_t run = block_excl_sum<NT>(s, wsum, nullptr);
+    for (int64_t i = b0; i < b1; i++) {
+        const uint32_t v = hist[i];
+        hist[i] = run;
+        run += v;
+    }
+    __syncthreads();
+    // per-destination totals from the scanned offsets
+    for (int g = threadIdx.x; g < G; g += NT) {
+        const int64_t lo = (int64_t)g * nch, hi = lo + nch;
+        counts[g] = (hi < len ? (int64_t)hist[hi] : n) - (int64_t)hist[lo];
+    }
+}
+
+__global__ void __launch_bounds__(SC_NT) k_gd_write(const int32_t* __restrict__ dest, int64_t n,
+                                                    const uint32_t* __restrict__ off,
+                                                    int64_t* __restrict__ order) {
+    __shared__ uint32_t wsum[32];
+    __shared__ uint16_t rcnt[SC_R * (SC_NT / 32)];
+    __shared__ uint16_t kA[GD_SUB], vA[GD_SUB], kB[GD_SUB], vB[GD_SUB];
+    const int64_t nch = (n + GD_SUB - 1) / GD_SUB;
+    const int64_t c0 = (int64_t)blockIdx.x * GD_SUB;
+    const int m = (int)min((int64_t)GD_SUB, n - c0);
+    for (int e = threadIdx.x; e < GD_SUB; e += SC_NT) {
+        kA[e] = e < m ? (uint16_t)dest[c0 + e] : (uint16_t)BID_SENTINEL;
+        vA[e] = (uint16_t)e;
+    }
+    __syncthreads();
+    rank_pass(kA, vA, kB, vB, 0, rcnt, wsum);
+    // run starts in the ranked chunk: q - start = rank among equal dests
+    const int q0 = threadIdx.x * SC_ITEMS;
+    uint32_t st[SC_ITEMS], mx = 0;
+#pragma unroll
+    for (int i = 0; i < SC_ITEMS; i++) {
+        const int q = q0 + i;
+        if (q < m && (q == 0 || kB[q - 1] != kB[q])) mx = q + 1;
+        st[i] = mx;
+    }
+    const uint32_t before = block_excl_max<SC_NT>(mx, wsum);
+#pragma unroll
+    for (int i = 0; i < SC_ITEMS; i++) {
+        const int q = q0 + i;
+        if (q >= m) break;
+        const uint32_t start = (st[i] ? st[i] : before) - 1;
+        const int g = kB[q];
+        order[off[(int64_t)g * nch + blockIdx.x] + (q - start)] = c0 + vB[q];
+    }
+}
+
+// Input position of every sorted handle, for unique handles below map_len:
+// map[handle] = position, then a gather (no search, no sort).
+__global__ void k_pos_scatter(const int64_t* __restrict__ handles, int64_t n,
+                              int32_t* __restrict__ map) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) map[handles[i]] = (int32_t)i;
+}
+__global__ void k_pos_gather(const int64_t* __restrict__ query, int64_t m,
+                             const int32_t* __restrict__ map, int64_t* __restrict__ out) {
+    const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (j < m) out[j] = map[query[j]];
+}
+
 // dist_stats (strset.py:290-309) from an exact LCP array: since every LCP is
 // at most the length of both its strings, D_i = max(h_i, h_{i+1}) + 1 with
 // h_0 = h_n = 0, and L = sum of lcps[1:].
@@ -1876,6 +1966,45 @@ int s5g_load_delimited(uint8_t* data, int64_t len, int32_t delimiter, int64_t* o
     CK(cudaStreamSynchronize(st));
     if (hbad) return fail(S5G_E_INVALID, "input contains byte 0, which is reserved as terminator");
     *out_n = hn;
+    return 0;
+}
+
+size_t s5g_group_workspace_bytes(int64_t n, int32_t G) {
+    const int64_t nch = (std::max<int64_t>(n, 1) + GD_SUB - 1) / GD_SUB;
+    return (size_t)(4 * nch * std::max(G, 1)) + 64;
+}
+
+int s5g_group_by_dest(const int32_t* dest, int64_t n, int32_t G, int64_t* out_order,
+                      int64_t* out_counts, void* workspace, size_t workspace_bytes, void* stream) {
+    if (n < 0 || G < 1 || G > 127) return fail(S5G_E_INVALID, "need n >= 0 and 1 <= G <= 127");
+    cudaStream_t st = (cudaStream_t)stream;
+    if (n == 0) {
+        CK(cudaMemsetAsync(out_counts, 0, 8 * (size_t)G, st));
+        CK(cudaStreamSynchronize(st));
+        return 0;
+    }
+    if (workspace_bytes < s5g_group_workspace_bytes(n, G)) return fail(S5G_E_WORKSPACE, "workspace too small");
+    const int64_t nch = (n + GD_SUB - 1) / GD_SUB;
+    uint32_t* hist = (uint32_t*)workspace;
+    g_launches += 3;
+    k_gd_hist<<<(unsigned)nch, SC_NT, 0, st>>>(dest, n, G, hist);
+    k_gd_scan<<<1, 1024, 0, st>>>(hist, nch * G, nch, G, n, out_counts);
+    k_gd_write<<<(unsigned)nch, SC_NT, 0, st>>>(dest, n, hist, out_order);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(st));
+    return 0;
+}
+
+int s5g_positions(const int64_t* handles, int64_t n, const int64_t* query, int64_t m,
+                  int32_t* map, int64_t map_len, int64_t* out_pos, void* stream) {
+    if (n < 0 || m < 0 || map_len < 0) return fail(S5G_E_INVALID, "negative size");
+    if (n > INT32_MAX) return fail(S5G_E_INVALID, "n exceeds 2^31-1");
+    cudaStream_t st = (cudaStream_t)stream;
+    g_launches += 2;
+    if (n) k_pos_scatter<<<blocks_for(n, 256), 256, 0, st>>>(handles, n, map);
+    if (m) k_pos_gather<<<blocks_for(m, 256), 256, 0, st>>>(query, m, map, out_pos);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(st));
     return 0;
 }
 

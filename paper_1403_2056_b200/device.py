@@ -260,3 +260,28 @@ def kway_merge(ds: DeviceStrings, run_offsets, handles: torch.Tensor, lcps: torc
                                ws.numel(), torch.cuda.current_stream(dev).cuda_stream,
                                C.byref(st)))
     return out_h, out_l
+
+
+def group_by_dest(dest: torch.Tensor, G: int):
+    """Stable order of the strings by destination rank and the per-rank
+    counts (s5g_group_by_dest)."""
+    n = dest.numel()
+    dev = dest.device
+    d = dest.to(torch.int32).contiguous()
+    order = torch.empty(n, dtype=torch.int64, device=dev)
+    counts = torch.empty(G, dtype=torch.int64, device=dev)
+    ws = torch.empty(max(int(lib().s5g_group_workspace_bytes(n, G)), 1), dtype=torch.uint8, device=dev)
+    check(lib().s5g_group_by_dest(d.data_ptr(), n, G, order.data_ptr(), counts.data_ptr(),
+                                  ws.data_ptr(), ws.numel(), torch.cuda.current_stream(dev).cuda_stream))
+    return order, counts
+
+
+def positions(handles: torch.Tensor, query: torch.Tensor, map_len: int) -> torch.Tensor:
+    """Input position of every query handle (unique handles < map_len): s5g_positions."""
+    dev = handles.device
+    out = torch.empty(query.numel(), dtype=torch.int64, device=dev)
+    mp = torch.empty(max(map_len, 1), dtype=torch.int32, device=dev)
+    check(lib().s5g_positions(handles.data_ptr(), handles.numel(), query.data_ptr(), query.numel(),
+                              mp.data_ptr(), map_len, out.data_ptr(),
+                              torch.cuda.current_stream(dev).cuda_stream))
+    return out

@@ -35,6 +35,7 @@ on ``gloo`` without a GPU.
 
 from __future__ import annotations
 
+import ctypes as C
 from dataclasses import dataclass
 
 import numpy as np
@@ -200,7 +201,7 @@ def distributed_merge_sort(shard: Shard, backend, group=None, samples_per_rank: 
     sp, sp_g = pick_splitters([x for part in gathered for x in part], G)
     # 2. cut the sorted run (destinations are non-decreasing along it)
     dest = backend.partition(local, shard, sp, sp_g, handles=sorted_h, gidx=gidx)
-    counts = torch.bincount(dest.long(), minlength=G).tolist() if n_local else [0] * G
+    counts = backend.dest_counts(dest, G) if n_local else [0] * G
     recv_counts = _exchange_counts(counts, backend.comm_device, group)
     # 3. exchange the sorted pieces
     gidx_r = _alltoallv(gidx.to(backend.comm_device), counts, recv_counts, group)
@@ -216,7 +217,7 @@ def distributed_merge_sort(shard: Shard, backend, group=None, samples_per_rank: 
     # 4. K-way LCP merge of the G received runs
     run_off = np.r_[0, np.cumsum(recv_counts)].astype(np.int64)
     mh, ml = backend.kway_merge(arena, run_off, starts, lcp_r, dchar_r)
-    pos = handle_positions(starts, mh)
+    pos = backend.positions(arena, starts, mh)
     out_g = gidx_r[pos]
     # 5. LCP at the rank boundary
     _boundary_lcp(backend, arena, mh, ml, G, r, group)
@@ -286,6 +287,14 @@ class GpuBackend:
     def handles_of(self, ds, shard: Shard):
         return ds.handles
 
+    def dest_counts(self, dest: torch.Tensor, G: int) -> list[int]:
+        return self.group_by_dest(dest, G)[1]
+
+    def positions(self, ds, handles: torch.Tensor, query: torch.Tensor) -> torch.Tensor:
+        from . import device as D
+
+        return D.positions(handles, query, ds.arena_len)
+
     def sample_run(self, ds, handles, gidx, k: int, maxlen: int):
         """Equally spaced strings of a sorted run (prefixes <= maxlen) with
         their global indices."""
@@ -314,9 +323,10 @@ class GpuBackend:
         return D.kway_merge(ds, run_off, handles, lcps, dchar, 0)
 
     def group_by_dest(self, dest: torch.Tensor, G: int):
-        order = torch.sort(dest, stable=True).indices
-        counts = torch.bincount(dest.long(), minlength=G).tolist()
-        return order, counts
+        from . import device as D
+
+        order, counts = D.group_by_dest(dest, G)  # stable counting sort (s5g_group_by_dest)
+        return order, counts.tolist()
 
     def global_index(self, shard: Shard, order: torch.Tensor):
         return order.to(torch.int64) + shard.base_index
@@ -339,22 +349,35 @@ class GpuBackend:
         return payload, byte_counts
 
     def unpack(self, rbytes: torch.Tensor):
+        """Received zero-terminated strings -> arena + string starts
+        (s5g_load_delimited with delimiter 0)."""
+        from . import _lib
         from . import device as D
 
         alen = int(rbytes.numel())
-        arena = D.alloc_arena(alen, rbytes.device)
+        dev = rbytes.device
+        arena = D.alloc_arena(alen, dev)
+        if alen == 0:
+            starts = torch.zeros(0, dtype=torch.int64, device=dev)
+            return D.DeviceStrings(arena, 0, starts), starts
         arena[:alen] = rbytes
-        zeros = torch.nonzero(rbytes == 0).squeeze(1)
-        starts = torch.cat([torch.zeros(1, dtype=torch.int64, device=rbytes.device),
-                            zeros[:-1] + 1]) if len(zeros) else zeros
+        handles = torch.empty(alen + 1, dtype=torch.int64, device=dev)
+        ws = torch.empty(16 + 4 * ((alen + 16383) // 16384), dtype=torch.uint8, device=dev)
+        n = C.c_int64()
+        _lib.check(_lib.lib().s5g_load_delimited(arena.data_ptr(), alen, 0, handles.data_ptr(),
+                                                 C.byref(n), ws.data_ptr(), ws.numel(),
+                                                 torch.cuda.current_stream(dev).cuda_stream))
+        starts = handles[: n.value]
         return D.DeviceStrings(arena, alen, starts), starts
 
     def local_sort(self, ds, handles, want_lcps, **kw):
+        """Sorted permutation of `handles` (unique offsets) and the LCPs:
+        s5g_sort, then s5g_positions (handle -> input position map)."""
         from . import device as D
 
         local = D.DeviceStrings(ds.arena, ds.arena_len, handles)
         out_h, lcps, _ = D.sort(local, want_lcps=want_lcps, **kw)
-        return handle_positions(handles, out_h), lcps
+        return D.positions(handles, out_h, ds.arena_len), lcps
 
     def string_bytes(self, ds, h1: torch.Tensor) -> bytes:
         from . import device as D

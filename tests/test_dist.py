@@ -67,6 +67,12 @@ class CpuBackend:
     def fill_dchar(self, buf, sorted_h, lcps):
         return torch.from_numpy(oracle.fill_dchar(buf, sorted_h.numpy(), lcps.numpy()))
 
+    def dest_counts(self, dest, G):
+        return torch.bincount(dest.long(), minlength=G).tolist()
+
+    def positions(self, buf, handles, query):
+        return handle_positions(handles, query)
+
     def kway_merge(self, buf, run_off, handles, lcps, dchar):
         h, l, _ = oracle.kway_merge(buf, run_off, handles.numpy(), lcps.numpy(),
                                     dchar.numpy() if dchar is not None else None)

@@ -80,3 +80,23 @@ def test_merge_strategy_pieces_match_cpu_backend():
     assert np.array_equal(d_gpu, d_cpu) and np.all(np.diff(d_gpu) >= 0)
     dc = gpu.fill_dchar(ds, sh, lcps).cpu().numpy()
     assert np.array_equal(dc, cpu.fill_dchar(buf, sh.cpu(), lcps.cpu()).numpy())
+
+
+@pytest.mark.parametrize("G", [1, 2, 7, 64, 127])
+@pytest.mark.parametrize("n", [1, 2047, 2048, 2049, 100_000])
+def test_group_by_dest_is_stable_counting_sort(n, G):
+    rng = np.random.default_rng(n + G)
+    dest = torch.from_numpy(rng.integers(0, G, size=n).astype(np.int32)).cuda()
+    order, counts = D.group_by_dest(dest, G)
+    want = torch.sort(dest.cpu().long(), stable=True).indices  # test-side reference
+    assert torch.equal(order.cpu(), want)
+    assert counts.cpu().tolist() == torch.bincount(dest.cpu().long(), minlength=G).tolist()
+
+
+def test_positions_inverts_unique_handles():
+    rng = np.random.default_rng(9)
+    h = torch.from_numpy(rng.permutation(1 << 20)[:300_000].astype(np.int64)).cuda()
+    q = h[torch.from_numpy(rng.permutation(300_000)).cuda()]
+    pos = D.positions(h, q, 1 << 20)
+    assert torch.equal(h[pos], q)
+    assert torch.equal(pos.cpu(), handle_positions(h.cpu(), q.cpu()))
