@@ -111,8 +111,13 @@ def check_set(buffer, handles: np.ndarray) -> None:
     if n == 0:
         return
     blen = len(buffer)
-    last_zero = bytes(buffer).rfind(b"\0") if not isinstance(buffer, np.ndarray) else (
-        int(np.flatnonzero(buffer == 0)[-1]) if (buffer == 0).any() else -1)
+    if blen and int(buffer[-1]) == 0:  # the common case: O(1)
+        last_zero = blen - 1
+    elif isinstance(buffer, np.ndarray):
+        z = np.flatnonzero(buffer == 0)
+        last_zero = int(z[-1]) if len(z) else -1
+    else:
+        last_zero = bytes(buffer).rfind(b"\0")
     if last_zero < 0:
         raise ValueError("buffer is not zero-terminated")
     lo, hi = int(handles.min()), int(handles.max())
