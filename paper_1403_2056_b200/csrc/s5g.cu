@@ -355,7 +355,31 @@ __global__ void __launch_bounds__(1024) k_scan_buckets(
 // terminator-covering equality buckets are final: their handles go straight
 // to the output and the equality bucket's interior LCPs are written
 // (ssss.py:345-357).
-constexpr int SCX_IT = 2, SCX_SUB = SC_NT * SCX_IT;  // k_scatter sub-tile: 1024 strings
+//
+// Stability without a local sort: the tile is cut into 128-string chunks
+// taken by the CTA's warps round-robin, and the chunks update the per-bucket
+// running offsets (shared memory) strictly in chunk order -- a turn passed
+// from warp to warp on named barriers.  Inside a chunk, __match_any_sync gives every
+// string its rank among the earlier same-bucket strings of its 32-string
+// round.  Everything else (record loads for the next chunk, the ranks, the
+// 32-byte record writes) runs outside the turn, so the chain costs one
+// shared read-modify-write per distinct bucket of a round.
+constexpr int SCX_IT = 4;                             // rounds of 32 per chunk
+constexpr int SCX_CHUNK = 32 * SCX_IT;                // strings per warp turn
+constexpr int SCX_SUB = SCX_CHUNK * (SC_NT / 32);     // 2048 strings per CTA pass
+static_assert(SC_NT / 32 == 16, "named-barrier turn chain assumes 16 warps");
+
+// Turn hand-off between consecutive warps on hardware named barriers: warp
+// w waits on barrier w (bar.sync, 64 threads) until warp w-1 arrives there
+// (bar.arrive, which does not block and orders the arriving warp's shared
+// stores before the waiting warp's loads).  Barrier 0 doubles as the 15 -> 0
+// hand-off, so no __syncthreads may follow the chained loop.
+__device__ __forceinline__ void turn_wait(int w) {
+    asm volatile("bar.sync %0, 64;" ::"r"(w) : "memory");
+}
+__device__ __forceinline__ void turn_pass(int w) {
+    asm volatile("bar.arrive %0, 64;" ::"r"((w + 1) & (SC_NT / 32 - 1)) : "memory");
+}
 
 __global__ void __launch_bounds__(SC_NT, 2) k_scatter(
     const StepDev* __restrict__ steps, const int32_t* __restrict__ tile_step,
@@ -363,21 +387,12 @@ __global__ void __launch_bounds__(SC_NT, 2) k_scatter(
     const uint32_t* __restrict__ cnt, const uint32_t* __restrict__ tot,
     const uint32_t* __restrict__ bstart, const uint8_t* __restrict__ tpos_g,
     Rec* __restrict__ recY, int64_t* __restrict__ out_h, int64_t* __restrict__ lcps) {
-    // Per 1024-string sub-tile: (1) the records and bucket ids of the NEXT
-    // sub-tile are loaded (coalesced, 2 per thread, double-buffered in
-    // registers) while (2) two stable 7-bit ranking passes in shared memory
-    // order this sub-tile by bucket; (3) run starts give each sorted slot its
-    // offset in its bucket; (4) each thread writes its own records to their
-    // ranked destinations (whole 32-byte sectors).
     extern __shared__ __align__(16) uint8_t smem[];
-    __shared__ uint32_t wsum[32];
-    uint32_t* run_off = reinterpret_cast<uint32_t*>(smem);                 // NBMAX+1
-    uint32_t* dst_by_e = run_off + (NBMAX + 1);                            // SCX_SUB
-    uint16_t* rcnt = reinterpret_cast<uint16_t*>(dst_by_e + SCX_SUB);      // SC_R*NW
-    uint16_t* kA = rcnt + SC_R * (SC_NT / 32);
-    uint16_t* vA = kA + SCX_SUB;
-    uint16_t* kB = vA + SCX_SUB;
-    uint16_t* vB = kB + SCX_SUB;
+    uint32_t* run_off = reinterpret_cast<uint32_t*>(smem);  // NBMAX+1
+    // per-bucket facts for the write phase, so no write waits on a dependent
+    // global load: bit 7 = singleton, bits 0-3 = terminator position of an
+    // equality bucket's splitter (WORD for range buckets / no terminator)
+    uint8_t* bfact = reinterpret_cast<uint8_t*>(run_off + NBMAX + 1);  // NBMAX+1
     const int t = blockIdx.x;
     const StepDev sd = steps[tile_step[t]];
     const int ti = t - (int)sd.tile0;
@@ -386,104 +401,75 @@ __global__ void __launch_bounds__(SC_NT, 2) k_scatter(
     const int nb = sd.nb;
     const uint32_t* row = cnt + sd.cnt_off + (int64_t)ti * nb;
     const uint8_t* tp = tpos_g + sd.tree_off;
-    for (int b = threadIdx.x; b < nb; b += SC_NT) run_off[b] = bstart[sd.bk_off + b] + row[b];
-    Rec nrec[SCX_IT];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t lt = lanemask_lt();
+    for (int b = threadIdx.x; b < nb; b += SC_NT) {
+        run_off[b] = bstart[sd.bk_off + b] + row[b];
+        const uint32_t tpv = (b & 1) ? tp[b >> 1] : WORD;
+        bfact[b] = (uint8_t)(tpv | (tot[sd.bk_off + b] == 1 ? 0x80u : 0u));
+    }
+    // bucket ids run one chunk ahead: the turn never waits on a load
     uint32_t nbid[SCX_IT];
 #pragma unroll
-    for (int i = 0; i < SCX_IT; i++) {
-        const int64_t e = beg + threadIdx.x + i * SC_NT;
-        nbid[i] = BID_SENTINEL;
-        if (e < end) {
-            nbid[i] = bid[e];
-            nrec[i] = recX[e];
-        }
+    for (int j = 0; j < SCX_IT; j++) {
+        const int64_t e = beg + (int64_t)w * SCX_CHUNK + j * 32 + lane;
+        nbid[j] = e < end ? bid[e] : BID_SENTINEL;
     }
     __syncthreads();
-    for (int64_t sub = beg; sub < end; sub += SCX_SUB) {
-        const int m = (int)min((int64_t)SCX_SUB, end - sub);
+    for (int64_t c0 = beg + (int64_t)w * SCX_CHUNK, tn = w; c0 < end;
+         c0 += SCX_SUB, tn += SC_NT / 32) {
         Rec rec[SCX_IT];
-        uint32_t myb[SCX_IT];
+        uint32_t myb[SCX_IT], peers[SCX_IT];
 #pragma unroll
-        for (int i = 0; i < SCX_IT; i++) {
-            const int e = threadIdx.x + i * SC_NT;
-            myb[i] = nbid[i];
-            rec[i] = nrec[i];
-            kA[e] = (uint16_t)myb[i];
-            vA[e] = (uint16_t)e;
+        for (int j = 0; j < SCX_IT; j++) {
+            const int64_t e = c0 + j * 32 + lane;
+            myb[j] = nbid[j];
+            if (e < end) rec[j] = recX[e];
+            const int64_t en = e + SCX_SUB;
+            nbid[j] = en < end ? bid[en] : BID_SENTINEL;
         }
 #pragma unroll
-        for (int i = 0; i < SCX_IT; i++) {  // next sub-tile, in flight during the ranking
-            const int64_t e = sub + SCX_SUB + threadIdx.x + i * SC_NT;
-            nbid[i] = BID_SENTINEL;
-            if (e < end) {
-                nbid[i] = bid[e];
-                nrec[i] = recX[e];
+        for (int j = 0; j < SCX_IT; j++) peers[j] = __match_any_sync(0xffffffffu, myb[j]);
+        // ---- this warp's turn: chunks update the running offsets in order
+        if (tn) turn_wait(w);
+        uint32_t rel[SCX_IT];
+#pragma unroll
+        for (int j = 0; j < SCX_IT; j++) {
+            const int leader = __ffs(peers[j]) - 1;
+            uint32_t base = 0;
+            if (lane == leader && myb[j] != BID_SENTINEL) {
+                base = run_off[myb[j]];
+                run_off[myb[j]] = base + __popc(peers[j]);
             }
+            base = __shfl_sync(0xffffffffu, base, leader);
+            rel[j] = base + __popc(peers[j] & lt);
+            __syncwarp();
         }
-        __syncthreads();
-        if (nb <= SC_R - 1) {
-            // few buckets (steps on small segments): one 7-bit pass suffices
-            // (the sentinel 0x3FFF has low digit 127 > any bucket id)
-            rank_pass<SCX_IT>(kA, vA, kB, vB, 0, rcnt, wsum);
-            for (int e = threadIdx.x; e < SCX_SUB; e += SC_NT) {
-                kA[e] = kB[e];
-                vA[e] = vB[e];
-            }
-            __syncthreads();
-        } else {
-            rank_pass<SCX_IT>(kA, vA, kB, vB, 0, rcnt, wsum);
-            rank_pass<SCX_IT>(kB, vB, kA, vA, SC_RB, rcnt, wsum);
-        }
-        // run starts in the sorted sub-tile: thread owns q = 2t .. 2t+1
-        const int q0 = threadIdx.x * SCX_IT;
-        uint32_t bq[SCX_IT], st[SCX_IT], mx = 0;
+        turn_pass(w);
+        // ---- writes (whole 32-byte sectors) -------------------------------
 #pragma unroll
-        for (int i = 0; i < SCX_IT; i++) {
-            const int q = q0 + i;
-            bq[i] = kA[q];
-            const bool start = q < m && (q == 0 || kA[q - 1] != bq[i]);
-            if (start) mx = q + 1;
-            st[i] = mx;  // 0 = run started before this thread
-        }
-        const uint32_t before = block_excl_max<SC_NT>(mx, wsum);
-#pragma unroll
-        for (int i = 0; i < SCX_IT; i++) {
-            const int q = q0 + i;
-            st[i] = (st[i] ? st[i] : before) - 1;
-            if (q < m) dst_by_e[vA[q]] = run_off[bq[i]] + (q - st[i]);
-        }
-        __syncthreads();
-#pragma unroll
-        for (int i = 0; i < SCX_IT; i++) {
-            const int e = threadIdx.x + i * SC_NT;
-            if (e >= m) break;
-            const uint32_t b = myb[i];
-            const uint32_t rel = dst_by_e[e];
-            const int64_t pos = sd.lo + rel;
-            const uint32_t size = tot[sd.bk_off + b];
+        for (int j = 0; j < SCX_IT; j++) {
+            const uint32_t b = myb[j];
+            if (b == BID_SENTINEL) continue;
+            const int64_t pos = sd.lo + rel[j];
+            const uint32_t f = bfact[b];
             const bool odd = b & 1;
-            const int tpv = odd ? tp[b >> 1] : WORD;
-            if (size == 1 || (odd && tpv < WORD)) {
-                out_h[pos] = rec[i].h;
-                if (lcps && size > 1 && rel != bstart[sd.bk_off + b]) lcps[pos] = sd.depth + tpv;
+            const int tpv = f & 0xf;
+            if ((f & 0x80) || tpv < WORD) {
+                out_h[pos] = rec[j].h;
+                if (lcps && !(f & 0x80) && rel[j] != bstart[sd.bk_off + b]) lcps[pos] = sd.depth + tpv;
             } else if (odd) {
                 // equality bucket: continues one word deeper -> shift the cache
                 Rec o;
-                o.h = rec[i].h;
-                o.w[0] = rec[i].w[1];
-                o.w[1] = rec[i].w[2];
+                o.h = rec[j].h;
+                o.w[0] = rec[j].w[1];
+                o.w[1] = rec[j].w[2];
                 o.w[2] = 0;
                 recY[pos] = o;
             } else {
-                recY[pos] = rec[i];
+                recY[pos] = rec[j];
             }
         }
-#pragma unroll
-        for (int i = 0; i < SCX_IT; i++) {
-            const int q = q0 + i;
-            if (q < m && (q == m - 1 || kA[q + 1] != bq[i])) run_off[bq[i]] += q - st[i] + 1;
-        }
-        __syncthreads();
     }
 }
 
@@ -497,14 +483,10 @@ struct StepCtaSmem {
     uint64_t s[16 * (MED_VMAX + 1)];       // sorted sample
     uint64_t tree[MED_VMAX + 1], inorder[MED_VMAX + 1];
     uint32_t hist[SC_R], bst[SC_R], run_off[SC_R];
-    uint32_t dst_by_e[SCX_SUB];
-    uint16_t rcnt[SC_R * (SC_NT / 32)];
-    uint16_t kA[SCX_SUB], vA[SCX_SUB], kB[SCX_SUB], vB[SCX_SUB];
     uint16_t eqb[MED_VMAX + 1];
     int16_t sa[MED_VMAX + 1], sb[MED_VMAX + 1], sp[MED_VMAX + 1];
     uint8_t tpos[MED_VMAX + 1];
     uint32_t wsum[32];
-    unsigned fetched;
 };
 
 template <int VARIANT>
@@ -529,7 +511,6 @@ __global__ void __launch_bounds__(SC_NT, 2) k_step_cta(
     int P = 1;
     while (P < count) P <<= 1;
     const int lane = threadIdx.x & 31;
-    if (threadIdx.x == 0) S.fetched = 0;
     unsigned my_fetch = 0;
     // ---- refill the cached words when the segment ran out of them --------
     if (!nvalid) {
@@ -625,75 +606,68 @@ __global__ void __launch_bounds__(SC_NT, 2) k_step_cta(
         }
     }
     __syncthreads();
-    // ---- stable scatter per SCX_SUB sub-tile (one 7-bit ranking pass) -----
-    for (int sub = 0; sub < n; sub += SCX_SUB) {
-        const int m = min(SCX_SUB, n - sub);
-        Rec rec[SCX_IT];
-        uint32_t myb[SCX_IT];
+    // ---- stable scatter: 64-string chunks update the offsets in chunk order
+    // (the turn chain of k_scatter); bucket ids are recomputed here
+    {
+        const int w = threadIdx.x >> 5;
+        const uint32_t lt = lanemask_lt();
+        __syncthreads();
+        for (int c0 = w * SCX_CHUNK, tn = w; c0 < n; c0 += SCX_SUB, tn += SC_NT / 32) {
+            Rec rec[SCX_IT];
+            uint32_t myb[SCX_IT], peers[SCX_IT];
 #pragma unroll
-        for (int it = 0; it < SCX_IT; it++) {
-            const int e = threadIdx.x + it * SC_NT;
-            myb[it] = BID_SENTINEL;
-            if (e < m) {
-                rec[it] = X[sub + e];
-                myb[it] = classify_one<VARIANT>(rec[it].w[0], S.tree, S.eqb, v, L);
+            for (int j = 0; j < SCX_IT; j++) {
+                const int e = c0 + j * 32 + lane;
+                myb[j] = BID_SENTINEL;
+                if (e < n) rec[j] = X[e];
             }
-            S.kA[e] = (uint16_t)myb[it];
-            S.vA[e] = (uint16_t)e;
-        }
-        __syncthreads();
-        rank_pass<SCX_IT>(S.kA, S.vA, S.kB, S.vB, 0, S.rcnt, S.wsum);
-        const int q0 = threadIdx.x * SCX_IT;
-        uint32_t bq[SCX_IT], st[SCX_IT], mx = 0;
 #pragma unroll
-        for (int it = 0; it < SCX_IT; it++) {
-            const int q = q0 + it;
-            bq[it] = S.kB[q];
-            const bool start = q < m && (q == 0 || S.kB[q - 1] != bq[it]);
-            if (start) mx = q + 1;
-            st[it] = mx;
-        }
-        const uint32_t before = block_excl_max<SC_NT>(mx, S.wsum);
+            for (int j = 0; j < SCX_IT; j++) {
+                const int e = c0 + j * 32 + lane;
+                if (e < n) myb[j] = classify_one<VARIANT>(rec[j].w[0], S.tree, S.eqb, v, L);
+                peers[j] = __match_any_sync(0xffffffffu, myb[j]);
+            }
+            if (tn) turn_wait(w);
+            uint32_t rel[SCX_IT];
 #pragma unroll
-        for (int it = 0; it < SCX_IT; it++) {
-            const int q = q0 + it;
-            st[it] = (st[it] ? st[it] : before) - 1;
-            if (q < m) S.dst_by_e[S.vB[q]] = S.run_off[bq[it]] + (q - st[it]);
-        }
-        __syncthreads();
+            for (int j = 0; j < SCX_IT; j++) {
+                const int leader = __ffs(peers[j]) - 1;
+                uint32_t base = 0;
+                if (lane == leader && myb[j] != BID_SENTINEL) {
+                    base = S.run_off[myb[j]];
+                    S.run_off[myb[j]] = base + __popc(peers[j]);
+                }
+                base = __shfl_sync(0xffffffffu, base, leader);
+                rel[j] = base + __popc(peers[j] & lt);
+                __syncwarp();
+            }
+            turn_pass(w);
 #pragma unroll
-        for (int it = 0; it < SCX_IT; it++) {
-            const int e = threadIdx.x + it * SC_NT;
-            if (e >= m) break;
-            const uint32_t b = myb[it];
-            const uint32_t rel = S.dst_by_e[e];
-            const uint32_t size = S.hist[b];
-            const bool odd = b & 1;
-            const int tpv = odd ? S.tpos[b >> 1] : WORD;
-            if (size == 1 || (odd && tpv < WORD)) {
-                out_h[lo + rel] = rec[it].h;
-                if (lcps && size > 1 && rel != S.bst[b]) lcps[lo + rel] = depth + tpv;
-            } else if (odd) {
-                Rec o;
-                o.h = rec[it].h;
-                o.w[0] = rec[it].w[1];
-                o.w[1] = rec[it].w[2];
-                o.w[2] = 0;
-                Y[rel] = o;
-            } else {
-                Y[rel] = rec[it];
+            for (int j = 0; j < SCX_IT; j++) {
+                const uint32_t b = myb[j];
+                if (b == BID_SENTINEL) continue;
+                const uint32_t size = S.hist[b];
+                const bool odd = b & 1;
+                const int tpv = odd ? S.tpos[b >> 1] : WORD;
+                if (size == 1 || (odd && tpv < WORD)) {
+                    out_h[lo + rel[j]] = rec[j].h;
+                    if (lcps && size > 1 && rel[j] != S.bst[b]) lcps[lo + rel[j]] = depth + tpv;
+                } else if (odd) {
+                    Rec o;
+                    o.h = rec[j].h;
+                    o.w[0] = rec[j].w[1];
+                    o.w[1] = rec[j].w[2];
+                    o.w[2] = 0;
+                    Y[rel[j]] = o;
+                } else {
+                    Y[rel[j]] = rec[j];
+                }
             }
         }
-#pragma unroll
-        for (int it = 0; it < SCX_IT; it++) {
-            const int q = q0 + it;
-            if (q < m && (q == m - 1 || S.kB[q + 1] != bq[it])) S.run_off[bq[it]] += q - st[it] + 1;
-        }
-        __syncthreads();
     }
-    if (my_fetch) atomicAdd(&S.fetched, my_fetch);
-    __syncthreads();
-    if (threadIdx.x == 0 && S.fetched) atomicAdd(&ctr->fetches, (unsigned long long)S.fetched);
+    // (no __syncthreads after the turn chain: barrier 0 may hold a hand-off)
+    my_fetch = __reduce_add_sync(0xffffffffu, my_fetch);
+    if (lane == 0 && my_fetch) atomicAdd(&ctr->fetches, (unsigned long long)my_fetch);
 }
 
 // LCP at a bucket boundary of a device-wide step at depth d: both strings
@@ -1168,8 +1142,7 @@ static size_t carve(Workspace* w, uint8_t* base, int64_t n, int64_t t_medium) {
 static size_t smem_sample(int P, int v) { return (size_t)P * 8 + (size_t)3 * (v + 1) * 2 + 16; }
 static constexpr size_t SMEM_CLS_UNROLL = (size_t)(VMAX + 1) * 8 + (size_t)(NBMAX + 1) / 2 * 4;
 static constexpr size_t SMEM_CLS = SMEM_CLS_UNROLL + (size_t)(VMAX + 1) * 2;
-static constexpr size_t SMEM_SC = (size_t)(NBMAX + 1) * 4 + (size_t)SCX_SUB * 4 +
-                                  (size_t)SC_R * (SC_NT / 32) * 2 + (size_t)4 * SCX_SUB * 2;
+static constexpr size_t SMEM_SC = (size_t)(NBMAX + 1) * 5;
 
 static int set_smem_attrs() {
     // per device: kernel attributes + the byte-PEXT table of the finishers
