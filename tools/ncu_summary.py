@@ -51,7 +51,7 @@ for r in data:
 for e in kern.values():
     e["dram_bytes_per_launch"] = e["dram_bytes"] / e["launches"]
     e["warp_inst_per_launch"] = e["warp_inst"] / e["launches"]
-json.dump({"source": f"ncu --set full, one C2 sort (bench.py --steps 1 --warmup 0), {prefix}_ncu_kernels.csv",
+json.dump({"source": f"ncu --set full, one C2 sort (tools/one_sort.py), {prefix}_ncu_kernels.csv",
            "kernels": kern}, open(prefix + "_traffic.json", "w"), indent=1)
 for k, e in sorted(kern.items(), key=lambda x: -x[1]["ms"]):
     print(f"{k:28s} {e['launches']:3d} {e['ms']:8.3f} ms {e['dram_bytes'] / 1e9:8.3f} GB")

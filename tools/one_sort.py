@@ -1,0 +1,21 @@
+"""Exactly one sort (with LCPs) of a config, for ncu captures: upload, one
+untimed warm-up sort outside the capture range is NOT done -- ncu replays
+each kernel anyway, and every launch of the capture belongs to this sort."""
+import argparse
+import sys
+
+import torch
+
+sys.path.insert(0, ".")
+from paper_1403_2056_b200 import corpora  # noqa: E402
+from paper_1403_2056_b200 import device as D  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="c2_dna")
+ap.add_argument("--scale", type=float, default=1.0)
+a = ap.parse_args()
+buf, hnd = corpora.CONFIGS[a.config](a.scale)
+ds = D.upload(buf, hnd)
+out = D.sort(ds, want_lcps=True)
+torch.cuda.synchronize()
+print("one sort done", a.config, len(hnd))
