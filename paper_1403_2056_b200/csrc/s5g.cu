@@ -4,6 +4,7 @@
 // _ParallelS5Run.execute (parallel.py:400-445): rounds of batched
 // device-wide S^5 steps over "large" segments, then one launch that finishes
 // every small segment in a CTA, then the boundary-LCP fix-up.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -70,7 +71,7 @@ __global__ void __launch_bounds__(NT) k_sample_tree(
     for (int j = threadIdx.x; j < P; j += NT) {
         uint64_t x = ~0ull;
         if (j < count) {
-            int64_t idx = (int64_t)(splitmix64(key0 + j) % (uint64_t)sd.n);
+            const int64_t idx = sample_pos(key0, j, count, sd.n);
             if (hroot) {  // the root step, sampled from the input while k_init runs
                 x = load_key(arena, alen, hroot[sd.lo + idx], sd.depth);
             } else {
@@ -89,13 +90,103 @@ __global__ void __launch_bounds__(NT) k_sample_tree(
                            inorder_g + sd.tree_off, tpos_g + sd.tree_off, eqb_g + sd.tree_off);
 }
 
+// Root sample on a thread-block cluster: the 16384-key root sample is sorted
+// by 8 CTAs (2048 keys each, register bitonic), then merged by rank -- each
+// key's position = its index in its own run + the number of keys of every
+// other run ordered before it (equal keys of lower-ranked CTAs first, so the
+// ranks are a permutation).  Every CTA first copies all 8 runs out of
+// distributed shared memory with coalesced 16-byte loads (random remote
+// loads in the binary searches were DSMEM-request bound: 0.11 ms), searches
+// locally, then stores its keys into CTA 0's shared memory at their ranks;
+// CTA 0 selects the splitter tree.  One CTA did the whole 16384-key sort in
+// 0.19 ms on the critical path of the root step; the cluster draws the same
+// sample, so the tree is identical.
+constexpr int SCL = 8, SCL_IT = 2, SCL_RUN = SAMPLE_NT * SCL_IT;  // 8 x 2048 keys
+
+__global__ void __cluster_dims__(SCL, 1, 1) __launch_bounds__(SAMPLE_NT) k_sample_root(
+    const StepDev* __restrict__ steps, const uint8_t* __restrict__ arena, int64_t alen,
+    const int64_t* __restrict__ hroot, uint64_t seed, uint64_t* __restrict__ tree_g,
+    uint64_t* __restrict__ inorder_g, uint8_t* __restrict__ tpos_g, uint16_t* __restrict__ eqb_g) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    extern __shared__ __align__(16) uint8_t smem[];
+    const StepDev sd = steps[0];
+    const int v = sd.v, count = sd.count;
+    constexpr int P = SCL * SCL_RUN;
+    uint64_t* run = reinterpret_cast<uint64_t*>(smem);  // this CTA's sorted keys
+    uint64_t* all = run + SCL_RUN;  // copies of all runs; then (CTA 0) the merged sample
+    int16_t* sa = reinterpret_cast<int16_t*>(all + P);
+    int16_t* sb = sa + (v + 1);
+    int16_t* sp = sb + (v + 1);
+    const int r = (int)cluster.block_rank();
+    const uint64_t key0 = splitmix64(seed ^ splitmix64(sd.lo ^ splitmix64(sd.n ^ splitmix64(sd.depth))));
+    uint64_t c[SCL_IT];
+    int64_t hv[SCL_IT];
+#pragma unroll
+    for (int e = 0; e < SCL_IT; e++) {  // same sample positions as k_sample_tree
+        const int j = r * SCL_RUN + threadIdx.x * SCL_IT + e;
+        hv[e] = j < count ? hroot[sd.lo + sample_pos(key0, j, count, sd.n)] : -1;
+    }
+#pragma unroll
+    for (int e = 0; e < SCL_IT; e++) c[e] = hv[e] >= 0 ? load_key(arena, alen, hv[e], sd.depth) : ~0ull;
+    reg_bitonic_keys<SCL_IT>(c, SCL_RUN, run, true);
+#pragma unroll
+    for (int e = 0; e < SCL_IT; e++) run[threadIdx.x * SCL_IT + e] = c[e];
+    cluster.sync();  // every run sorted and visible cluster-wide
+    {
+        constexpr int V4 = SCL_RUN / 2;  // uint4 per run
+        uint4* dst = reinterpret_cast<uint4*>(all);
+#pragma unroll
+        for (int q = 0; q < SCL; q++) {
+            const uint4* src = reinterpret_cast<const uint4*>(cluster.map_shared_rank(run, q));
+            for (int i = threadIdx.x; i < V4; i += SAMPLE_NT) dst[q * V4 + i] = src[i];
+        }
+    }
+    __syncthreads();
+    int pos[SCL_IT];
+#pragma unroll
+    for (int e = 0; e < SCL_IT; e++) {
+        const uint64_t x = c[e];
+        int lo[SCL];
+#pragma unroll
+        for (int q = 0; q < SCL; q++) lo[q] = 0;
+        // branch-free binary searches, the runs interleaved; runs of lower
+        // rank count keys <= x, higher rank keys < x (own run: skipped)
+#pragma unroll 1
+        for (int half = SCL_RUN / 2; half > 0; half >>= 1) {
+#pragma unroll
+            for (int q = 0; q < SCL; q++) {
+                const uint64_t y = all[q * SCL_RUN + lo[q] + half - 1];
+                const bool before = q < r ? y <= x : y < x;
+                lo[q] += before ? half : 0;
+            }
+        }
+        int p = threadIdx.x * SCL_IT + e;
+#pragma unroll
+        for (int q = 0; q < SCL; q++) {
+            if (q == r) continue;
+            const uint64_t y = all[q * SCL_RUN + lo[q]];
+            p += lo[q] + ((lo[q] == SCL_RUN - 1) && (q < r ? y <= x : y < x));
+        }
+        pos[e] = p;
+    }
+    cluster.sync();  // all searches done: CTA 0's copy region can take the merge
+    uint64_t* s0 = cluster.map_shared_rank(all, 0);
+#pragma unroll
+    for (int e = 0; e < SCL_IT; e++) s0[pos[e]] = c[e];
+    cluster.sync();  // CTA 0 holds the merged sample
+    if (r != 0) return;
+    select_tree<SAMPLE_NT>(all, count, v, sd.levels, sa, sb, sp, tree_g + sd.tree_off,
+                           inorder_g + sd.tree_off, tpos_g + sd.tree_off, eqb_g + sd.tree_off);
+}
+
 // Test entry: select_splitters on a given sorted sample.
-__global__ void __launch_bounds__(SAMPLE_NT) k_select_only(const uint64_t* sample, int count, int v,
-                                                           int L, uint64_t* tree, uint64_t* inorder,
+__global__ void __launch_bounds__(SAMPLE_NT) k_select_only(const uint64_t* sample, int count, int cap,
+                                                           int v, int L, uint64_t* tree, uint64_t* inorder,
                                                            uint8_t* tpos, uint16_t* eqb) {
     extern __shared__ __align__(16) uint8_t smem[];
     uint64_t* s = reinterpret_cast<uint64_t*>(smem);
-    int16_t* sa = reinterpret_cast<int16_t*>(s + count);
+    int16_t* sa = reinterpret_cast<int16_t*>(s + cap);
     int16_t* sb = sa + (v + 1);
     int16_t* sp = sb + (v + 1);
     for (int j = threadIdx.x; j < count; j += SAMPLE_NT) s[j] = sample[j];
@@ -136,7 +227,10 @@ __global__ void __launch_bounds__(CLS_NT) k_classify(
     const uint8_t* __restrict__ arena, int64_t alen, Rec* __restrict__ recX,
     uint16_t* __restrict__ bid, uint32_t* __restrict__ cnt,
     const uint64_t* __restrict__ tree_g, const uint16_t* __restrict__ eqb_g,
-    Counters* __restrict__ ctr) {
+    Counters* __restrict__ ctr, const int64_t* __restrict__ hroot) {
+    // hroot != null: the root step builds the work records itself from the
+    // input handles (k_init fused in: one pass over the input instead of a
+    // record write + re-read)
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ __align__(8) uint64_t bar;
     __shared__ unsigned fetched;
@@ -179,7 +273,13 @@ __global__ void __launch_bounds__(CLS_NT) k_classify(
             ok[u] = i < end;
             key[u] = 0;
             if (ok[u]) {
-                if (sd.nvalid) {
+                if (hroot) {
+                    Rec r;
+                    r.h = hroot[i];
+                    load_words3(arena, alen, r.h, sd.depth, r.w);
+                    recX[i] = r;
+                    key[u] = r.w[0];
+                } else if (sd.nvalid) {
                     key[u] = recX[i].w[0];
                 } else {  // refill the record's three cached words
                     uint64_t wv[3];
@@ -1104,7 +1204,8 @@ static size_t carve(Workspace* w, uint8_t* base, int64_t n, int64_t t_medium) {
     // big steps round their tile count up to whole waves: <= 2x the tiles
     w->tiles_cap = 2 * (nn / TILE) + w->steps_cap + 1 + (nn + 2 * w->steps_cap) / 32 +
                    (nn + 2 * w->steps_cap) / 1024 + 2 * w->steps_cap + 2;
-    w->cnt_cap = nn * (2 * (int64_t)NBMAX / TILE + 2) + w->steps_cap * 2;
+    w->cnt_cap = nn * (2 * (int64_t)NBMAX / TILE + 2) + w->steps_cap * 2 +
+                 2 * (int64_t)NBMAX;  // a small root's MIN_TILE tiles: <= (n / MIN_TILE + 1) * NBMAX
     w->bk_cap = nn + 2 * w->steps_cap;
     w->tree_cap = nn / 2 + 4 * w->steps_cap + 2;
     {
@@ -1140,6 +1241,8 @@ static size_t carve(Workspace* w, uint8_t* base, int64_t n, int64_t t_medium) {
 
 
 static size_t smem_sample(int P, int v) { return (size_t)P * 8 + (size_t)3 * (v + 1) * 2 + 16; }
+static constexpr size_t SMEM_SAMPLE_ROOT =
+    (size_t)SCL_RUN * 8 + (size_t)SCL * SCL_RUN * 8 + (size_t)3 * (VMAX + 1) * 2 + 16;
 static constexpr size_t SMEM_CLS_UNROLL = (size_t)(VMAX + 1) * 8 + (size_t)(NBMAX + 1) / 2 * 4;
 static constexpr size_t SMEM_CLS = SMEM_CLS_UNROLL + (size_t)(VMAX + 1) * 2;
 static constexpr size_t SMEM_SC = (size_t)(NBMAX + 1) * 5;
@@ -1162,6 +1265,8 @@ static int set_smem_attrs() {
             }
         CK(cudaMemcpyToSymbol(g_pext8, lut, sizeof(lut)));
     }
+    CK(cudaFuncSetAttribute(k_sample_root, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)SMEM_SAMPLE_ROOT));
     CK(cudaFuncSetAttribute(k_sample_tree<SAMPLE_NT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)smem_sample(2 * (VMAX + 1), VMAX)));
     CK(cudaFuncSetAttribute(k_sample_tree<256, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1386,11 +1491,11 @@ static int sort_impl_body(const s5g_sort_args* a) {
         int P = 1;
         while (P < d.count) P <<= 1;
         const long long sb = (long long)d.count * 16 + 27LL * d.v;
-        if (P == 16 * SAMPLE_NT)
+        if (P == SCL * SCL_RUN)
             SPROF(prof_hi, K_SAMPLE, 1, sb,
-                  (k_sample_tree<SAMPLE_NT, true><<<1, SAMPLE_NT, smem_sample(P, d.v), st_hi>>>(
-                      w.root_step, a->arena, a->arena_len, w.recA, a->seed, w.tree, w.inorder,
-                      w.tpos, w.eqb, a->handles)));
+                  (k_sample_root<<<SCL, SAMPLE_NT, SMEM_SAMPLE_ROOT, st_hi>>>(
+                      w.root_step, a->arena, a->arena_len, a->handles, a->seed, w.tree,
+                      w.inorder, w.tpos, w.eqb)));
         else
             SPROF(prof_hi, K_SAMPLE, 1, sb,
                   (k_sample_tree<256, false><<<1, 256, smem_sample(P, d.v), st_hi>>>(
@@ -1399,10 +1504,12 @@ static int sort_impl_body(const s5g_sort_args* a) {
         CK(cudaGetLastError());
         CK(cudaEventRecord(ev_samp, st_hi));
     }
-    PROF(K_INIT, n, 56LL * n, (k_init<<<blocks_for(n, 256), 256, 0, st>>>(a->arena, a->arena_len,
-                                                                 a->handles, n, a->depth,
-                                                                 w.recA)));
-    CK(cudaGetLastError());
+    if (!early_root) {  // else the root's k_classify builds the records
+        PROF(K_INIT, n, 56LL * n, (k_init<<<blocks_for(n, 256), 256, 0, st>>>(a->arena, a->arena_len,
+                                                                     a->handles, n, a->depth,
+                                                                     w.recA)));
+        CK(cudaGetLastError());
+    }
     hc.fetches = 0;
     int64_t n_jobs = 0;
     std::vector<SegDev> large;
@@ -1488,6 +1595,11 @@ static int sort_impl_body(const s5g_sort_args* a) {
                 d.nb = 2 * d.v + 1;
                 d.nvalid = s.flags & SEG_NV_MASK;
                 d.ntiles = (int32_t)((s.n + TILE - 1) / TILE);
+                if (round == 0 && d.ntiles < 2 * g_sms)
+                    // a small root (C1: 10^6 strings = 31 tiles) would run on a
+                    // fifth of the SMs: spread it over up to two CTAs per SM
+                    d.ntiles = (int32_t)std::max<int64_t>(
+                        d.ntiles, std::min<int64_t>(2 * g_sms, (s.n + MIN_TILE - 1) / MIN_TILE));
                 if (d.ntiles >= g_sms) {
                     // big steps: a whole number of waves of 2 CTAs per SM
                     const int wave = 2 * g_sms;
@@ -1565,21 +1677,22 @@ static int sort_impl_body(const s5g_sort_args* a) {
                          w.eqb, nullptr)));
             CK(cudaGetLastError());
             const unsigned ntiles = (unsigned)tile0;
+            const int64_t* root_h = (round == 0 && early_root) ? a->handles : nullptr;
             int64_t round_elems = 0, cls_bytes = 0;
             for (auto& d : steps) {
                 round_elems += d.n;
-                cls_bytes += (d.nvalid ? 10LL : 66LL) * d.n;
+                cls_bytes += (root_h ? 74LL : d.nvalid ? 10LL : 66LL) * d.n;  // root: h, 3 words, record, id
             }
             if (a->variant == S5G_VARIANT_UNROLL)
                 PROF(K_CLASSIFY, round_elems, cls_bytes,
                      (k_classify<S5G_VARIANT_UNROLL><<<ntiles, CLS_NT, SMEM_CLS_UNROLL, st>>>(
                          w.steps, w.tile_step, a->arena, a->arena_len, recX, w.bid, w.cnt,
-                         w.tree, w.eqb, w.ctr)));
+                         w.tree, w.eqb, w.ctr, root_h)));
             else
                 PROF(K_CLASSIFY, round_elems, cls_bytes,
                      (k_classify<S5G_VARIANT_EQUAL><<<ntiles, CLS_NT, SMEM_CLS, st>>>(
                          w.steps, w.tile_step, a->arena, a->arena_len, recX, w.bid, w.cnt,
-                         w.tree, w.eqb, w.ctr)));
+                         w.tree, w.eqb, w.ctr, root_h)));
             CK(cudaGetLastError());
             PROF(K_SCAN_COLS, cnt_off, 8LL * cnt_off + 4LL * bk_off,
                  (k_scan_cols<<<(unsigned)cblk_step.size(), 1024, 0, st>>>(
@@ -1838,9 +1951,10 @@ int s5g_select_splitters(const uint64_t* sample, int64_t count, int64_t v, uint6
         return fail(S5G_E_INVALID, "v must be 2^d-1 <= 8191 and 1 <= count <= 16384");
     if (int rc = set_smem_attrs()) return rc;
     cudaStream_t st = (cudaStream_t)stream;
-    size_t smem = (size_t)count * 8 + (size_t)3 * (v + 1) * 2 + 16;
+    const int64_t cap = std::max(count, v);  // select_tree reuses the sample region (>= v words)
+    size_t smem = (size_t)cap * 8 + (size_t)3 * (v + 1) * 2 + 16;
     g_launches++;
-    k_select_only<<<1, SAMPLE_NT, smem, st>>>(sample, (int)count, (int)v, levels_of(v), tree,
+    k_select_only<<<1, SAMPLE_NT, smem, st>>>(sample, (int)count, (int)cap, (int)v, levels_of(v), tree,
                                               inorder, term_pos, eq_bucket);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(st));

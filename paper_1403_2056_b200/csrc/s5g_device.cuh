@@ -104,6 +104,18 @@ __device__ __forceinline__ uint64_t splitmix64(uint64_t z) {
     return z ^ (z >> 31);
 }
 
+// Position of sample j of `count` in a segment of n strings: stratified --
+// one uniform pick inside each of `count` equal strata (draw_sample,
+// ssss.py:76-82, picks uniformly at random; which positions are sampled
+// never changes the output).  Consecutive samples fall in consecutive
+// address ranges, so the random gathers of a large root sample share TLB
+// entries instead of missing on nearly every one.
+__device__ __forceinline__ int64_t sample_pos(uint64_t key0, int j, int count, int64_t n) {
+    const int64_t a = (int64_t)j * n / count, b = (int64_t)(j + 1) * n / count;
+    const int64_t w = b > a ? b - a : 1;
+    return min(a + (int64_t)(splitmix64(key0 + j) % (uint64_t)w), n - 1);
+}
+
 // ---------------------------------------------------------------------------
 // TMA-class 1-D bulk copies (cp.async.bulk) completing on an mbarrier.
 

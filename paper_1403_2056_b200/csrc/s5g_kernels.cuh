@@ -17,6 +17,7 @@
 namespace s5g {
 
 constexpr int TILE = 32768;     // elements per classify / scatter CTA
+constexpr int MIN_TILE = 8192;  // ... at least, for a root step spread over all SMs
 constexpr int CLS_NT = 512;
 constexpr int SC_NT = 512;
 constexpr int SC_ITEMS = 4;
@@ -302,6 +303,29 @@ __device__ __forceinline__ int upper_bound_u64(const uint64_t* s, int a, int b, 
     }
     return a;
 }
+// Equal-run bounds around a pick m (s[m] == x, s sorted), galloping out of
+// m: O(log run) probes, one probe when x is not duplicated (a full binary
+// search over the node's range was 14 bank-conflicted probes at the top).
+__device__ __forceinline__ int run_lo(const uint64_t* s, int a, int m, uint64_t x) {
+    int hi = m, k = 1;  // s[hi] >= x
+    for (;;) {
+        const int p = m - k;
+        if (p < a) return lower_bound_u64(s, a, hi, x);
+        if (s[p] < x) return lower_bound_u64(s, p + 1, hi, x);
+        hi = p;
+        k <<= 1;
+    }
+}
+__device__ __forceinline__ int run_hi(const uint64_t* s, int m, int b, uint64_t x) {
+    int lo = m + 1, k = 1;  // first index > x lies in [lo, b]
+    for (;;) {
+        const int p = m + k;
+        if (p >= b) return upper_bound_u64(s, lo, b, x);
+        if (s[p] > x) return upper_bound_u64(s, lo, p, x);
+        lo = p + 1;
+        k <<= 1;
+    }
+}
 
 template <int NT>
 __device__ void select_tree(const uint64_t* s, int count, int v, int L, int16_t* sa, int16_t* sb,
@@ -328,8 +352,8 @@ __device__ void select_tree(const uint64_t* s, int count, int v, int L, int16_t*
                 int m = (a + b) >> 1;
                 val = s[m];
                 la = a;
-                lb = lower_bound_u64(s, a, m, val);
-                ra = upper_bound_u64(s, m + 1, b, val);
+                lb = run_lo(s, a, m, val);
+                ra = run_hi(s, m, b, val);
                 rb = b;
                 cp = m;
             }
@@ -345,11 +369,36 @@ __device__ void select_tree(const uint64_t* s, int count, int v, int L, int16_t*
         __syncthreads();
     }
     // term_pos / eq_final per in-order slot, and the equality bucket each
-    // node maps to: 2*eq_leftmost[node_to_inorder[node]] + 1 (ssss.py:137-143)
-    for (int i = threadIdx.x; i < v; i += NT) tpos[i] = (uint8_t)term_pos(inorder[i]);
+    // node maps to: 2*eq_leftmost[node_to_inorder[node]] + 1 (ssss.py:137-143).
+    // `inorder` may be global memory: it is scanned from a copy in the (now
+    // dead) sample's shared memory -- binary searches into it in place were
+    // 8 x 13 dependent L2 round trips per thread (0.04 ms of the root step).
+    uint64_t* ino = const_cast<uint64_t*>(s);  // count >= v
+    for (int i = threadIdx.x; i < v; i += NT) ino[i] = inorder[i];
+    __syncthreads();
+    // eq_leftmost of every in-order slot = start of its run of equal
+    // splitters: a block max-scan of run starts (chunks of consecutive slots
+    // per thread), kept in sa; a node's slot is its level-order position
+    // mapped through the complete tree's in-order numbering
+    {
+        const int per = (v + NT - 1) / NT, i0 = threadIdx.x * per, i1 = min(v, i0 + per);
+        uint32_t mx = 0;
+        for (int i = i0; i < i1; i++) {
+            tpos[i] = (uint8_t)term_pos(ino[i]);
+            if (i == 0 || ino[i] != ino[i - 1]) mx = i + 1;
+        }
+        __shared__ uint32_t wsum[32];
+        uint32_t run = block_excl_max<NT>(mx, wsum);
+        for (int i = i0; i < i1; i++) {
+            if (i == 0 || ino[i] != ino[i - 1]) run = i + 1;
+            sa[i] = (int16_t)(run - 1);
+        }
+    }
+    __syncthreads();
     for (int node = 1 + threadIdx.x; node <= v; node += NT) {
-        int lo = lower_bound_u64(inorder, 0, v, tree[node]);
-        eqb[node] = (uint16_t)(2 * lo + 1);
+        const int l = 31 - __clz(node), p = node - (1 << l);
+        const int slot = p * (1 << (L - l)) + (1 << (L - l - 1)) - 1;
+        eqb[node] = (uint16_t)(2 * sa[slot] + 1);
     }
     if (threadIdx.x == 0) { tree[0] = 0; eqb[0] = 0; }
 }
