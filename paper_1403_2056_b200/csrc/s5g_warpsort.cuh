@@ -15,13 +15,12 @@
 // a 3-way comparator), so whenever the varying bits of the round's words fit,
 // a slot is ONE u64: group | PEXT(word, varying-bit mask) | tag, compared and
 // moved as a single value; the words stay in shared memory by tag.  The
-// PEXT runs byte-wise through a 256x256 lookup table in global memory (L1).
+// PEXT is a six-step register compress network (pext_key).
 #pragma once
 #include "s5g_kernels.cuh"
 
 namespace s5g {
 
-__device__ uint8_t g_pext8[256 * 256];  // [mask * 256 + byte] = pext(byte, mask)
 __device__ unsigned long long g_fin_ctr[12];  // s5g_finisher_counters
 
 // meta = active << 22 | group << 11 | tag   (11-bit slots and tags)
@@ -33,13 +32,23 @@ __device__ __forceinline__ bool cs_less(uint64_t ka, uint32_t ma, uint64_t kb, u
 }
 
 struct Pext {
+    uint64_t V;      // varying-bit mask
+    uint64_t mv[6];  // bits moved right by 2^i in step i of the compress network
+    int cb;          // popcount(V)
+};
+
+__device__ uint8_t g_pext8[256 * 256];  // [mask * 256 + byte] = pext(byte, mask)
+
+// Byte-wise PEXT through a 256x256 table (L1): cheap to set up, so the warp
+// finisher's many small rounds use it (a few strings per lane and round).
+struct PextLut {
     uint64_t V;   // varying-bit mask
     uint64_t SH;  // 6-bit shift of byte b's extracted bits at 6b
     int cb;       // popcount(V)
 };
 
-__device__ __forceinline__ Pext pext_setup(uint64_t V) {
-    Pext p;
+__device__ __forceinline__ PextLut pext_lut_setup(uint64_t V) {
+    PextLut p;
     p.V = V;
     p.cb = __popcll(V);
     uint64_t sh = 0;
@@ -53,10 +62,7 @@ __device__ __forceinline__ Pext pext_setup(uint64_t V) {
     return p;
 }
 
-// Bit-extract of x under the CTA-uniform mask V, byte-wise through a 256x256
-// table.  Callers run it in ONE rolled loop over the slots staged in shared
-// memory: inlined per register slot it was a third of the finishers' code.
-__device__ __forceinline__ uint64_t pext_key(uint64_t x, const Pext& p) {
+__device__ __forceinline__ uint64_t pext_lut_key(uint64_t x, const PextLut& p) {
     uint64_t c = 0;
 #pragma unroll
     for (int b = 0; b < 8; b++) {
@@ -66,6 +72,44 @@ __device__ __forceinline__ uint64_t pext_key(uint64_t x, const Pext& p) {
                  << ((p.SH >> (6 * b)) & 63);
     }
     return c;
+}
+
+// Bit-extract (PEXT) under a mask uniform over the caller, as the
+// compress network of Hacker's Delight 7-4: the mask's six move sets are
+// derived once per round (~170 instructions), after which an extract is 6
+// register-only steps.  The CTA rounds pack up to 2048 words per round with
+// it (through the table, ~12 instructions and an L1 load per byte, packing
+// was a fifth of the CTA finishers' instructions).  Order-preserving: the
+// kept bits keep their significance order, exactly as pext_lut_key.
+__device__ __forceinline__ Pext pext_setup(uint64_t V) {
+    Pext p;
+    p.V = V;
+    p.cb = __popcll(V);
+    uint64_t m = V, mk = ~m << 1;
+#pragma unroll
+    for (int i = 0; i < 6; i++) {
+        uint64_t mp = mk ^ (mk << 1);  // parallel suffix of the zeros to the right
+        mp ^= mp << 2;
+        mp ^= mp << 4;
+        mp ^= mp << 8;
+        mp ^= mp << 16;
+        mp ^= mp << 32;
+        const uint64_t mv = mp & m;
+        p.mv[i] = mv;
+        m = (m ^ mv) | (mv >> (1 << i));
+        mk &= ~mp;
+    }
+    return p;
+}
+
+__device__ __forceinline__ uint64_t pext_key(uint64_t x, const Pext& p) {
+    x &= p.V;
+#pragma unroll
+    for (int i = 0; i < 6; i++) {
+        const uint64_t t = x & p.mv[i];
+        x = (x ^ t) | (t >> (1 << i));
+    }
+    return x;
 }
 
 // Words at `depth` of the active slots, from the work records while `depth`
@@ -465,7 +509,7 @@ __device__ void warp_finish(const int64_t* __restrict__ hbt, uint16_t* __restric
 #pragma unroll
         for (int e = 0; e < IT; e++)
             if (meta[e] >> 22 & 1) { o |= key[e]; a &= key[e]; }
-        const Pext px = pext_setup(warp_or64(o) ^ warp_and64(a));
+        const PextLut px = pext_lut_setup(warp_or64(o) ^ warp_and64(a));
         if (px.cb == 0) {
             // all active words equal: the slots are already in (group, tag)
             // order (duplicate-heavy inputs spend most rounds here)
@@ -478,7 +522,7 @@ __device__ void warp_finish(const int64_t* __restrict__ hbt, uint16_t* __restric
                 if (i < gn) xs[g0 + i] = key[e];
             }
             __syncwarp();
-            for (int q = lane; q < gn; q += 32) xs[g0 + q] = pext_key(xs[g0 + q], px);
+            for (int q = lane; q < gn; q += 32) xs[g0 + q] = pext_lut_key(xs[g0 + q], px);
             __syncwarp();
             uint64_t c[IT];
 #pragma unroll
@@ -885,16 +929,16 @@ __global__ void __launch_bounds__(32 * W, 24 / W) k_cta_sort(
                 o1 |= S.red[2 * W + v];
                 a1 &= S.red[3 * W + v];
             }
-            const Pext px = pext_setup(o ^ a);
+            const int cb0 = __popcll(o ^ a);  // word0 bits (the plans: thread 0, below)
             if (try_two) {
                 // as many leading characters of word1 as fit beside word0's
                 // varying bits in 53 bits; u32 single-word rounds are cheaper
                 // when ties after word0 are unlikely (m^2 <= 2^cb0)
                 const uint64_t V1 = o1 ^ a1;
-                int bits = px.cb;
+                int bits = cb0;
                 while (jb < WORD && bits + __popc((uint32_t)(V1 >> (56 - 8 * jb)) & 255u) <= 53)
                     bits += __popc((uint32_t)(V1 >> (56 - 8 * jb)) & 255u), jb++;
-                const bool u32_ok = px.cb <= 21 && (uint64_t)m * (uint64_t)m <= (1ull << px.cb);
+                const bool u32_ok = cb0 <= 21 && (uint64_t)m * (uint64_t)m <= (1ull << cb0);
                 two = jb > 0 && !u32_ok;
                 if (!two) jb = 0;
                 const uint64_t keep1 = jb == WORD ? ~0ull : ~(~0ull >> (8 * jb));
@@ -903,8 +947,8 @@ __global__ void __launch_bounds__(32 * W, 24 / W) k_cta_sort(
                 o1 &= keep1;
                 a1 &= keep1;
             }
-            const int mode = two ? 0 : (first_round && px.cb <= 21) ? 1 : (px.cb <= 42) ? 2 : 3;
-            if (px.cb == 0 && (!two || (o1 ^ a1) == 0)) {
+            const int mode = two ? 0 : (first_round && cb0 <= 21) ? 1 : (cb0 <= 42) ? 2 : 3;
+            if (cb0 == 0 && (!two || (o1 ^ a1) == 0)) {
                 // every active slot has the same window: already in (group,
                 // tag) order, nothing to sort
             } else if (mode != 3) {
@@ -913,7 +957,7 @@ __global__ void __launch_bounds__(32 * W, 24 / W) k_cta_sort(
                 // sort values: two-word (word0 bits | word1 bits | tag), u32
                 // (word bits | tag) on the first round, else (group | bits | tag)
                 if (threadIdx.x == 0) {
-                    S.px[0] = px;
+                    S.px[0] = pext_setup(o ^ a);
                     S.px[1] = pext_setup(o1 ^ a1);
                 }
 #pragma unroll
@@ -927,9 +971,10 @@ __global__ void __launch_bounds__(32 * W, 24 / W) k_cta_sort(
                 }
                 __syncthreads();
                 const int lim = first_round ? m : 256 * W;
+                const Pext p0 = S.px[0], p1 = S.px[1];
                 for (int q = threadIdx.x; q < lim; q += NT) {
-                    uint64_t v = pext_key(S.xk[q], S.px[0]);
-                    if (two) v = (v << S.px[1].cb) | pext_key(S.kb1[q], S.px[1]);
+                    uint64_t v = pext_key(S.xk[q], p0);
+                    if (two) v = (v << p1.cb) | pext_key(S.kb1[q], p1);
                     S.xk[q] = v;
                 }
                 __syncthreads();
