@@ -281,21 +281,30 @@ __device__ __forceinline__ uint64_t warp_and64(uint64_t x) {
     return x;
 }
 
+// First stop of two raw little-endian 8-byte windows of strings equal so
+// far: the lowest byte where they differ or where `ra` holds its terminator
+// (bytes past the arena read 0), or 8 if none.  Raw words: no byte swap or
+// terminator masking on the long equal stretches of deep-LCP pairs (they
+// were a third of the C4 finishers' instructions as load_key).
+__device__ __forceinline__ int raw_stop(uint64_t ra, uint64_t rb) {
+    const uint64_t x = (ra ^ rb) | zero_bytes(ra);
+    return x ? (__ffsll((long long)x) - 1) >> 3 : WORD;
+}
+
 // LCP of the strings at a and b, known equal before depth d, capped at cap:
 // the warp compares 32 words (256 characters) per step.
 __device__ __forceinline__ int64_t warp_lcp_from(const uint8_t* __restrict__ arena, int64_t alen,
                                                  int64_t a, int64_t b, int64_t d, int64_t cap,
                                                  unsigned& fetches, int lane) {
     for (; d < cap; d += 32 * WORD) {
-        const uint64_t wa = load_key(arena, alen, a, d + WORD * lane);
-        const uint64_t wb = load_key(arena, alen, b, d + WORD * lane);
+        const uint64_t ra = load_word_le(arena, alen, a + d + WORD * lane);
+        const uint64_t rb = load_word_le(arena, alen, b + d + WORD * lane);
         fetches += 2;
-        const int tp = term_pos(wa);
-        const bool stop = wa != wb || tp < WORD;
-        const uint32_t m = __ballot_sync(0xffffffffu, stop);
+        const int p = raw_stop(ra, rb);
+        const uint32_t m = __ballot_sync(0xffffffffu, p < WORD);
         if (m) {
             const int f = __ffs(m) - 1;
-            const int64_t l = d + WORD * lane + (wa != wb ? (__clzll(wa ^ wb) >> 3) : tp);
+            const int64_t l = d + WORD * lane + p;
             return min(cap, __shfl_sync(0xffffffffu, l, f));
         }
     }
@@ -339,14 +348,10 @@ __device__ __forceinline__ int64_t run_common_prefix(const uint32_t (&meta)[IT],
         int64_t my = c;
         if (lane >= 2 && lane < (int)r) {
             for (int64_t d = depth; d < my; d += WORD) {
-                const uint64_t wa = load_key(arena, alen, h0, d), wb = load_key(arena, alen, hm, d);
+                const int p = raw_stop(load_word_le(arena, alen, h0 + d), load_word_le(arena, alen, hm + d));
                 fetches += 2;
-                if (wa != wb) {
-                    my = min(my, d + (__clzll(wa ^ wb) >> 3));
-                    break;
-                }
-                if (term_pos(wa) < WORD) {
-                    my = min(my, d + term_pos(wa));
+                if (p < WORD) {
+                    my = min(my, d + p);
                     break;
                 }
             }
@@ -364,21 +369,24 @@ constexpr int SMALL_RUN = 8;  // runs finished by direct comparisons
 #endif
 
 // Order two strings sharing d characters: (a <= b, their LCP); a warp-wide
-// 256-character compare per step.
+// 256-character compare per step on raw words (raw_stop).
 __device__ __forceinline__ bool warp_le(const uint8_t* __restrict__ arena, int64_t alen,
                                        int64_t a, int64_t b, int64_t d, int64_t* l,
                                        unsigned& fetches, int lane) {
     for (;; d += 32 * WORD) {
-        const uint64_t wa = load_key(arena, alen, a, d + WORD * lane);
-        const uint64_t wb = load_key(arena, alen, b, d + WORD * lane);
+        const uint64_t ra = load_word_le(arena, alen, a + d + WORD * lane);
+        const uint64_t rb = load_word_le(arena, alen, b + d + WORD * lane);
         fetches += 2;
-        const int tp = term_pos(wa);
-        const bool stop = wa != wb || tp < WORD;
-        const uint32_t m = __ballot_sync(0xffffffffu, stop);
+        const int p = raw_stop(ra, rb);
+        const uint32_t m = __ballot_sync(0xffffffffu, p < WORD);
         if (m) {
             const int f = __ffs(m) - 1;
-            const int64_t lf = d + WORD * lane + (wa != wb ? (__clzll(wa ^ wb) >> 3) : tp);
-            const int le = wa <= wb;
+            const int64_t lf = d + WORD * lane + p;
+            // at the stop byte: a's terminator with b equal (equal strings),
+            // or the first differing byte (a terminator is the smallest byte)
+            const uint32_t ca = p < WORD ? (uint32_t)(ra >> (8 * p)) & 255u : 0u;
+            const uint32_t cb = p < WORD ? (uint32_t)(rb >> (8 * p)) & 255u : 0u;
+            const int le = ca <= cb;
             *l = __shfl_sync(0xffffffffu, lf, f);
             return __shfl_sync(0xffffffffu, le, f);
         }
