@@ -165,3 +165,27 @@ def test_config_parity_scaled(cfg, scale):
     got_h = out_h.cpu().numpy()
     assert np.array_equal(got_h, h)
     assert np.array_equal(lcps.cpu().numpy(), l)
+
+
+@pytest.mark.parametrize("n", [32769, 40000, 8192 * 148 * 2 + 7, 3_000_000])
+@pytest.mark.parametrize("alphabet", [2, 4, 26])
+def test_root_step_sizes_vs_oracle(n, alphabet):
+    """Roots just above the fused-CTA limit (device-wide root, cluster root
+    sample with strata narrower than a string, few tiles), around the
+    small-root tile spreading limit (2 x SMs x MIN_TILE), and larger; small
+    alphabets make most scatter rounds collide inside a 32-string round."""
+    rng = np.random.default_rng(n + alphabet)
+    lens = rng.integers(0, 14, size=n).astype(np.int64)
+    off = np.zeros(n, dtype=np.int64)
+    np.cumsum(lens[:-1] + 1, out=off[1:])
+    buf = np.zeros(int(lens.sum()) + n, dtype=np.uint8)
+    chars = (97 + rng.integers(0, alphabet, size=int(lens.sum()))).astype(np.uint8)
+    mask = np.ones(len(buf), dtype=bool)
+    mask[off + lens] = False
+    buf[mask] = chars
+    hnd = rng.permutation(off) if alphabet == 4 else off
+    ds = D.upload(buf, hnd)
+    h, l, _ = D.sort(ds, want_lcps=True)
+    oh, ol, _ = oracle.parallel_s5(buf, hnd)
+    assert np.array_equal(h.cpu().numpy(), oh)
+    assert np.array_equal(l.cpu().numpy(), ol)
