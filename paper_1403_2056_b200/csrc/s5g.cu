@@ -334,7 +334,11 @@ __global__ void k_classify_only(const uint64_t* __restrict__ keys, int64_t n,
 
 // Tile-minor running prefix per bucket column; bucket totals.  One CTA per
 // 32 bucket columns: lane = column (coalesced 128 B rows), warp = a chunk of
-// tiles; chunk sums are scanned in shared memory, then applied.
+// tiles; chunk sums are scanned in shared memory, then applied.  A chunk of
+// up to SCAN_REG tiles is held in registers: its column loads are issued
+// together (they were a serial chain of L2 round trips, read twice).
+constexpr int SCAN_REG = 16;
+
 __global__ void __launch_bounds__(1024) k_scan_cols(const StepDev* __restrict__ steps,
                                                     const int32_t* __restrict__ cblk_step,
                                                     uint32_t* __restrict__ cnt,
@@ -347,27 +351,46 @@ __global__ void __launch_bounds__(1024) k_scan_cols(const StepDev* __restrict__ 
     const int per = (sd.ntiles + 31) / 32;
     const int t0 = c * per, t1 = min(sd.ntiles, t0 + per);
     uint32_t* col = cnt + sd.cnt_off + b;
+    const bool reg = per <= SCAN_REG;
+    uint32_t v[SCAN_REG];
     uint32_t s = 0;
-    if (b < sd.nb)
-        for (int t = t0; t < t1; t++) s += col[(int64_t)t * sd.nb];
+    if (b < sd.nb) {
+        if (reg) {
+#pragma unroll
+            for (int k = 0; k < SCAN_REG; k++) v[k] = t0 + k < t1 ? col[(int64_t)(t0 + k) * sd.nb] : 0u;
+#pragma unroll
+            for (int k = 0; k < SCAN_REG; k++) s += v[k];
+        } else {
+            for (int t = t0; t < t1; t++) s += col[(int64_t)t * sd.nb];
+        }
+    }
     part[c][bl] = s;
     __syncthreads();
     if (c == 0) {
         uint32_t run = 0;
         for (int i = 0; i < 32; i++) {
-            uint32_t v = part[i][bl];
+            uint32_t x = part[i][bl];
             part[i][bl] = run;
-            run += v;
+            run += x;
         }
         if (b < sd.nb) tot[sd.bk_off + b] = run;
     }
     __syncthreads();
     if (b < sd.nb) {
         uint32_t run = part[c][bl];
-        for (int t = t0; t < t1; t++) {
-            uint32_t v = col[(int64_t)t * sd.nb];
-            col[(int64_t)t * sd.nb] = run;
-            run += v;
+        if (reg) {
+#pragma unroll
+            for (int k = 0; k < SCAN_REG; k++)
+                if (t0 + k < t1) {
+                    col[(int64_t)(t0 + k) * sd.nb] = run;
+                    run += v[k];
+                }
+        } else {
+            for (int t = t0; t < t1; t++) {
+                uint32_t x = col[(int64_t)t * sd.nb];
+                col[(int64_t)t * sd.nb] = run;
+                run += x;
+            }
         }
     }
 }
