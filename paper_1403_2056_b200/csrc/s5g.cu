@@ -1443,7 +1443,11 @@ static int sort_impl_body(const s5g_sort_args* a) {
         cudaError_t e0 = cudaEventRecord(s_pfork[dev_id], fs_main);
         if (e0 != cudaSuccess) return e0;
         bool used[3] = {false, false, false};
-        for (int c = 0; c < NCLS; c++) {
+        // the warp classes share pool 0: the largest first, so the short
+        // launches fill the tail instead of delaying it
+        static const int order[NCLS] = {3, 2, 1, 0, 4, 5, 6};
+        for (int oi = 0; oi < NCLS; oi++) {
+            const int c = order[oi];
             const int q = c < 4 ? 0 : c - 3;  // pool stream of this class (3 = main)
             cudaStream_t fs = q < 3 ? s_pool[dev_id][q] : fs_main;
             Profiler& fp = q < 3 ? prof_pool[q] : fp_main;
