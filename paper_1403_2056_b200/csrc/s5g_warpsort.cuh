@@ -645,12 +645,14 @@ __device__ void warp_finish(const int64_t* __restrict__ hbt, uint16_t* __restric
 // one segment per warp; 8 warps per CTA (4 for 256-string segments, whose
 // per-warp staging would exceed the 48 KB of static shared memory)
 __host__ __device__ constexpr int ws_nt(int items) { return items >= 8 ? 128 : 256; }
+// 4 CTAs per SM: caps k_warp_sort<8> at 128 registers (it took 167, 3 CTAs)
+constexpr int WS_MINB = 4;
 #ifndef GROUP_MODE_MIN_W
 #define GROUP_MODE_MIN_W 8
 #endif
 
 template <int ITEMS>
-__global__ void __launch_bounds__(ws_nt(ITEMS)) k_warp_sort(
+__global__ void __launch_bounds__(ws_nt(ITEMS), WS_MINB) k_warp_sort(
     const SegDev* __restrict__ segs, int64_t nsegs, Rec* __restrict__ recA,
     Rec* __restrict__ recB, const uint8_t* __restrict__ arena, int64_t alen,
     int64_t* __restrict__ out_h, int64_t* __restrict__ lcps, Counters* __restrict__ ctr) {
