@@ -1,6 +1,6 @@
-"""Exactly one sort (with LCPs) of a config, for ncu captures: upload, one
-untimed warm-up sort outside the capture range is NOT done -- ncu replays
-each kernel anyway, and every launch of the capture belongs to this sort."""
+"""Exactly one sort (with LCPs) of a config, for ncu captures: no warm-up
+sort, so every captured launch belongs to this one sort (ncu replays each
+kernel itself; its times are cold-cache and serialised anyway)."""
 import argparse
 import sys
 
