@@ -134,6 +134,28 @@ def test_step_hook_bucket_lcp_property():
     assert checked > 100
 
 
+def test_step_hook_full_tree_root():
+    # a root with the full v = 8191 tree (the cluster-sampled root step and the
+    # root classify that builds the work records) seen through the hook:
+    # bounds cover the input, Eq. 1 credits hold, output equals the oracle
+    # (GPU-sized trees reach v = 8191 above 8192 x SEG_TARGET strings)
+    buf, hnd = corpora.gen_random(9_000_000, 21)
+    s = P.StringSet(buf.tobytes(), hnd)
+    records = []
+    res = P.s5_sort(s, want_lcps=True, step_hook=records.append)
+    h, lcps, _ = oracle.parallel_s5(s.buffer, s.handles)
+    assert np.array_equal(res.set.handles, h) and np.array_equal(res.lcps, lcps)
+    root = records[0]
+    assert root.lo == 0 and root.hi == len(hnd) and root.tree.num_buckets == 2 * 8191 + 1
+    assert root.bounds[0] == 0 and root.bounds[-1] == len(hnd)
+    assert (np.diff(root.bounds) >= 0).all()
+    rng = np.random.default_rng(1)
+    for i in rng.integers(0, root.tree.num_buckets, size=400):
+        lo, hi = int(root.bounds[i]), int(root.bounds[i + 1])
+        if hi - lo >= 2:
+            assert oracle.lcp(s.buffer, res.set.handles[lo], res.set.handles[hi - 1]) >= int(root.child_depths[i])
+
+
 def test_hook_errors_propagate():
     s = _clusters(3000)
 
@@ -167,13 +189,14 @@ def test_config_parity_scaled(cfg, scale):
     assert np.array_equal(lcps.cpu().numpy(), l)
 
 
-@pytest.mark.parametrize("n", [32769, 40000, 8192 * 148 * 2 + 7, 3_000_000])
+@pytest.mark.parametrize("n", [32769, 40000, 8192 * 148 * 2 + 7, 9_000_000])
 @pytest.mark.parametrize("alphabet", [2, 4, 26])
 def test_root_step_sizes_vs_oracle(n, alphabet):
-    """Roots just above the fused-CTA limit (device-wide root, cluster root
-    sample with strata narrower than a string, few tiles), around the
-    small-root tile spreading limit (2 x SMs x MIN_TILE), and larger; small
-    alphabets make most scatter rounds collide inside a 32-string round."""
+    """Roots just above the fused-CTA limit (device-wide root with few tiles),
+    around the small-root tile spreading limit (2 x SMs x MIN_TILE), and
+    above 8192 x SEG_TARGET (the full v = 8191 tree drawn by the cluster
+    root sample); small alphabets make most scatter rounds collide inside a
+    32-string round."""
     rng = np.random.default_rng(n + alphabet)
     lens = rng.integers(0, 14, size=n).astype(np.int64)
     off = np.zeros(n, dtype=np.int64)
