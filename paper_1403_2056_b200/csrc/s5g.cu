@@ -1263,6 +1263,9 @@ static size_t carve(Workspace* w, uint8_t* base, int64_t n, int64_t t_medium) {
 }
 
 
+// samples of at least this many keys sort with 1024 threads per step
+// (C1's root: 2048 keys on 256 threads were 0.05 ms of its 0.37 ms sort)
+constexpr int SAMPLE_WIDE_P = 2048;
 static size_t smem_sample(int P, int v) { return (size_t)P * 8 + (size_t)3 * (v + 1) * 2 + 16; }
 static constexpr size_t SMEM_SAMPLE_ROOT =
     (size_t)SCL_RUN * 8 + (size_t)SCL * SCL_RUN * 8 + (size_t)3 * (VMAX + 1) * 2 + 16;
@@ -1293,6 +1296,8 @@ static int set_smem_attrs() {
     CK(cudaFuncSetAttribute(k_sample_tree<SAMPLE_NT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)smem_sample(2 * (VMAX + 1), VMAX)));
     CK(cudaFuncSetAttribute(k_sample_tree<256, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)smem_sample(2 * (VMAX + 1), VMAX)));
+    CK(cudaFuncSetAttribute(k_sample_tree<SAMPLE_NT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)smem_sample(2 * (VMAX + 1), VMAX)));
     CK(cudaFuncSetAttribute(k_select_only, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)smem_sample(2 * (VMAX + 1), VMAX)));
@@ -1523,6 +1528,11 @@ static int sort_impl_body(const s5g_sort_args* a) {
                   (k_sample_root<<<SCL, SAMPLE_NT, SMEM_SAMPLE_ROOT, st_hi>>>(
                       w.root_step, a->arena, a->arena_len, a->handles, a->seed, w.tree,
                       w.inorder, w.tpos, w.eqb)));
+        else if (P >= SAMPLE_WIDE_P)  // one CTA: the widest that fits the sample
+            SPROF(prof_hi, K_SAMPLE, 1, sb,
+                  (k_sample_tree<SAMPLE_NT, false><<<1, SAMPLE_NT, smem_sample(P, d.v), st_hi>>>(
+                      w.root_step, a->arena, a->arena_len, w.recA, a->seed, w.tree, w.inorder,
+                      w.tpos, w.eqb, a->handles)));
         else
             SPROF(prof_hi, K_SAMPLE, 1, sb,
                   (k_sample_tree<256, false><<<1, 256, smem_sample(P, d.v), st_hi>>>(
@@ -1695,6 +1705,11 @@ static int sort_impl_body(const s5g_sort_args* a) {
             } else if (maxP == 16 * SAMPLE_NT)
                 PROF(K_SAMPLE, nsteps, sample_bytes,
                      (k_sample_tree<SAMPLE_NT, true><<<nsteps, SAMPLE_NT, smem_sample(maxP, maxv), st>>>(
+                         w.steps, a->arena, a->arena_len, recX, a->seed, w.tree, w.inorder, w.tpos,
+                         w.eqb, nullptr)));
+            else if (maxP >= SAMPLE_WIDE_P)
+                PROF(K_SAMPLE, nsteps, sample_bytes,
+                     (k_sample_tree<SAMPLE_NT, false><<<nsteps, SAMPLE_NT, smem_sample(maxP, maxv), st>>>(
                          w.steps, a->arena, a->arena_len, recX, a->seed, w.tree, w.inorder, w.tpos,
                          w.eqb, nullptr)));
             else
