@@ -334,10 +334,11 @@ __global__ void k_classify_only(const uint64_t* __restrict__ keys, int64_t n,
 
 // Tile-minor running prefix per bucket column; bucket totals.  One CTA per
 // 32 bucket columns: lane = column (coalesced 128 B rows), warp = a chunk of
-// tiles; chunk sums are scanned in shared memory, then applied.  A chunk of
-// up to SCAN_REG tiles is held in registers: its column loads are issued
-// together (they were a serial chain of L2 round trips, read twice).
-constexpr int SCAN_REG = 16;
+// tiles; chunk sums are scanned in shared memory, then applied.  A chunk is
+// walked in blocks of SCAN_REG tiles whose column loads are issued together
+// (one at a time they were a serial chain of round trips: 0.085 ms at C2's
+// 592 tiles).
+constexpr int SCAN_REG = 16, SCAN_KEEP = 24;
 
 __global__ void __launch_bounds__(1024) k_scan_cols(const StepDev* __restrict__ steps,
                                                     const int32_t* __restrict__ cblk_step,
@@ -351,19 +352,24 @@ __global__ void __launch_bounds__(1024) k_scan_cols(const StepDev* __restrict__ 
     const int per = (sd.ntiles + 31) / 32;
     const int t0 = c * per, t1 = min(sd.ntiles, t0 + per);
     uint32_t* col = cnt + sd.cnt_off + b;
-    const bool reg = per <= SCAN_REG;
-    uint32_t v[SCAN_REG];
     uint32_t s = 0;
-    if (b < sd.nb) {
-        if (reg) {
+    // chunks of up to SCAN_KEEP tiles (C2: 592 tiles -> 19) stay in registers
+    // between the two passes: one round of loads in all
+    const bool keep = per <= SCAN_KEEP;
+    uint32_t kv[SCAN_KEEP];
+    if (b < sd.nb && keep) {
 #pragma unroll
-            for (int k = 0; k < SCAN_REG; k++) v[k] = t0 + k < t1 ? col[(int64_t)(t0 + k) * sd.nb] : 0u;
+        for (int k = 0; k < SCAN_KEEP; k++) kv[k] = t0 + k < t1 ? col[(int64_t)(t0 + k) * sd.nb] : 0u;
+#pragma unroll
+        for (int k = 0; k < SCAN_KEEP; k++) s += kv[k];
+    } else if (b < sd.nb)
+        for (int tb = t0; tb < t1; tb += SCAN_REG) {
+            uint32_t v[SCAN_REG];
+#pragma unroll
+            for (int k = 0; k < SCAN_REG; k++) v[k] = tb + k < t1 ? col[(int64_t)(tb + k) * sd.nb] : 0u;
 #pragma unroll
             for (int k = 0; k < SCAN_REG; k++) s += v[k];
-        } else {
-            for (int t = t0; t < t1; t++) s += col[(int64_t)t * sd.nb];
         }
-    }
     part[c][bl] = s;
     __syncthreads();
     if (c == 0) {
@@ -376,21 +382,26 @@ __global__ void __launch_bounds__(1024) k_scan_cols(const StepDev* __restrict__ 
         if (b < sd.nb) tot[sd.bk_off + b] = run;
     }
     __syncthreads();
-    if (b < sd.nb) {
+    if (b < sd.nb && keep) {
         uint32_t run = part[c][bl];
-        if (reg) {
+#pragma unroll
+        for (int k = 0; k < SCAN_KEEP; k++)
+            if (t0 + k < t1) {
+                col[(int64_t)(t0 + k) * sd.nb] = run;
+                run += kv[k];
+            }
+    } else if (b < sd.nb) {
+        uint32_t run = part[c][bl];
+        for (int tb = t0; tb < t1; tb += SCAN_REG) {
+            uint32_t v[SCAN_REG];
+#pragma unroll
+            for (int k = 0; k < SCAN_REG; k++) v[k] = tb + k < t1 ? col[(int64_t)(tb + k) * sd.nb] : 0u;
 #pragma unroll
             for (int k = 0; k < SCAN_REG; k++)
-                if (t0 + k < t1) {
-                    col[(int64_t)(t0 + k) * sd.nb] = run;
+                if (tb + k < t1) {
+                    col[(int64_t)(tb + k) * sd.nb] = run;
                     run += v[k];
                 }
-        } else {
-            for (int t = t0; t < t1; t++) {
-                uint32_t x = col[(int64_t)t * sd.nb];
-                col[(int64_t)t * sd.nb] = run;
-                run += x;
-            }
         }
     }
 }
