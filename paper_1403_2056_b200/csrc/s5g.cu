@@ -611,12 +611,14 @@ __global__ void __launch_bounds__(SC_NT, 2) k_scatter(
 // (sample + select_splitters + classify + counts + stable scatter +
 // children), so the many small steps of later rounds cost one launch
 // instead of five and never round-trip their counts through global memory.
-// Bucket ids are recomputed in the scatter pass (<= 5 tree levels) instead of
-// being stored.  Same outputs as the device-wide step (ssss.py:281-358).
+// Bucket ids (<= 63 buckets) are kept in shared memory by the count pass,
+// so the scatter's turn chain never waits on a record load.  Same outputs as
+// the device-wide step (ssss.py:281-358).
 struct StepCtaSmem {
     uint64_t s[16 * (MED_VMAX + 1)];       // sorted sample
     uint64_t tree[MED_VMAX + 1], inorder[MED_VMAX + 1];
     uint32_t hist[SC_R], bst[SC_R], run_off[SC_R];
+    uint8_t bids[MED_MAX];  // bucket of every string (<= 63 buckets), from the count pass
     uint16_t eqb[MED_VMAX + 1];
     int16_t sa[MED_VMAX + 1], sb[MED_VMAX + 1], sp[MED_VMAX + 1];
     uint8_t tpos[MED_VMAX + 1];
@@ -683,6 +685,7 @@ __global__ void __launch_bounds__(SC_NT, 2) k_step_cta(
             const uint32_t b = ok ? classify_one<VARIANT>(key[u], S.tree, S.eqb, v, L) : 0;
             const uint32_t mask = __ballot_sync(0xffffffffu, ok);
             if (ok) {
+                S.bids[i] = (uint8_t)b;
                 const uint32_t peers = __match_any_sync(mask, b);
                 if (lane == __ffs(peers) - 1) atomicAdd(&S.hist[b], (uint32_t)__popc(peers));
             }
@@ -747,20 +750,20 @@ __global__ void __launch_bounds__(SC_NT, 2) k_step_cta(
         const uint32_t lt = lanemask_lt();
         __syncthreads();
         for (int c0 = w * SCX_CHUNK, tn = w; c0 < n; c0 += SCX_SUB, tn += SC_NT / 32) {
+            // bucket ids from shared memory: the turn never waits on a load
             Rec rec[SCX_IT];
             uint32_t myb[SCX_IT], peers[SCX_IT];
 #pragma unroll
             for (int j = 0; j < SCX_IT; j++) {
                 const int e = c0 + j * 32 + lane;
                 myb[j] = BID_SENTINEL;
-                if (e < n) rec[j] = X[e];
+                if (e < n) {
+                    rec[j] = X[e];
+                    myb[j] = S.bids[e];
+                }
             }
 #pragma unroll
-            for (int j = 0; j < SCX_IT; j++) {
-                const int e = c0 + j * 32 + lane;
-                if (e < n) myb[j] = classify_one<VARIANT>(rec[j].w[0], S.tree, S.eqb, v, L);
-                peers[j] = __match_any_sync(0xffffffffu, myb[j]);
-            }
+            for (int j = 0; j < SCX_IT; j++) peers[j] = __match_any_sync(0xffffffffu, myb[j]);
             if (tn) turn_wait(w);
             uint32_t rel[SCX_IT];
 #pragma unroll
