@@ -35,12 +35,12 @@ PEAKS = ROOT / "MEASURED_PEAKS.json"
 FALLBACK_HBM = 6650.0  # GB/s, B200_PROFILING.md fallback
 
 
-TRAFFIC = ROOT / "profiles" / "r01h_traffic.json"
+TRAFFIC = ROOT / "profiles" / "r01i_traffic.json"
 
 
 def ncu_traffic(kernel: str):
     """dram bytes per launch of `kernel` from the committed ncu --set full
-    capture (profiles/r01h_traffic.json), or None."""
+    capture (profiles/r01i_traffic.json), or None."""
     try:
         d = json.loads(TRAFFIC.read_text())["kernels"]
     except Exception:
