@@ -263,7 +263,7 @@ __global__ void __launch_bounds__(CLS_NT) k_classify(
     mbar_wait(&bar, 0);
     const int lane = threadIdx.x & 31;
     unsigned my_fetch = 0;
-    constexpr int U = 8;
+    constexpr int U = 6;  // keys in flight per thread (8: 0.47 ms, 6: 0.45 ms for the C2 root)
     for (int64_t base = beg; base < end; base += (int64_t)CLS_NT * U) {
         uint64_t key[U];
         bool ok[U];
