@@ -2,14 +2,17 @@
 """Benchmark: GPU S^5 string sort with LCP array (BASELINE.json metric).
 
 One "step" = one full sort (handles + LCP array) of the workload, inputs
-resident in HBM.  Default workload: BASELINE.json configs[1] (C2, 2^24 DNA
-reads of length 100, seed 1).  Prints ONE JSON line on rank 0.
+resident in HBM.  Default workload: BASELINE.json configs[4] (C5, 2^28
+unique strings of 32-200 characters, 31.4 GB -- the configuration the metric
+is quoted on "at 1/2/4/8 B200", and the largest that fits one GPU), generated
+on the device by the counter-based generator (csrc/s5g_gen.cu; the host copy
+for the e2e and CPU legs is read back once).  Prints ONE JSON line on rank 0.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2_dna]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5_nodup]
   python bench.py --impl reference ...   # CPU S^5 (oracle port), all host cores
 
-The arena (1.69 GB at C2) is larger than the 126 MB L2, so no explicit L2
-flush is needed between timed steps.
+The arena (31.4 GB at C5, 1.69 GB at C2) is larger than the 126 MB L2, so no
+explicit L2 flush is needed between timed steps.
 """
 
 from __future__ import annotations
@@ -36,6 +39,7 @@ FALLBACK_HBM = 6650.0  # GB/s, B200_PROFILING.md fallback
 
 
 TRAFFIC = ROOT / "profiles" / "r01i_traffic.json"
+PASS_BYTES = 24  # algorithmic bytes per string per distribution pass
 
 
 def ncu_traffic(kernel: str):
@@ -195,10 +199,46 @@ def cpu_reference(buf, hnd, sample_n: int, reps: int, threads: int):
     return len(shnd) / statistics.median(times), times
 
 
-def load_config(name: str, scale: float):
+def config_n(name: str, scale: float) -> int:
+    base = {"c1_random": 1_000_000, "c2_dna": 1 << 24, "c3_urls": 1 << 23,
+            "c4_suffixes": 1 << 24, "c5_nodup": 1 << 28}[name]
+    return int(base * scale)
+
+
+def load_config(name: str, scale: float, pinned: bool = False):
+    """Host copy (buffer, handles) of the workload; C5 is generated on all
+    host cores (optionally straight into pinned memory)."""
     from paper_1403_2056_b200 import corpora
 
+    if name == "c5_nodup":
+        n = config_n(name, scale)
+        out = None
+        if pinned:
+            import torch
+
+            out = torch.empty(corpora.nodup_bytes(n), dtype=torch.uint8,
+                              pin_memory=True).numpy()
+        return corpora.gen_nodup(n, 4, out=out)
     return corpora.CONFIGS[name](scale)
+
+
+def load_device(name: str, scale: float, dev):
+    """(DeviceStrings, host buffer, host handles, buffer pinned?): C5 is generated in HBM
+    and read back once into pinned host memory (the e2e and CPU legs' copy);
+    the other configs are generated on the host and uploaded."""
+    import torch
+
+    from paper_1403_2056_b200 import corpora
+    from paper_1403_2056_b200 import device as DV
+
+    if name == "c5_nodup":
+        arena, alen, h = corpora.gen_nodup_device(config_n(name, scale), 4, dev)
+        buf = torch.empty(alen, dtype=torch.uint8, pin_memory=True)
+        buf.copy_(arena[:alen])
+        hnd = h.cpu().numpy()
+        return DV.DeviceStrings(arena, alen, h), buf.numpy(), hnd, True
+    buf, hnd = corpora.CONFIGS[name](scale)
+    return DV.upload(buf, hnd, dev), buf, hnd, False
 
 
 def dist_env():
@@ -215,8 +255,12 @@ def run_reference(args):
     threads = os.cpu_count() or 1
     buf, hnd = load_config(args.config, args.scale)
     n = len(hnd)
-    sample = min(n, args.cpu_sample)
-    for _ in range(args.warmup):
+    sample = min(n, args.cpu_sample) if args.cpu_sample > 0 else n
+    # the CPU needs no clock / cache warm-up beyond one pass (a full C5 sort
+    # takes ~10 s on 16 threads): min(W, 1) untimed passes keep the run at a
+    # few minutes
+    cpu_warm = min(args.warmup, 1)
+    for _ in range(cpu_warm):
         cpu_reference(buf, hnd, sample, 1, threads)
     rate, times = cpu_reference(buf, hnd, sample, args.steps, threads)
     total = sum(times)
@@ -226,9 +270,11 @@ def run_reference(args):
         "ms_per_step": 1000 * total / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
         "config": {"workload": args.config, "n": n, "scale": args.scale,
-                   "sample_strings": sample, "parallelism": f"cpu{threads}"},
+                   "sample_strings": sample, "parallelism": f"cpu{threads}",
+                   "cpu_warmup_passes": cpu_warm},
         "cpu_baseline": {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"first {sample} strings of {args.config} "
+                         "sample": (f"all {n} strings" if sample == n else
+                                    f"first {sample} strings") + f" of {args.config} "
                                    f"(oracle/s5_oracle.c parallel_s5, {threads} OpenMP threads, "
                                    f"{cpu_model()})"},
         "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -334,20 +380,20 @@ def run_ours(args):
         torch.cuda.set_device(local)
         dist.init_process_group("nccl")
     dev = torch.device("cuda", torch.cuda.current_device())
-    buf, hnd = load_config(args.config, args.scale)
+    ds, buf, hnd, pinned = load_device(args.config, args.scale, dev)
     n = len(hnd)
     threads = os.cpu_count() or 1
 
     cpu_line = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        sample = min(n, args.cpu_sample)
+        sample = min(n, args.cpu_sample) if args.cpu_sample > 0 else n
         rate, times = cpu_reference(buf, hnd, sample, 1, threads)
         cpu_line = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
-                    "sample": f"first {sample} strings of {args.config}, 1 rep, "
+                    "sample": (f"all {n} strings" if sample == n else f"first {sample} strings")
+                              + f" of {args.config}, 1 rep, "
                               f"{times[0]:.2f} s (oracle/s5_oracle.c parallel_s5, "
                               f"{threads} OpenMP threads, {cpu_model()})"}
 
-    ds = DV.upload(buf, hnd, dev)
     ws = torch.empty(DV.workspace_bytes(n, 1 << 20), dtype=torch.uint8, device=dev)
     out = (torch.empty(n, dtype=torch.int64, device=dev),
            torch.empty(n, dtype=torch.int64, device=dev))
@@ -398,32 +444,50 @@ def run_ours(args):
     total_strings = n * world
     value = total_strings / (ms_step / 1000.0)
 
-    # end to end through the public C ABI on pinned host buffers
+    # end to end through the reference-facing call: s5_sort(sset, want_lcps=True)
+    # on a string set whose buffer and handles sit in pinned host memory; the
+    # library copies them in (s5g_sort_host), sorts, and copies the handles
+    # and LCPs back into new host arrays -- all inside the timed region
     e2e = None
     if not args.no_e2e:
-        pin_buf = torch.empty(len(buf), dtype=torch.uint8, pin_memory=True)
-        pin_buf.numpy()[:] = buf
+        from paper_1403_2056_b200 import ssss
+        from paper_1403_2056_b200.strset import StringSet
+
+        ref_h = out[0].cpu().numpy()
+        del ds, ws, out
+        torch.cuda.empty_cache()
+        if not pinned:
+            pin_buf = torch.empty(len(buf), dtype=torch.uint8, pin_memory=True)
+            pin_buf.numpy()[:] = buf
+            buf = pin_buf.numpy()
         pin_h = torch.empty(n, dtype=torch.int64, pin_memory=True)
         pin_h.numpy()[:] = hnd
-        pin_oh = torch.empty(n, dtype=torch.int64, pin_memory=True).numpy()
-        pin_ol = torch.empty(n, dtype=torch.int64, pin_memory=True).numpy()
-        bnp, hnp = pin_buf.numpy(), pin_h.numpy()
-        DV.sort_host(bnp, hnp, out_handles=pin_oh, out_lcps=pin_ol)  # warm-up
+        sset = StringSet(buf, pin_h.numpy())
+        res = ssss.s5_sort(sset, want_lcps=True)  # warm-up (device pool, staging ring)
         ts = []
         for _ in range(max(1, min(args.steps, 3))):
             t0 = time.perf_counter()
-            DV.sort_host(bnp, hnp, out_handles=pin_oh, out_lcps=pin_ol)
+            res = ssss.s5_sort(sset, want_lcps=True)
             ts.append(time.perf_counter() - t0)
-        assert np.array_equal(pin_oh, out[0].cpu().numpy())
+        assert np.array_equal(res.set.handles, ref_h)
+        del res
+        _lib.lib().s5g_release_cached_memory()
         e2e = {"value": n / statistics.median(ts), "unit": UNIT,
                "h2d_bytes_per_step": int(len(buf) + 8 * n),
-               "d2h_bytes_per_step": int(16 * n), "ms_per_step": 1000 * statistics.median(ts)}
+               "d2h_bytes_per_step": int(16 * n), "ms_per_step": 1000 * statistics.median(ts),
+               "call": "paper_1403_2056_b200.s5_sort(sset, want_lcps=True) -> s5g_sort_host, "
+                       "buffer + handles in pinned host memory, outputs to new numpy arrays"}
 
     peak, peak_src = hbm_peak()
     kernels = {k: v for k, v in prof.items() if v["launches"]}
     top = dominant_kernel(kernels)
     kt = kernels[top]
-    ach = kt["bytes"] / (kt["ms"] / 1000.0) / 1e9 if kt["ms"] > 0 else 0.0
+    # 24 algorithmic bytes per string per distribution pass (the
+    # 8-byte word plus the 8-byte handle read and written); the kernel's own
+    # record model (DESIGN.md kernel table) is reported beside it
+    alg_bytes = PASS_BYTES * kt["units"]
+    ach = alg_bytes / (kt["ms"] / 1000.0) / 1e9 if kt["ms"] > 0 else 0.0
+    ach_rec = kt["bytes"] / (kt["ms"] / 1000.0) / 1e9 if kt["ms"] > 0 else 0.0
     sort_gbs = b_alg(n, D) / (ms_step / 1000.0) / 1e9
     step_ms_sum = sum(v["ms"] for v in kernels.values()) / args.steps
     line = {
@@ -438,9 +502,14 @@ def run_ours(args):
         "d_bytes_per_s": D * world / (ms_step / 1000.0),
         "roofline": {"bound": "hbm", "kernel": top, "achieved": ach, "peak": peak,
                      "unit": "GB/s", "frac": ach / peak, "traffic": ncu_traffic(top),
-                     "algorithmic_bytes_per_launch": kt["bytes"] / max(1, kt["launches"]),
+                     "algorithmic_bytes_per_launch": alg_bytes / max(1, kt["launches"]),
+                     "bytes_model": f"{PASS_BYTES} B per string (SURVEY 8d)",
                      "peak_source": peak_src,
-                     "share_of_step": kt["ms"] / args.steps / ms_step},
+                     "share_of_step": kt["ms"] / args.steps / ms_step,
+                     "record_model": {"achieved": ach_rec, "frac": ach_rec / peak,
+                                      "bytes_per_launch": kt["bytes"] / max(1, kt["launches"]),
+                                      "model": "the kernel's own record traffic model "
+                                               "(DESIGN.md kernel table)"}},
         "issue_roofline": issue_roofline(
             top, kt["ms"] / max(1, kt["launches"]), (clk.summary() or {}).get("sm_mhz") or 0,
             torch.cuda.get_device_properties(dev).multi_processor_count),
@@ -471,9 +540,10 @@ def main(argv=None):
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", default="c2_dna")
+    ap.add_argument("--config", default="c5_nodup")
     ap.add_argument("--scale", type=float, default=1.0)
-    ap.add_argument("--cpu-sample", type=int, default=1 << 22)
+    ap.add_argument("--cpu-sample", type=int, default=0,
+                    help="strings the CPU legs sort (prefix; 0 = the whole workload)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--l2-fetch", type=int, default=32)

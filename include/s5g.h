@@ -14,6 +14,10 @@
  *  - Return 0 on success, a negative S5G_E* code on failure; the message is
  *    in s5g_last_error() (thread-local).
  *  - Calls are synchronous: all work is complete when they return.
+ *  - Threading: any host thread may call any entry point.  Sorts on the
+ *    same device are serialised inside the library (they share the
+ *    device's side streams, events and staging buffers); sorts on different
+ *    devices run concurrently.  Errors are reported per thread.
  *  - Arena: 0-terminated strings back to back; every handle h satisfies
  *    0 <= h < arena_len and the string at h ends at a 0 byte.  The arena
  *    pointer must be 8-byte aligned and readable for S5G_ARENA_PAD bytes
@@ -89,11 +93,17 @@ size_t s5g_workspace_bytes(int64_t n, int64_t t_medium);
 /* Sort on HOST buffers (copies in, sorts, copies out; device memory is
  * managed internally).  This is the reference-facing end-to-end call:
  * s5_sort(sset, want_lcps=...) with sset.buffer/handles in host memory.
- * out_lcps / out_dchar may be NULL. */
+ * out_lcps / out_dchar may be NULL.  Page-locked buffers are copied by DMA
+ * directly; pageable ones through a pinned staging ring filled by all host
+ * threads.  Device memory comes from a library-owned pool (the device's
+ * default pool is left alone) that keeps it between calls. */
 int s5g_sort_host(const uint8_t *arena, int64_t arena_len, const int64_t *handles, int64_t n,
                   int64_t depth, int64_t *out_handles, int64_t *out_lcps, uint8_t *out_dchar,
                   int32_t variant, int32_t v, uint64_t seed, int64_t t_medium,
                   s5g_stats *stats);
+
+/* Return the device memory s5g_sort_host keeps cached between calls. */
+void s5g_release_cached_memory(void);
 
 /* --- kernel-level entry points (parity tests of single rows of the path) --- */
 

@@ -826,6 +826,52 @@ static int cmp_pair(const void *a, const void *b)
  * content and out_lcps (nullable) is its exact LCP array.
  * report[0] = status (0 ok, 1 not a permutation, 2 order violated,
  * 3 stability violated, 4 lcp mismatch), report[1] = first bad index. */
+/* Stable parallel LSD radix sort of pairs by key (keys >= 0): the pairs
+ * start in idx order, so equal keys stay in increasing idx order -- the
+ * order cmp_pair gives. */
+static void radix_pairs(pair_t *a, int64_t n)
+{
+    if (n < 2) return;
+    int64_t mx = 0;
+    #pragma omp parallel for reduction(max : mx)
+    for (int64_t i = 0; i < n; i++) if (a[i].key > mx) mx = a[i].key;
+    int bits = 0;
+    while (bits < 63 && (mx >> bits)) bits++;
+    pair_t *b = malloc(n * sizeof(pair_t));
+    const int R = 11, B = 1 << R;
+    int T = omp_get_max_threads();
+    int64_t *cnt = malloc((size_t)T * B * sizeof(int64_t));
+    for (int sh = 0; sh < bits; sh += R) {
+        #pragma omp parallel num_threads(T)
+        {
+            int t = omp_get_thread_num(), nt = omp_get_num_threads();
+            int64_t lo = n * t / nt, hi = n * (t + 1) / nt;
+            int64_t *c = cnt + (size_t)t * B;
+            memset(c, 0, B * sizeof(int64_t));
+            for (int64_t i = lo; i < hi; i++) c[(a[i].key >> sh) & (B - 1)]++;
+            #pragma omp barrier
+            #pragma omp single
+            {
+                int64_t run = 0;
+                for (int d = 0; d < B; d++)
+                    for (int u = 0; u < nt; u++) {
+                        int64_t x = cnt[(size_t)u * B + d];
+                        cnt[(size_t)u * B + d] = run;
+                        run += x;
+                    }
+            }
+            for (int64_t i = lo; i < hi; i++) b[c[(a[i].key >> sh) & (B - 1)]++] = a[i];
+        }
+        memcpy(a, b, n * sizeof(pair_t));
+    }
+    free(cnt);
+    free(b);
+}
+
+/* K11 certificate: verify (strset.py:250-281) -- the output is a
+ * permutation of the input handles in non-descending content order --, plus
+ * stability of equal strings and the exact LCP array (lcp_array_oracle,
+ * strset.py:220-240).  O(n + L) string work, all host threads. */
 int s5o_certify(const uint8_t *buf, const int64_t *in_handles, const int64_t *out_handles,
                 const int64_t *out_lcps, int64_t n, int64_t *report)
 {
@@ -835,32 +881,59 @@ int s5o_certify(const uint8_t *buf, const int64_t *in_handles, const int64_t *ou
     /* input position of every output element (duplicate handles are
      * matched in increasing order, the favourable assignment) */
     pair_t *in = malloc(n * sizeof(pair_t)), *out = malloc(n * sizeof(pair_t));
+    #pragma omp parallel for
     for (int64_t i = 0; i < n; i++) {
         in[i] = (pair_t){in_handles[i], i};
         out[i] = (pair_t){out_handles[i], i};
     }
-    qsort(in, n, sizeof(pair_t), cmp_pair);
-    qsort(out, n, sizeof(pair_t), cmp_pair);
+    int neg = 0;
+    #pragma omp parallel for reduction(| : neg)
+    for (int64_t i = 0; i < n; i++) neg |= in[i].key < 0 || out[i].key < 0;
+    if (neg) {
+        qsort(in, n, sizeof(pair_t), cmp_pair);
+        qsort(out, n, sizeof(pair_t), cmp_pair);
+    } else {
+        radix_pairs(in, n);
+        radix_pairs(out, n);
+    }
     int64_t *inpos = malloc(n * sizeof(int64_t));
+    int64_t bad = INT64_MAX;
+    #pragma omp parallel for reduction(min : bad)
     for (int64_t i = 0; i < n; i++) {
-        if (in[i].key != out[i].key) {
-            report[0] = 1; report[1] = out[i].idx;
-            free(in); free(out); free(inpos);
-            return 1;
-        }
+        if (in[i].key != out[i].key) { if (i < bad) bad = i; continue; }
         inpos[out[i].idx] = in[i].idx;
+    }
+    if (bad != INT64_MAX) {
+        report[0] = 1; report[1] = out[bad].idx;
+        free(in); free(out); free(inpos);
+        return 1;
     }
     free(in);
     free(out);
-    if (out_lcps && out_lcps[0] != LCP_UNDEF) { report[0] = 4; report[1] = 0; }
-    for (int64_t i = 1; i < n && report[0] == 0; i++) {
-        int64_t a = out_handles[i - 1], b = out_handles[i];
-        int64_t h = s5o_lcp(buf, a, b);
-        uint8_t ca = buf[a + h], cb = buf[b + h];
-        if (ca > cb) { report[0] = 2; report[1] = i; break; }
-        if (ca == cb && a != b && inpos[i - 1] > inpos[i]) { report[0] = 3; report[1] = i; break; }
-        if (out_lcps && out_lcps[i] != h) { report[0] = 4; report[1] = i; break; }
+    if (out_lcps && out_lcps[0] != LCP_UNDEF) { report[0] = 4; report[1] = 0; free(inpos); return 4; }
+    /* first failing adjacent pair (smallest i), found by all threads */
+    int64_t first = INT64_MAX;
+    int code_at_first = 0;
+    #pragma omp parallel
+    {
+        int64_t my = INT64_MAX;
+        int mycode = 0;
+        #pragma omp for schedule(static)
+        for (int64_t i = 1; i < n; i++) {
+            if (i >= my) continue;
+            int64_t a = out_handles[i - 1], b = out_handles[i];
+            int64_t h = s5o_lcp(buf, a, b);
+            uint8_t ca = buf[a + h], cb = buf[b + h];
+            int code = 0;
+            if (ca > cb) code = 2;
+            else if (ca == cb && a != b && inpos[i - 1] > inpos[i]) code = 3;
+            else if (out_lcps && out_lcps[i] != h) code = 4;
+            if (code && i < my) { my = i; mycode = code; }
+        }
+        #pragma omp critical
+        if (my < first) { first = my; code_at_first = mycode; }
     }
+    if (first != INT64_MAX) { report[0] = code_at_first; report[1] = first; }
     free(inpos);
     return (int)report[0];
 }

@@ -56,6 +56,7 @@ SIGNATURES = {
     "s5g_workspace_bytes": (C.c_size_t, [_i64, _i64]),
     "s5g_sort_host": (C.c_int, [_p, _i64, _p, _i64, _i64, _p, _p, _p, _i32, _i32, _u64, _i64,
                                 C.POINTER(Stats)]),
+    "s5g_release_cached_memory": (None, []),
     "s5g_extract_keys": (C.c_int, [_p, _i64, _p, _i64, _i64, _p, _p]),
     "s5g_select_splitters": (C.c_int, [_p, _i64, _i64, _p, _p, _p, _p, _p]),
     "s5g_classify": (C.c_int, [_p, _i64, _p, _p, _i64, _i32, _p, _p]),

@@ -12,7 +12,8 @@ sizes and value distributions BASELINE.json names:
   C4  suffixes : all 2^24 suffixes of an order-2 Markov text over a-z with
                  5% of the text overwritten by copies of earlier 1-4 KB blocks
   C5  nodup    : n = 2^28, lengths U[32,200]: 16-char prefix from a 2^16-word
-                 vocabulary + lowercase filler + unique 6-char base-36 counter
+                 vocabulary + lowercase filler + unique 6-char base-36 counter;
+                 counter-based (csrc/s5g_gen.cu), host and device generators
 
 Every generator returns (buffer: np.ndarray[uint8], handles: np.ndarray[int64]).
 """
@@ -163,36 +164,78 @@ def gen_suffix_markov(n: int = 1 << 24, seed: int = 3, copy_frac: float = 0.05,
     return buf, np.arange(n, dtype=np.int64)
 
 
-def gen_nodup(n: int = 1 << 28, seed: int = 4, vocab: int = 1 << 16):
-    """C5: unique strings, lengths U[32,200]: 16-char vocabulary prefix,
-    lowercase filler, 6-char base-36 counter (36^6 > 2^28 keeps them unique)."""
-    rng = np.random.default_rng(seed)
-    words = ALPHA[rng.integers(0, 26, size=(vocab, 16))]
-    lens = rng.integers(32, 201, size=n).astype(np.int64)
-    offsets = np.zeros(n, dtype=np.int64)
-    np.cumsum(lens[:-1] + 1, out=offsets[1:])
-    buf = np.zeros(int(lens.sum()) + n, dtype=np.uint8)
-    CH = 1 << 20
-    for lo in range(0, n, CH):
-        hi = min(n, lo + CH)
-        m = hi - lo
-        L = lens[lo:hi]
-        off = offsets[lo:hi] - offsets[lo]
-        seg = np.zeros(int(L.sum()) + m, dtype=np.uint8)
-        fill = ALPHA[rng.integers(0, 26, size=len(seg), dtype=np.uint8)]
-        mask = np.ones(len(seg), dtype=bool)
-        mask[off + L] = False
-        seg[mask] = fill[mask]
-        w = words[rng.integers(0, vocab, size=m)]
-        seg[(off[:, None] + np.arange(16)).reshape(-1)] = w.reshape(-1)
-        cnt = np.arange(lo, hi, dtype=np.int64)
-        digits = np.empty((m, 6), dtype=np.uint8)
-        for j in range(5, -1, -1):
-            digits[:, j] = B36[cnt % 36]
-            cnt //= 36
-        seg[(off[:, None] + (L - 6)[:, None] + np.arange(6)).reshape(-1)] = digits.reshape(-1)
-        buf[offsets[lo]: offsets[lo] + len(seg)] = seg
-    return buf, offsets
+_gen_lib = None
+
+
+def _gen():
+    """libs5gen.so (csrc/s5g_gen.cu): the counter-based C5 generator."""
+    global _gen_lib
+    if _gen_lib is None:
+        import ctypes as C
+
+        from .build import GEN_PATH
+
+        if not GEN_PATH.exists():
+            raise ImportError(f"{GEN_PATH} is missing: build it with "
+                              "`python -m paper_1403_2056_b200.build`")
+        L = C.CDLL(str(GEN_PATH))
+        i64, u64, p = C.c_int64, C.c_uint64, C.c_void_p
+        L.s5gen_nodup_bytes.restype = i64
+        L.s5gen_nodup_bytes.argtypes = [i64, i64, u64]
+        L.s5gen_nodup_host.restype = C.c_int
+        L.s5gen_nodup_host.argtypes = [i64, i64, u64, p, p]
+        L.s5gen_nodup_device.restype = C.c_int
+        L.s5gen_nodup_device.argtypes = [i64, i64, u64, p, p, p]
+        L.s5gen_last_error.restype = C.c_char_p
+        _gen_lib = L
+    return _gen_lib
+
+
+def _gen_check(rc: int) -> None:
+    if rc != 0:
+        raise RuntimeError("s5gen: " + _gen().s5gen_last_error().decode())
+
+
+def nodup_bytes(n: int, seed: int = 4) -> int:
+    """Arena length (terminators included) of the first n C5 strings."""
+    return int(_gen().s5gen_nodup_bytes(0, n, seed))
+
+
+def gen_nodup(n: int = 1 << 28, seed: int = 4, out: np.ndarray | None = None):
+    """C5: unique strings, lengths U[32,200]: 16-char prefix from a 2^16-word
+    vocabulary, lowercase filler, 6-char base-36 counter (36^6 > 2^28 keeps
+    them unique).  Counter-based (csrc/s5g_gen.cu): every byte is a function
+    of (seed, string index, position), so gen_nodup(m) is a prefix of
+    gen_nodup(n) for m <= n and gen_nodup_device writes the same bytes.
+    Generated on all host cores (OpenMP); `out` (uint8, >= nodup_bytes(n))
+    may be a pinned buffer."""
+    total = nodup_bytes(n, seed)
+    buf = out[:total] if out is not None else np.empty(total, dtype=np.uint8)
+    assert buf.dtype == np.uint8 and buf.size == total and buf.flags.c_contiguous
+    hnd = np.empty(n, dtype=np.int64)
+    _gen_check(_gen().s5gen_nodup_host(0, n, seed, buf.ctypes.data if total else None,
+                                       hnd.ctypes.data if n else None))
+    return buf, hnd
+
+
+def gen_nodup_device(n: int = 1 << 28, seed: int = 4, device=None):
+    """C5 generated directly in HBM (same bytes as gen_nodup): returns
+    (arena uint8 tensor padded with zeros past arena_len, arena_len, handles
+    int64 tensor) -- the device.DeviceStrings fields."""
+    import torch
+
+    from ._lib import S5G_ARENA_PAD
+
+    dev = device or torch.device("cuda", torch.cuda.current_device())
+    total = nodup_bytes(n, seed)
+    cap = (total + S5G_ARENA_PAD + 15) // 16 * 16
+    arena = torch.empty(cap, dtype=torch.uint8, device=dev)
+    arena[total:].zero_()
+    hnd = torch.empty(max(n, 1), dtype=torch.int64, device=dev)[:n]
+    with torch.cuda.device(dev):
+        st = torch.cuda.current_stream(dev).cuda_stream
+        _gen_check(_gen().s5gen_nodup_device(0, n, seed, arena.data_ptr(), hnd.data_ptr(), st))
+    return arena, total, hnd
 
 
 CONFIGS = {

@@ -7,8 +7,12 @@
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
+#include <omp.h>
+
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
+#include <mutex>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -1077,8 +1081,14 @@ __global__ void k_single(const int64_t* __restrict__ handles, int64_t* __restric
 // host side
 
 static thread_local std::string g_err;
-static size_t g_l2_fetch = 32;  // s5g_set_l2_fetch_granularity
-static int g_sms = 148;         // multiprocessors of the current device
+static std::atomic<size_t> g_l2_fetch{32};  // s5g_set_l2_fetch_granularity
+static thread_local int g_sms = 148;        // multiprocessors of the current device
+// Threading contract (s5g.h): sorts on one device are serialised by its
+// mutex (they share the device's side streams, events and staging buffers);
+// sorts on different devices run concurrently.
+constexpr int MAX_DEV = 64;
+static std::mutex g_dev_mu[MAX_DEV];
+static std::mutex g_prof_mu;  // profile table + timeline
 
 // ---- live per-kernel timing (CUDA events on the launching stream) --------
 enum KernelId { K_INIT, K_SAMPLE, K_CLASSIFY, K_SCAN_COLS, K_SCAN_BUCKETS, K_SCATTER, K_SEG_WARP,
@@ -1104,7 +1114,7 @@ struct TimelineEntry {
 };
 static std::vector<TimelineEntry> g_timeline;
 static cudaEvent_t g_tl_base = nullptr;
-static unsigned long long g_launches = 0;
+static std::atomic<unsigned long long> g_launches{0};
 
 struct Profiler {
     cudaStream_t st;
@@ -1113,7 +1123,7 @@ struct Profiler {
     std::vector<long long> units, bytes;
     explicit Profiler(cudaStream_t s, int id = 0) : st(s), sid(id) {}
     static std::vector<cudaEvent_t>& pool() {
-        static std::vector<cudaEvent_t> p;
+        static thread_local std::vector<cudaEvent_t> p;
         return p;
     }
     static cudaEvent_t take() {
@@ -1150,6 +1160,7 @@ struct Profiler {
     }
     // call after the stream is synchronized
     void flush() {
+        std::lock_guard<std::mutex> lk(g_prof_mu);
         for (size_t i = 0; i < ev.size(); i++) {
             float ms = 0;
             cudaEventElapsedTime(&ms, ev[i].second.first, ev[i].second.second);
@@ -1290,6 +1301,8 @@ static constexpr size_t SMEM_SC = (size_t)(NBMAX + 1) * 5;
 static int set_smem_attrs() {
     // per device: kernel attributes + the byte-PEXT table of the finishers
     static unsigned long long done_mask = 0;
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lk(mu);
     int dev = 0;
     CK(cudaGetDevice(&dev));
     CK(cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev));
@@ -1371,16 +1384,26 @@ struct Staging {
         return p;
     }
 };
-static Staging g_stage_up, g_stage_down;
+static Staging g_stage_up[MAX_DEV], g_stage_down[MAX_DEV];
 
-static int sort_impl_body(const s5g_sort_args* a);
+static int sort_impl_body(const s5g_sort_args* a, int dev_id);
 
 static int sort_impl(const s5g_sort_args* a) {
+    // argument errors are reported without touching the device
+    if (a->n < 0 || a->arena_len < 0) return fail(S5G_E_INVALID, "negative size");
+    if (a->variant != S5G_VARIANT_UNROLL && a->variant != S5G_VARIANT_EQUAL)
+        return fail(S5G_E_VARIANT, "unknown classify variant");
+    if (a->n > INT32_MAX) return fail(S5G_E_INVALID, "n exceeds 2^31-1");
+    if (a->n == 0) return 0;
+    int dev_id = 0;
+    CK(cudaGetDevice(&dev_id));
+    if (dev_id >= MAX_DEV) return fail(S5G_E_INVALID, "device id >= 64");
+    std::lock_guard<std::mutex> lk(g_dev_mu[dev_id]);
     L2Granularity l2g(g_l2_fetch);
-    return sort_impl_body(a);
+    return sort_impl_body(a, dev_id);
 }
 
-static int sort_impl_body(const s5g_sort_args* a) {
+static int sort_impl_body(const s5g_sort_args* a, int dev_id) {
     const int64_t n = a->n;
     cudaStream_t st = (cudaStream_t)a->stream;
     if (n < 0 || a->arena_len < 0) return fail(S5G_E_INVALID, "negative size");
@@ -1428,12 +1451,10 @@ static int sort_impl_body(const s5g_sort_args* a) {
     // there concurrently with the next round's device-wide step
     // and a high-priority stream for the root step's sample, drawn from the
     // input while k_init copies it (its one CTA is scheduled first)
-    static cudaStream_t s_st2[64], s_hi[64], s_pool[64][3];
-    static cudaEvent_t s_fork[64], s_join[64], s_samp[64], s_pfork[64], s_pjoin[64][3];
-    int dev_id = 0;
-    CK(cudaGetDevice(&dev_id));
-    if (dev_id >= 64) return fail(S5G_E_INVALID, "device id >= 64");
-    if (!s_st2[dev_id]) {
+    static cudaStream_t s_st2[MAX_DEV], s_hi[MAX_DEV], s_pool[MAX_DEV][3];
+    static cudaEvent_t s_fork[MAX_DEV], s_join[MAX_DEV], s_samp[MAX_DEV], s_pfork[MAX_DEV],
+        s_pjoin[MAX_DEV][3];
+    if (!s_st2[dev_id]) {  // created under the device's mutex
         int lo_prio = 0, hi_prio = 0;
         CK(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
         CK(cudaStreamCreateWithFlags(&s_st2[dev_id], cudaStreamNonBlocking));
@@ -1628,6 +1649,7 @@ static int sort_impl_body(const s5g_sort_args* a) {
         int64_t cnt_off = 0, bk_off = 0, tree_off = 0, tile0 = 0;
         size_t i0 = 0;
         // a round may be split into batches when it exceeds the capacities
+        int batch = 0;
         while (i0 < large.size()) {
             steps.clear();
             tile_step.clear();
@@ -1691,11 +1713,13 @@ static int sort_impl_body(const s5g_sort_args* a) {
             }
             n_jobs += nsteps;
             {
-                // previous round's uploads are complete: this round began after
-                // a stream sync, so the staging buffer can be reused
+                // the first batch of a round follows the round's stream sync;
+                // later batches must wait for the previous batch's upload
+                // before the staging buffer is rewritten (or reallocated)
+                if (batch++) CK(cudaStreamSynchronize(st));
                 const size_t b1 = sizeof(StepDev) * nsteps, b2 = 4 * tile_step.size(),
                              b3 = 4 * cblk_step.size(), b4 = 4 * sblk_step.size();
-                uint8_t* up = (uint8_t*)g_stage_up.get(b1 + b2 + b3 + b4);
+                uint8_t* up = (uint8_t*)g_stage_up[dev_id].get(b1 + b2 + b3 + b4);
                 if (!up) return fail(S5G_E_CUDA, "cudaMallocHost failed");
                 memcpy(up, steps.data(), b1);
                 memcpy(up + b1, tile_step.data(), b2);
@@ -1789,7 +1813,7 @@ static int sort_impl_body(const s5g_sort_args* a) {
         {
             // counters + a speculative prefix of the next round's list in one sync
             const int64_t spec = std::min<int64_t>(w.steps_cap, 4096);
-            uint8_t* down = (uint8_t*)g_stage_down.get(sizeof(Counters) + sizeof(SegDev) * spec);
+            uint8_t* down = (uint8_t*)g_stage_down[dev_id].get(sizeof(Counters) + sizeof(SegDev) * spec);
             if (!down) return fail(S5G_E_CUDA, "cudaMallocHost failed");
             SegDev* dl = reinterpret_cast<SegDev*>(down + sizeof(Counters));
             CK(cudaMemcpyAsync(down, w.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
@@ -1854,6 +1878,98 @@ static int sort_impl_body(const s5g_sort_args* a) {
     }
     return 0;
 }
+
+// ---- host-buffer entry (s5g_sort_host) ----------------------------------
+// Device buffers come from a library-owned memory pool (never the device's
+// default pool, whose attributes belong to the caller / PyTorch): it keeps
+// its memory between calls, s5g_release_cached_memory() trims it.  Host
+// buffers that are page-locked (cudaHostAlloc / cudaHostRegister) are copied
+// directly; pageable ones go through a ring of pinned staging chunks, filled
+// and drained by all host threads (OpenMP) while the DMA of the previous
+// chunk runs, so a pageable `bytes` buffer moves at close to the PCIe rate.
+struct HostCtx {
+    static constexpr int NSLOT = 4;
+    static constexpr size_t CHUNK = size_t(64) << 20;
+    std::mutex mu;
+    cudaMemPool_t pool = nullptr;
+    cudaStream_t st = nullptr;
+    uint8_t* slot[NSLOT] = {};
+    cudaEvent_t ev[NSLOT] = {};
+    int init(int dev) {
+        if (pool) return 0;
+        cudaMemPoolProps props{};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = dev;
+        CK(cudaMemPoolCreate(&pool, &props));
+        uint64_t thr = UINT64_MAX;
+        CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+        CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        return 0;
+    }
+    cudaError_t ring() {
+        if (slot[0]) return cudaSuccess;
+        for (int k = 0; k < NSLOT; k++) {
+            cudaError_t e = cudaHostAlloc((void**)&slot[k], CHUNK, cudaHostAllocPortable);
+            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev[k], cudaEventDisableTiming);
+            if (e != cudaSuccess) return e;
+        }
+        return cudaSuccess;
+    }
+    static bool pinned(const void* p) {
+        cudaPointerAttributes at{};
+        const bool ok = cudaPointerGetAttributes(&at, p) == cudaSuccess;
+        cudaGetLastError();
+        return ok && at.type == cudaMemoryTypeHost;
+    }
+    static void par_copy(void* dst, const void* src, size_t bytes) {
+        const int64_t parts = (int64_t)std::min<size_t>(64, (bytes + (1 << 20) - 1) >> 20);
+#pragma omp parallel for schedule(static)
+        for (int64_t q = 0; q < parts; q++) {
+            const size_t lo = bytes * q / parts, hi = bytes * (q + 1) / parts;
+            memcpy((uint8_t*)dst + lo, (const uint8_t*)src + lo, hi - lo);
+        }
+    }
+    cudaError_t h2d(void* dst, const void* src, size_t bytes) {
+        if (!bytes) return cudaSuccess;
+        if (pinned(src)) return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st);
+        cudaError_t e = ring();
+        for (size_t off = 0, c = 0; e == cudaSuccess && off < bytes; off += CHUNK, c++) {
+            const int k = (int)(c % NSLOT);
+            const size_t len = std::min(CHUNK, bytes - off);
+            if (c >= NSLOT) e = cudaEventSynchronize(ev[k]);  // its previous DMA is done
+            if (e != cudaSuccess) break;
+            par_copy(slot[k], (const uint8_t*)src + off, len);
+            e = cudaMemcpyAsync((uint8_t*)dst + off, slot[k], len, cudaMemcpyHostToDevice, st);
+            if (e == cudaSuccess) e = cudaEventRecord(ev[k], st);
+        }
+        return e;
+    }
+    cudaError_t d2h(void* dst, const void* src, size_t bytes) {
+        if (!bytes) return cudaSuccess;
+        if (pinned(dst)) return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st);
+        cudaError_t e = ring();
+        const size_t nc = (bytes + CHUNK - 1) / CHUNK;
+        // DMA chunk c into slot c % NSLOT; drain chunk c - NSLOT + 1 meanwhile
+        for (size_t c = 0; e == cudaSuccess && c < nc + NSLOT - 1; c++) {
+            if (c < nc) {
+                const int k = (int)(c % NSLOT);
+                const size_t off = c * CHUNK, len = std::min(CHUNK, bytes - off);
+                e = cudaMemcpyAsync(slot[k], (const uint8_t*)src + off, len, cudaMemcpyDeviceToHost, st);
+                if (e == cudaSuccess) e = cudaEventRecord(ev[k], st);
+            }
+            if (e == cudaSuccess && c + 1 >= NSLOT) {
+                const size_t d = c + 1 - NSLOT;
+                const int k = (int)(d % NSLOT);
+                const size_t off = d * CHUNK, len = std::min(CHUNK, bytes - off);
+                e = cudaEventSynchronize(ev[k]);
+                if (e == cudaSuccess) par_copy((uint8_t*)dst + off, slot[k], len);
+            }
+        }
+        return e;
+    }
+};
+static HostCtx g_host[MAX_DEV];
 
 }  // namespace s5g
 
@@ -1931,18 +2047,15 @@ int s5g_sort_host(const uint8_t* arena, int64_t arena_len, const int64_t* handle
     if (variant != S5G_VARIANT_UNROLL && variant != S5G_VARIANT_EQUAL)
         return fail(S5G_E_VARIANT, "unknown classify variant");
     if (n == 0) return 0;
-    static bool pool_set = false;
-    if (!pool_set) {
-        int dev = 0;
-        cudaMemPool_t pool;
-        if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-            uint64_t thr = UINT64_MAX;
-            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-        }
-        pool_set = true;
-    }
-    cudaStream_t st;
-    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    if (dev >= MAX_DEV) return fail(S5G_E_INVALID, "device id >= 64");
+    HostCtx& hx = g_host[dev];
+    // one host-buffer sort per device at a time: the staging ring is shared
+    // (the sort itself takes the device mutex inside)
+    std::lock_guard<std::mutex> lk(hx.mu);
+    if (int rc = hx.init(dev)) return rc;
+    cudaStream_t st = hx.st;
     const int64_t tm = t_medium > 0 ? t_medium : (1 << 20);
     size_t ws = s5g_workspace_bytes(n, tm);
     size_t alen_pad = ((size_t)arena_len + S5G_ARENA_PAD + 15) & ~size_t(15);
@@ -1953,7 +2066,6 @@ int s5g_sort_host(const uint8_t* arena, int64_t arena_len, const int64_t* handle
         cudaFreeAsync(d_arena, st); cudaFreeAsync(d_ws, st); cudaFreeAsync(d_h, st);
         cudaFreeAsync(d_out, st); cudaFreeAsync(d_lcp, st); cudaFreeAsync(d_dchar, st);
         cudaStreamSynchronize(st);
-        cudaStreamDestroy(st);
     };
 #define CKH(call)                                                                        \
     do {                                                                                 \
@@ -1964,15 +2076,15 @@ int s5g_sort_host(const uint8_t* arena, int64_t arena_len, const int64_t* handle
             return rc;                                                                   \
         }                                                                                \
     } while (0)
-    CKH(cudaMallocAsync((void**)&d_arena, alen_pad, st));
-    CKH(cudaMallocAsync((void**)&d_ws, ws, st));
-    CKH(cudaMallocAsync((void**)&d_h, 8 * n, st));
-    CKH(cudaMallocAsync((void**)&d_out, 8 * n, st));
-    if (out_lcps || out_dchar) CKH(cudaMallocAsync((void**)&d_lcp, 8 * n, st));
-    if (out_dchar) CKH(cudaMallocAsync((void**)&d_dchar, n, st));
+    CKH(cudaMallocFromPoolAsync((void**)&d_arena, alen_pad, hx.pool, st));
+    CKH(cudaMallocFromPoolAsync((void**)&d_ws, ws, hx.pool, st));
+    CKH(cudaMallocFromPoolAsync((void**)&d_h, 8 * n, hx.pool, st));
+    CKH(cudaMallocFromPoolAsync((void**)&d_out, 8 * n, hx.pool, st));
+    if (out_lcps || out_dchar) CKH(cudaMallocFromPoolAsync((void**)&d_lcp, 8 * n, hx.pool, st));
+    if (out_dchar) CKH(cudaMallocFromPoolAsync((void**)&d_dchar, n, hx.pool, st));
     CKH(cudaMemsetAsync(d_arena + arena_len, 0, alen_pad - arena_len, st));
-    CKH(cudaMemcpyAsync(d_arena, arena, arena_len, cudaMemcpyHostToDevice, st));
-    CKH(cudaMemcpyAsync(d_h, handles, 8 * n, cudaMemcpyHostToDevice, st));
+    CKH(hx.h2d(d_h, handles, 8 * n));
+    CKH(hx.h2d(d_arena, arena, arena_len));
     s5g_sort_args a{};
     a.arena = d_arena; a.arena_len = arena_len; a.handles = d_h; a.n = n; a.depth = depth;
     a.out_handles = d_out; a.out_lcps = d_lcp; a.out_dchar = d_dchar;
@@ -1980,13 +2092,20 @@ int s5g_sort_host(const uint8_t* arena, int64_t arena_len, const int64_t* handle
     a.variant = variant; a.v = v; a.seed = seed; a.t_medium = tm; a.stats = stats;
     rc = sort_impl(&a);
     if (rc) { std::string keep = g_err; cleanup(); g_err = keep; return rc; }
-    CKH(cudaMemcpyAsync(out_handles, d_out, 8 * n, cudaMemcpyDeviceToHost, st));
-    if (out_lcps) CKH(cudaMemcpyAsync(out_lcps, d_lcp, 8 * n, cudaMemcpyDeviceToHost, st));
-    if (out_dchar) CKH(cudaMemcpyAsync(out_dchar, d_dchar, n, cudaMemcpyDeviceToHost, st));
+    CKH(hx.d2h(out_handles, d_out, 8 * n));
+    if (out_lcps) CKH(hx.d2h(out_lcps, d_lcp, 8 * n));
+    if (out_dchar) CKH(hx.d2h(out_dchar, d_dchar, n));
     CKH(cudaStreamSynchronize(st));
     cleanup();
 #undef CKH
     return 0;
+}
+
+void s5g_release_cached_memory(void) {
+    for (int d = 0; d < MAX_DEV; d++) {
+        std::lock_guard<std::mutex> lk(g_host[d].mu);
+        if (g_host[d].pool) cudaMemPoolTrimTo(g_host[d].pool, 0);
+    }
 }
 
 int s5g_extract_keys(const uint8_t* arena, int64_t arena_len, const int64_t* handles, int64_t n,

@@ -179,14 +179,28 @@ def s5_sort(
             return out
         return SortedWithLcp(out, np.zeros(0, dtype=np.int64),
                              np.zeros(0, dtype=np.uint8) if want_dchar else None, stats)
-    ds = D.upload(sset.buffer, handles)
     st = _lib.Stats()
-    hook = _HookAdapter(step_hook) if step_hook is not None else None
+    if step_hook is None:
+        # the end-to-end C-ABI call on the host buffers (s5g_sort_host): the
+        # library copies the (pageable or pinned) buffer in, sorts, copies out
+        arr = sset.buffer if isinstance(sset.buffer, np.ndarray) else \
+            np.frombuffer(sset.buffer, dtype=np.uint8)
+        D._require_cuda()
+        out_h, lcp_h, dchar_h = D.sort_host(arr, handles, depth=depth, want_lcps=want_lcps,
+                                            want_dchar=want_dchar and want_lcps,
+                                            variant=variant, v=v, seed=seed,
+                                            t_medium=t_medium, stats=st)
+        _accumulate(stats, st)
+        out = sset.with_handles(out_h)
+        if not want_lcps:
+            return out
+        return SortedWithLcp(out, lcp_h, dchar_h, stats)
+    ds = D.upload(sset.buffer, handles)
+    hook = _HookAdapter(step_hook)
     out_h, lcps, dchar = D.sort(ds, depth=depth, want_lcps=want_lcps,
                                 want_dchar=want_dchar and want_lcps, variant=variant, v=v,
-                                seed=seed, t_medium=t_medium, stats=st,
-                                step_cb=hook.cb if hook else None)
-    if hook is not None and hook.error is not None:
+                                seed=seed, t_medium=t_medium, stats=st, step_cb=hook.cb)
+    if hook.error is not None:
         raise hook.error
     _accumulate(stats, st)
     out = sset.with_handles(out_h.cpu().numpy())

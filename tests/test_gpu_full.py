@@ -34,11 +34,45 @@ def test_full_size_bit_exact(cfg):
     assert np.array_equal(l, ol)
 
 
-@pytest.mark.parametrize("cfg,scale", [("c4_suffixes", 1.0), ("c5_nodup", 1 / 16)])
+@pytest.mark.parametrize("cfg,scale", [("c4_suffixes", 1.0)])
 def test_full_size_certificate(cfg, scale):
     buf, hnd = corpora.CONFIGS[cfg](scale)
     h, l = gpu_sort(buf, hnd)
     status, bad = oracle.certify(buf, hnd, h, l)
+    assert status == 0, (oracle.CERT_STATUS[status], bad)
+
+
+def test_nodup_device_generator_matches_host():
+    """The bench generates C5 in HBM; its bytes equal the host generator's."""
+    n = 1 << 22
+    arena, alen, h = corpora.gen_nodup_device(n)
+    buf, hnd = corpora.gen_nodup(n)
+    assert alen == len(buf)
+    assert np.array_equal(h.cpu().numpy(), hnd)
+    assert np.array_equal(arena[:alen].cpu().numpy(), buf)
+    assert int(arena[alen:].abs().sum()) == 0  # zero padding past the arena
+
+
+@pytest.mark.parametrize("scale", [1.0])
+def test_c5_full_size_certificate(scale):
+    """BASELINE configs[4] at its stated size -- 2^28 strings, 31.4 GB arena,
+    the workload bench.py measures -- certified by K11 (permutation, order,
+    stability of ties, exact LCP array; the reference's verify,
+    strset.py:250-281, plus lcp_array_oracle, :220-240).  Generated on the
+    device (seconds instead of minutes); the checker reads the host copy."""
+    n = int((1 << 28) * scale)
+    arena, alen, hd = corpora.gen_nodup_device(n)
+    ds = D.DeviceStrings(arena, alen, hd)
+    st = D.Stats()
+    h, l, _ = D.sort(ds, want_lcps=True, stats=st)
+    torch.cuda.synchronize()
+    oh, ol = h.cpu().numpy(), l.cpu().numpy()
+    del h, l
+    buf = arena[:alen].cpu().numpy()
+    hnd = hd.cpu().numpy()
+    del ds, arena, hd
+    torch.cuda.empty_cache()
+    status, bad = oracle.certify(buf, hnd, oh, ol)
     assert status == 0, (oracle.CERT_STATUS[status], bad)
 
 

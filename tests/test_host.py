@@ -72,10 +72,31 @@ def test_corpora_shapes():
     buf, h = corpora.gen_urls(2000, hosts=50, pool=8)
     s = StringSet(buf.tobytes(), h)
     assert all(x.startswith(b"http://") for x in s.strings()[:50])
-    buf, h = corpora.gen_nodup(5000, vocab=64)
+    buf, h = corpora.gen_nodup(5000)
     s = StringSet(buf.tobytes(), h)
     strs = s.strings()
     assert len(set(strs)) == 5000 and all(32 <= len(x) <= 200 for x in strs)
+
+
+def test_nodup_generator_definition():
+    """C5 generator (csrc/s5g_gen.cu): counter-based, so a smaller corpus is a
+    prefix of a larger one; lengths U[32,200]; a base-36 counter suffix; the
+    16-character prefix is one of at most 2^16 vocabulary words."""
+    n = 20000
+    buf, h = corpora.gen_nodup(n)
+    assert len(buf) == corpora.nodup_bytes(n) and h[0] == 0
+    b2, h2 = corpora.gen_nodup(n // 3)
+    assert np.array_equal(h2, h[: n // 3]) and np.array_equal(b2, buf[: len(b2)])
+    strs = StringSet(buf.tobytes(), h).strings()
+    lens = np.array([len(x) for x in strs])
+    assert lens.min() == 32 and lens.max() == 200 and abs(lens.mean() - 116) < 2
+    for i in (0, 1, 35, 36, 12345, n - 1):
+        assert int(strs[i][-6:].decode(), 36) == i
+    assert all(x[:-6].isalpha() and x.islower() for x in strs[:500])
+    prefixes = {x[:16] for x in strs}
+    assert len(prefixes) <= 1 << 16 and len(prefixes) > n * 0.8  # 2^16 words, n << 2^16 draws
+    assert len(set(strs)) == n
+    assert corpora.gen_nodup(1000, seed=5)[0][:64].tobytes() != buf[:64].tobytes()
 
 
 def test_register_with_reference_harness():
