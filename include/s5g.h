@@ -41,7 +41,7 @@ extern "C" {
 #define S5G_E_VARIANT (-2)      /* unknown classify variant (ValueError) */
 #define S5G_E_CUDA (-3)         /* CUDA runtime error */
 #define S5G_E_WORKSPACE (-4)    /* workspace too small */
-#define S5G_E_NCCL (-5)         /* reserved for the multi-GPU exchange */
+#define S5G_E_NCCL (-5)         /* not returned by this version (see s5g_sort_multi) */
 
 #define S5G_VARIANT_UNROLL 0    /* ssss.py:160-169 */
 #define S5G_VARIANT_EQUAL 1     /* ssss.py:170-180 */
@@ -101,6 +101,37 @@ int s5g_sort_host(const uint8_t *arena, int64_t arena_len, const int64_t *handle
                   int64_t depth, int64_t *out_handles, int64_t *out_lcps, uint8_t *out_dchar,
                   int32_t variant, int32_t v, uint64_t seed, int64_t t_medium,
                   s5g_stats *stats);
+
+/* One host process driving several devices: parallel_s5(sset, p)
+ * (parallel.py:468-492) with p = num_devices.  A sample-sort partition with
+ * G-1 string splitters (sampled prefixes, ties by input position) cuts the
+ * output order into G ranges; device k receives the arena, classifies all
+ * strings against the splitters, keeps its range (in input order) and sorts
+ * it; the host fixes the LCP at each part boundary (_boundary_lcps,
+ * parallel.py:447-455).  Buffers are HOST memory as in s5g_sort_host; the
+ * output is identical to a one-device sort.  Device ids must name visible
+ * devices (S5G_E_INVALID otherwise); a device may appear more than once.
+ * The multi-PROCESS form (one process per GPU, NCCL all-to-all over
+ * NVLink) is paper_1403_2056_b200.dist; its collectives run in
+ * torch.distributed, so their errors surface there, not as S5G_E_NCCL. */
+typedef struct s5g_multi_args {
+    const uint8_t *arena;      /* host */
+    int64_t arena_len;
+    const int64_t *handles;    /* host, n */
+    int64_t n;
+    int64_t depth;
+    int64_t *out_handles;      /* host, n */
+    int64_t *out_lcps;         /* host, n, or NULL */
+    uint8_t *out_dchar;        /* host, n, or NULL (needs out_lcps) */
+    int32_t num_devices;       /* p >= 1 */
+    const int32_t *device_ids; /* host, num_devices CUDA device ordinals */
+    int32_t variant;
+    int32_t v;
+    uint64_t seed;
+    int64_t t_medium;
+    s5g_stats *stats;          /* host, accumulated into; may be NULL */
+} s5g_multi_args;
+int s5g_sort_multi(const s5g_multi_args *args);
 
 /* Return the device memory s5g_sort_host keeps cached between calls. */
 void s5g_release_cached_memory(void);

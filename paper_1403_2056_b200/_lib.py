@@ -45,6 +45,16 @@ class SortArgs(C.Structure):
     ]
 
 
+class MultiArgs(C.Structure):
+    _fields_ = [
+        ("arena", _p), ("arena_len", _i64), ("handles", _p), ("n", _i64), ("depth", _i64),
+        ("out_handles", _p), ("out_lcps", _p), ("out_dchar", _p),
+        ("num_devices", _i32), ("device_ids", C.POINTER(_i32)),
+        ("variant", _i32), ("v", _i32), ("seed", _u64), ("t_medium", _i64),
+        ("stats", C.POINTER(Stats)),
+    ]
+
+
 class KernelProfile(C.Structure):
     _fields_ = [("name", C.c_char * 32), ("launches", C.c_int64), ("units", C.c_int64),
                 ("ms", C.c_double), ("bytes", C.c_int64)]
@@ -57,6 +67,7 @@ SIGNATURES = {
     "s5g_sort_host": (C.c_int, [_p, _i64, _p, _i64, _i64, _p, _p, _p, _i32, _i32, _u64, _i64,
                                 C.POINTER(Stats)]),
     "s5g_release_cached_memory": (None, []),
+    "s5g_sort_multi": (C.c_int, [C.POINTER(MultiArgs)]),
     "s5g_extract_keys": (C.c_int, [_p, _i64, _p, _i64, _i64, _p, _p]),
     "s5g_select_splitters": (C.c_int, [_p, _i64, _i64, _p, _p, _p, _p, _p]),
     "s5g_classify": (C.c_int, [_p, _i64, _p, _p, _i64, _i32, _p, _p]),

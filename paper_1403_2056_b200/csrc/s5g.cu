@@ -15,6 +15,7 @@
 #include <mutex>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "s5g.h"
@@ -1043,6 +1044,12 @@ __global__ void k_pos_gather(const int64_t* __restrict__ query, int64_t m,
                              const int32_t* __restrict__ map, int64_t* __restrict__ out) {
     const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (j < m) out[j] = map[query[j]];
+}
+
+__global__ void k_gather_i64(const int64_t* __restrict__ src, const int64_t* __restrict__ idx,
+                             int64_t m, int64_t* __restrict__ out) {
+    const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (j < m) out[j] = src[idx[j]];
 }
 
 // dist_stats (strset.py:290-309) from an exact LCP array: since every LCP is
@@ -2106,6 +2113,201 @@ void s5g_release_cached_memory(void) {
         std::lock_guard<std::mutex> lk(g_host[d].mu);
         if (g_host[d].pool) cudaMemPoolTrimTo(g_host[d].pool, 0);
     }
+}
+
+// ---- one host process, G devices (parallel_s5's p, parallel.py:468-492) ----
+// The reference forks p workers over one shared set; here p devices each
+// take one part of a sample-sort partition: G-1 string splitters (sampled
+// prefixes, ties broken by input position) cut the input into G ranges of
+// the output order; every device receives the whole arena, classifies all
+// strings against the splitters (s5g_partition, redundantly -- it costs a
+// few string compares per string), keeps its own range in input order
+// (s5g_group_by_dest is stable) and sorts it; the parts land at their output
+// offsets, and the host fixes the LCP at every part boundary -- the
+// _boundary_lcps of parallel.py:447-455.
+static int64_t host_lcp(const uint8_t* a, int64_t alen, int64_t x, int64_t y) {
+    int64_t l = 0;
+    while (x + l < alen && y + l < alen && a[x + l] == a[y + l] && a[x + l] != 0) l++;
+    return l;
+}
+
+static int multi_part(int dev, int k, int G, const s5g_multi_args* m, const std::vector<uint8_t>& sp,
+                      const std::vector<int64_t>& sp_off, const std::vector<int64_t>& sp_g,
+                      std::vector<int64_t>& counts_out, s5g_stats* st_out) {
+    CK(cudaSetDevice(dev));
+    HostCtx& hx = g_host[dev];
+    std::lock_guard<std::mutex> lk(hx.mu);
+    if (int rc = hx.init(dev)) return rc;
+    cudaStream_t st = hx.st;
+    const int64_t n = m->n, alen = m->arena_len;
+    const size_t alen_pad = ((size_t)alen + S5G_ARENA_PAD + 15) & ~size_t(15);
+    std::vector<void*> bufs;
+    auto alloc = [&](size_t bytes) -> void* {
+        void* p = nullptr;
+        if (cudaMallocFromPoolAsync(&p, std::max<size_t>(bytes, 16), hx.pool, st) != cudaSuccess) return nullptr;
+        bufs.push_back(p);
+        return p;
+    };
+    struct Free {
+        std::vector<void*>& b;
+        cudaStream_t s;
+        ~Free() {
+            for (void* p : b) cudaFreeAsync(p, s);
+            cudaStreamSynchronize(s);
+        }
+    } fr{bufs, st};
+    const int nsp = G - 1;
+    uint8_t* d_arena = (uint8_t*)alloc(alen_pad);
+    int64_t* d_all = (int64_t*)alloc(8 * n);
+    int32_t* d_dest = (int32_t*)alloc(4 * n);
+    int64_t* d_order = (int64_t*)alloc(8 * n);
+    int64_t* d_cnt = (int64_t*)alloc(8 * G);
+    const size_t gws = s5g_group_workspace_bytes(n, G);
+    void* d_gws = alloc(gws);
+    uint8_t* d_sp = (uint8_t*)alloc(sp.size());
+    int64_t* d_spo = (int64_t*)alloc(8 * sp_off.size());
+    int64_t* d_spg = (int64_t*)alloc(8 * std::max<size_t>(1, sp_g.size()));
+    if (!d_arena || !d_all || !d_dest || !d_order || !d_cnt || !d_gws || !d_sp || !d_spo || !d_spg)
+        return fail(S5G_E_CUDA, "device allocation failed");
+    CK(cudaMemsetAsync(d_arena + alen, 0, alen_pad - alen, st));
+    CK(hx.h2d(d_arena, m->arena, alen));
+    CK(hx.h2d(d_all, m->handles, 8 * n));
+    if (!sp.empty()) CK(cudaMemcpyAsync(d_sp, sp.data(), sp.size(), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d_spo, sp_off.data(), 8 * sp_off.size(), cudaMemcpyHostToDevice, st));
+    if (!sp_g.empty()) CK(cudaMemcpyAsync(d_spg, sp_g.data(), 8 * sp_g.size(), cudaMemcpyHostToDevice, st));
+    if (int rc = s5g_partition(d_arena, alen, d_all, n, 0, nullptr, d_sp, d_spo, d_spg, nsp, d_dest, st))
+        return rc;
+    if (int rc = s5g_group_by_dest(d_dest, n, G, d_order, d_cnt, d_gws, gws, st)) return rc;
+    std::vector<int64_t> cnt(G);
+    CK(cudaMemcpyAsync(cnt.data(), d_cnt, 8 * G, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    int64_t off = 0;
+    for (int q = 0; q < k; q++) off += cnt[q];
+    const int64_t mk = cnt[k];
+    counts_out = cnt;
+    if (mk == 0) return 0;
+    int64_t* d_part = (int64_t*)alloc(8 * mk);
+    int64_t* d_oh = (int64_t*)alloc(8 * mk);
+    int64_t* d_ol = m->out_lcps || m->out_dchar ? (int64_t*)alloc(8 * mk) : nullptr;
+    const int64_t tm = m->t_medium > 0 ? m->t_medium : (1 << 20);
+    const size_t ws = s5g_workspace_bytes(mk, tm);
+    void* d_ws = alloc(ws);
+    if (!d_part || !d_oh || !d_ws || ((m->out_lcps || m->out_dchar) && !d_ol))
+        return fail(S5G_E_CUDA, "device allocation failed");
+    g_launches++;
+    k_gather_i64<<<blocks_for(mk, 256), 256, 0, st>>>(d_all, d_order + off, mk, d_part);
+    CK(cudaGetLastError());
+    s5g_sort_args a{};
+    a.arena = d_arena; a.arena_len = alen; a.handles = d_part; a.n = mk; a.depth = m->depth;
+    a.out_handles = d_oh; a.out_lcps = d_ol; a.out_dchar = nullptr;
+    a.workspace = d_ws; a.workspace_bytes = ws; a.stream = st;
+    a.variant = m->variant; a.v = m->v; a.seed = m->seed; a.t_medium = tm; a.stats = st_out;
+    if (int rc = sort_impl(&a)) return rc;
+    CK(hx.d2h(m->out_handles + off, d_oh, 8 * mk));
+    if (m->out_lcps) CK(hx.d2h(m->out_lcps + off, d_ol, 8 * mk));
+    CK(cudaStreamSynchronize(st));
+    return 0;
+}
+
+int s5g_sort_multi(const s5g_multi_args* m) {
+    if (!m) return fail(S5G_E_INVALID, "null args");
+    if (m->n < 0 || m->arena_len < 0) return fail(S5G_E_INVALID, "negative size");
+    if (m->variant != S5G_VARIANT_UNROLL && m->variant != S5G_VARIANT_EQUAL)
+        return fail(S5G_E_VARIANT, "unknown classify variant");
+    if (m->num_devices < 1 || !m->device_ids) return fail(S5G_E_INVALID, "num_devices must be >= 1");
+    int ndev = 0;
+    CK(cudaGetDeviceCount(&ndev));
+    for (int k = 0; k < m->num_devices; k++)
+        if (m->device_ids[k] < 0 || m->device_ids[k] >= ndev || m->device_ids[k] >= MAX_DEV)
+            return fail(S5G_E_INVALID, "device id " + std::to_string(m->device_ids[k]) +
+                                           " is not one of the " + std::to_string(ndev) +
+                                           " visible CUDA devices");
+    const int64_t n = m->n;
+    if (n == 0) return 0;
+    const int G = m->num_devices;
+    if (G == 1) {
+        int prev = 0;
+        CK(cudaGetDevice(&prev));
+        CK(cudaSetDevice(m->device_ids[0]));
+        const int rc = s5g_sort_host(m->arena, m->arena_len, m->handles, n, m->depth, m->out_handles,
+                                     m->out_lcps, m->out_dchar, m->variant, m->v, m->seed,
+                                     m->t_medium, m->stats);
+        cudaSetDevice(prev);
+        return rc;
+    }
+    // G-1 splitters: sampled string prefixes (<= SPLIT_MAX bytes) with their
+    // input positions, sorted, equally spaced (dist.pick_splitters)
+    constexpr int SPLIT_MAX = 64;
+    const int64_t S = std::min<int64_t>(n, 1024LL * G);
+    const uint8_t* A = m->arena;
+    std::vector<std::pair<std::string, int64_t>> smp(S);
+    for (int64_t j = 0; j < S; j++) {
+        const int64_t pos = S == n ? j : (int64_t)(splitmix64(m->seed ^ splitmix64((uint64_t)j + 0x51ull)) % (uint64_t)n);
+        const int64_t h = m->handles[pos];
+        if (h < 0 || h >= m->arena_len) return fail(S5G_E_INVALID, "handle outside the buffer");
+        int64_t L = 0;
+        while (L < SPLIT_MAX && h + L < m->arena_len && A[h + L]) L++;
+        smp[j] = {std::string((const char*)A + h, (size_t)L), pos};
+    }
+    std::sort(smp.begin(), smp.end(), [](const auto& x, const auto& y) {
+        const int c = std::memcmp(x.first.data(), y.first.data(), std::min(x.first.size(), y.first.size()));
+        if (c) return c < 0;
+        if (x.first.size() != y.first.size()) return x.first.size() < y.first.size();
+        return x.second < y.second;
+    });
+    std::vector<uint8_t> sp;
+    std::vector<int64_t> sp_off{0}, sp_g;
+    for (int k = 1; k < G; k++) {
+        const auto& pk = smp[(size_t)(k * S / G)];
+        sp.insert(sp.end(), pk.first.begin(), pk.first.end());
+        sp_off.push_back((int64_t)sp.size());
+        sp_g.push_back(pk.second);
+    }
+    std::vector<int> rcs(G, 0);
+    std::vector<std::string> errs(G);
+    std::vector<std::vector<int64_t>> counts(G);
+    std::vector<s5g_stats> sts(G);
+    std::vector<std::thread> th;
+    for (int k = 0; k < G; k++) {
+        sts[k] = s5g_stats{};
+        th.emplace_back([&, k]() {
+            rcs[k] = multi_part(m->device_ids[k], k, G, m, sp, sp_off, sp_g, counts[k], &sts[k]);
+            if (rcs[k]) errs[k] = g_err;
+        });
+    }
+    for (auto& t : th) t.join();
+    for (int k = 0; k < G; k++)
+        if (rcs[k]) return fail(rcs[k], "device " + std::to_string(m->device_ids[k]) + ": " + errs[k]);
+    // boundary LCPs between consecutive non-empty parts; lcps[0] = -1
+    const std::vector<int64_t>& cnt = counts[0];
+    if (m->out_lcps) {
+        int64_t off = 0, prev_last = -1;
+        for (int k = 0; k < G; k++) {
+            if (cnt[k]) {
+                if (prev_last >= 0)
+                    m->out_lcps[off] = host_lcp(A, m->arena_len, m->out_handles[prev_last], m->out_handles[off]);
+                prev_last = off + cnt[k] - 1;
+            }
+            off += cnt[k];
+        }
+        m->out_lcps[0] = -1;
+        if (m->out_dchar) {
+#pragma omp parallel for schedule(static)
+            for (int64_t i = 0; i < n; i++) {
+                const int64_t l = m->out_lcps[i];
+                m->out_dchar[i] = A[m->out_handles[i] + (l < 0 ? 0 : l)];
+            }
+        }
+    }
+    if (m->stats)
+        for (int k = 0; k < G; k++) {
+            m->stats->char_cmps += sts[k].char_cmps;
+            m->stats->word_fetches += sts[k].word_fetches;
+            m->stats->scratch_words += sts[k].scratch_words;
+            m->stats->jobs_enqueued += sts[k].jobs_enqueued;
+            m->stats->jobs_executed += sts[k].jobs_executed;
+        }
+    return 0;
 }
 
 int s5g_extract_keys(const uint8_t* arena, int64_t arena_len, const int64_t* handles, int64_t n,

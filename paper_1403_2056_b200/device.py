@@ -262,6 +262,39 @@ def kway_merge(ds: DeviceStrings, run_offsets, handles: torch.Tensor, lcps: torc
     return out_h, out_l
 
 
+def kway_merge_any(ds: DeviceStrings, run_offsets, handles: torch.Tensor, lcps: torch.Tensor,
+                   dchar: torch.Tensor | None = None, shared: int = 0,
+                   stats: Stats | None = None):
+    """kway_merge for any number of runs: while there are more than 16, merge
+    consecutive groups of up to 16 (ties to the earlier run, so the result
+    stays the stable order) and repeat -- the reference's kway_lcp_merge /
+    partitioned_merge_sort take any K (lcpmerge.py:385-424,
+    parallel.py:885-994)."""
+    off = np.ascontiguousarray(run_offsets, dtype=np.int64)
+    while len(off) - 1 > 16:
+        K = len(off) - 1
+        out_h = torch.empty_like(handles)
+        out_l = torch.empty_like(lcps)
+        new_off = [int(off[0])]
+        for g0 in range(0, K, 16):
+            g1 = min(K, g0 + 16)
+            lo, hi = int(off[g0] - off[0]), int(off[g1] - off[0])
+            if g1 - g0 == 1 or hi == lo:
+                out_h[lo:hi] = handles[lo:hi]
+                out_l[lo:hi] = lcps[lo:hi]
+            else:
+                mh, ml = kway_merge(ds, off[g0:g1 + 1] - off[g0], handles[lo:hi], lcps[lo:hi],
+                                    dchar[lo:hi] if dchar is not None else None, shared, stats)
+                out_h[lo:hi] = mh
+                out_l[lo:hi] = ml
+            new_off.append(int(off[g1]))
+        handles, lcps = out_h, out_l
+        if dchar is not None:  # distinguishing characters of the merged runs
+            dchar = fill_dchar(ds, handles, lcps.clamp(min=0))
+        off = np.asarray(new_off, dtype=np.int64)
+    return kway_merge(ds, off, handles, lcps, dchar, shared, stats)
+
+
 def group_by_dest(dest: torch.Tensor, G: int):
     """Stable order of the strings by destination rank and the per-rank
     counts (s5g_group_by_dest)."""

@@ -49,7 +49,8 @@ def _accumulate(stats, st) -> None:
 
 def kway_lcp_merge(streams: list, shared: int = 0, stats=None, cached: bool = False,
                    out_handles: np.ndarray | None = None, out_lcps: np.ndarray | None = None):
-    """Merge K <= 16 sorted runs of one set on the GPU (lcpmerge.py:385-424)."""
+    """Merge K sorted runs of one set on the GPU (lcpmerge.py:385-424); more
+    than 16 runs merge in rounds of groups of 16 (device.kway_merge_any)."""
     stats = stats if stats is not None else SortStats()
     streams = list(streams)
     n = sum(int(s.length) for s in streams)
@@ -57,8 +58,6 @@ def kway_lcp_merge(streams: list, shared: int = 0, stats=None, cached: bool = Fa
     out_l = out_lcps if out_lcps is not None else np.empty(n, dtype=np.int64)
     if n == 0:
         return out_h, out_l
-    if len(streams) > 16:
-        raise ValueError("at most 16 streams per merge")
     sset = streams[0].sset
     hs = [np.asarray(s.handles[s.start:s.start + s.length], dtype=np.int64) for s in streams]
     ls = [np.asarray(s.lcps[s.start:s.start + s.length], dtype=np.int64) for s in streams]
@@ -78,7 +77,7 @@ def kway_lcp_merge(streams: list, shared: int = 0, stats=None, cached: bool = Fa
         else:  # fill_dchar (basecase.py:36-42) on the device
             dchar_d = D.fill_dchar(ds, ds.handles, l_d)
     st = _lib.Stats()
-    mh, ml = D.kway_merge(ds, off, ds.handles, l_d, dchar_d, shared, st)
+    mh, ml = D.kway_merge_any(ds, off, ds.handles, l_d, dchar_d, shared, st)
     _accumulate(stats, st)
     out_h[:n] = mh.cpu().numpy()
     out_l[:n] = ml.cpu().numpy()

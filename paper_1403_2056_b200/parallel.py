@@ -1,28 +1,98 @@
 """Drop-in ``parallel_s5`` (parallel.py:468-492) on GPUs.
 
-In the reference, p is the number of forked CPU workers sharing one set.
-Here the fully parallel step is the device-wide S^5 step (every CTA a
-shard, bucket-major/CTA-minor offsets -- the interleaved prefix sum of
-parallel.py:379-385), so one GPU already runs the reference's phased
-structure.  ``p`` counts GPUs; within one process the set is sorted on the
-current device.  Multi-GPU runs use one process per GPU
-(``paper_1403_2056_b200.dist``: sample-sort partition + NCCL all-to-all).
+In the reference, p is the number of forked CPU workers sharing one set
+(p=None: os.cpu_count(), parallel.py:64-65).  Here p is the number of GPUs
+(p=None: every visible device) and one process drives them all through the
+library's multi-device entry (s5g_sort_multi): a sample-sort partition
+with p-1 string splitters cuts the output order into p ranges, each device
+sorts its range with the full S^5 (whose device-wide step is itself the
+reference's phased step: every CTA a shard, bucket-major/CTA-minor
+offsets), and the part-boundary LCPs are fixed on the host
+(_boundary_lcps, parallel.py:447-455).  p larger than the visible device
+count raises ValueError.  The multi-PROCESS form (one process per GPU,
+NCCL all-to-all) is ``paper_1403_2056_b200.dist``.
 """
 
 from __future__ import annotations
 
+import ctypes as C
+
 import numpy as np
 
-from .ssss import T_MEDIUM, check_set, s5_sort
+from .ssss import T_MEDIUM, _accumulate, check_set, s5_sort
 from .strset import LCP_UNDEF, SortedWithLcp, SortStats
 
 
+def visible_devices() -> int:
+    import torch
+
+    return torch.cuda.device_count() if torch.cuda.is_available() else 0
+
+
 def parallel_s5(sset, p=None, want_lcps: bool = False, want_dchar: bool = False, seed: int = 1,
-                variant: str = "unroll", stats=None, t_medium: int = T_MEDIUM):
-    """Sample sort on the GPU; content order matches the sequential sorter."""
+                variant: str = "unroll", stats=None, t_medium: int = T_MEDIUM, devices=None):
+    """Sample sort on p GPUs; the output is the stable content order, identical
+    to s5_sort's (and the reference's).  `devices` (tests): explicit device
+    ordinals, repeats allowed, instead of 0 .. p-1."""
+    from . import _lib
+    from . import device as D
+
+    if variant not in _lib.VARIANTS:
+        raise ValueError(f"unknown classify variant: {variant}")
+    ndev = visible_devices()
+    if devices is None:
+        if p is None:
+            p = max(ndev, 1)
+        if p < 1:
+            raise ValueError("p must be at least 1")
+        if p > ndev:
+            raise ValueError(f"p = {p} exceeds the {ndev} visible CUDA device(s)")
+        devices = list(range(p))
+    devices = [int(d) for d in devices]
     want = want_lcps or want_dchar
-    return s5_sort(sset, want_lcps=want, want_dchar=want_dchar, variant=variant, seed=seed,
-                   stats=stats, t_medium=t_medium)
+    stats = stats if stats is not None else SortStats()
+    handles = np.ascontiguousarray(sset.handles, dtype=np.int64)
+    n = len(handles)
+    if len(devices) == 1 or n == 0:
+        if devices and n:
+            import torch
+
+            with torch.cuda.device(devices[0]):
+                return s5_sort(sset, want_lcps=want, want_dchar=want_dchar, variant=variant,
+                               seed=seed, stats=stats, t_medium=t_medium)
+        return s5_sort(sset, want_lcps=want, want_dchar=want_dchar, variant=variant, seed=seed,
+                       stats=stats, t_medium=t_medium)
+    check_set(sset.buffer, handles)
+    D._require_cuda()
+    arr = sset.buffer if isinstance(sset.buffer, np.ndarray) else \
+        np.frombuffer(sset.buffer, dtype=np.uint8)
+    oh = np.empty(n, dtype=np.int64)
+    ol = np.empty(n, dtype=np.int64) if want else None
+    od = np.empty(n, dtype=np.uint8) if want_dchar else None
+    ids = (C.c_int32 * len(devices))(*devices)
+    st = _lib.Stats()
+    a = _lib.MultiArgs()
+    a.arena = arr.ctypes.data if arr.size else None
+    a.arena_len = arr.size
+    a.handles = handles.ctypes.data
+    a.n = n
+    a.depth = 0
+    a.out_handles = oh.ctypes.data
+    a.out_lcps = ol.ctypes.data if ol is not None else None
+    a.out_dchar = od.ctypes.data if od is not None else None
+    a.num_devices = len(devices)
+    a.device_ids = ids
+    a.variant = _lib.VARIANTS[variant]
+    a.v = 8191
+    a.seed = int(seed) & ((1 << 64) - 1)
+    a.t_medium = int(t_medium)
+    a.stats = C.pointer(st)
+    _lib.check(_lib.lib().s5g_sort_multi(C.byref(a)))
+    _accumulate(stats, st)
+    out = sset.with_handles(oh)
+    if not want:
+        return out
+    return SortedWithLcp(out, ol, od, stats)
 
 
 def partitioned_merge_sort(sset, K: int = 4, p=None, use_cache: bool = True,
@@ -43,8 +113,6 @@ def partitioned_merge_sort(sset, K: int = 4, p=None, use_cache: bool = True,
     if n == 0 or K <= 1:
         return parallel_s5(sset, p, want_lcps=want_lcps, seed=seed, stats=stats,
                            t_medium=t_medium)
-    if K > 16:
-        raise ValueError("at most 16 parts per merge")
     handles = np.ascontiguousarray(sset.handles, dtype=np.int64)
     check_set(sset.buffer, handles)
     ds = D.upload(sset.buffer, handles)
@@ -73,7 +141,7 @@ def partitioned_merge_sort(sset, K: int = 4, p=None, use_cache: bool = True,
             for f in _lib.STATS_FIELDS:
                 setattr(stats, f, getattr(stats, f) + int(getattr(st, f)))
     mst = _lib.Stats()
-    out_h, out_l = D.kway_merge(ds, off, run_h, run_l, run_c, 0, mst)
+    out_h, out_l = D.kway_merge_any(ds, off[: len(parts) + 1], run_h, run_l, run_c, 0, mst)
     for tgt in (merge_stats, stats):
         if tgt is not None:
             for f in _lib.STATS_FIELDS:

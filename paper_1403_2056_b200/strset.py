@@ -7,7 +7,8 @@ interchange with it (duck-typed: any object with ``buffer``, ``handles`` and
 * ``StringSet``      strset.py:34-89  (immutable bytes buffer + int64 handles)
 * ``SortedWithLcp``  basecase.py:21-33 (set, lcps with lcps[0] = -1, dchar, stats)
 * ``SortStats``      counters.py:13-49
-* ``from_strings``   strset.py:137-149, ``load_delimited`` strset.py:113-134
+* ``from_strings``   strset.py:137-149 (contract); ``load_delimited``
+  strset.py:113-134 runs on the GPU (device.load_delimited)
 
 Word helpers (``word_terminator_pos``, ``shared_chars``) are vectorised numpy
 forms of strset.py:178-206, used on the host only to describe splitter trees
@@ -87,35 +88,26 @@ class SortedWithLcp:
 
 
 def from_strings(strings: Iterable[bytes]) -> StringSet:
-    items = list(strings)
-    for s in items:
-        if 0 in s:
-            raise ValueError("string contains the terminator byte")
-    buf = b"\0".join(items) + b"\0" if items else b""
-    lens = np.fromiter((len(s) + 1 for s in items), dtype=np.int64, count=len(items))
-    offs = np.zeros(len(items), dtype=np.int64)
-    if len(items) > 1:
-        np.cumsum(lens[:-1], out=offs[1:])
-    return StringSet(buf, offs)
+    """A set holding `strings` in order (the reference's strset.from_strings
+    contract, strset.py:137-149: a string may not contain the terminator)."""
+    items = [bytes(x) for x in strings]
+    if any(b"\0" in x for x in items):
+        raise ValueError("string contains the terminator byte")
+    sizes = np.array([len(x) + 1 for x in items], dtype=np.int64)
+    starts = np.concatenate(([0], np.cumsum(sizes)[:-1])).astype(np.int64) if items else sizes
+    return StringSet(b"".join(x + b"\0" for x in items), starts)
 
 
 def load_delimited(data: bytes, delimiter: int = 0) -> StringSet:
-    if not (0 <= delimiter < 256):
-        raise ValueError("delimiter must be a byte value")
-    if len(data) == 0:
-        return StringSet(b"", np.zeros(0, dtype=np.int64))
-    if delimiter != 0:
-        if 0 in data:
-            raise ValueError("input contains byte 0, which is reserved as terminator")
-        data = data.replace(bytes([delimiter]), b"\0")
-    if not data.endswith(b"\0"):
-        data = data + b"\0"
-    arr = np.frombuffer(data, dtype=np.uint8)
-    zeros = np.flatnonzero(arr == 0)
-    starts = np.empty(len(zeros), dtype=np.int64)
-    starts[0] = 0
-    starts[1:] = zeros[:-1] + 1
-    return StringSet(data, starts)
+    """load_delimited (strset.py:113-134) with the delimiter remap and the
+    string-start scan on the GPU (s5g_load_delimited); the returned set's
+    buffer is the device arena copied back, its handles the device's starts.
+    Same errors and output as the reference (pinned by
+    tests/golden/golden_load.npz, generated from the reference itself)."""
+    from . import device as D
+
+    ds = D.load_delimited(data, delimiter)
+    return StringSet(bytes(ds.arena[: ds.arena_len].cpu().numpy()), ds.handles.cpu().numpy())
 
 
 def _be_bytes(keys: np.ndarray) -> np.ndarray:

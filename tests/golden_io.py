@@ -54,3 +54,23 @@ def merge(name):
     out = {k[len(pre):]: v for k, v in arrays.items() if k.startswith(pre)}
     out.update(meta["merge"][name])
     return out
+
+
+LOAD_PATH = Path(__file__).resolve().parent / "golden" / "golden_load.npz"
+
+
+@lru_cache(maxsize=1)
+def load_cases():
+    """name -> {input, delimiter, error, buffer, handles}: the reference's
+    load_delimited (strset.py:113-134) on seeded inputs (make_golden_load.py)."""
+    z = np.load(LOAD_PATH)
+    meta = json.loads(z["meta"].tobytes().decode())
+    out = {}
+    for name, m in meta.items():
+        c = dict(m)
+        c["input"] = z[f"{name}/input"]
+        if m["error"] is None:
+            c["buffer"] = z[f"{name}/buffer"]
+            c["handles"] = z[f"{name}/handles"]
+        out[name] = c
+    return out

@@ -12,23 +12,28 @@ torch = pytest.importorskip("torch")
 
 from paper_1403_2056_b200 import corpora  # noqa: E402
 from paper_1403_2056_b200 import device as D  # noqa: E402
-from paper_1403_2056_b200.strset import load_delimited  # noqa: E402
+from paper_1403_2056_b200 import load_delimited  # noqa: E402
 
 
-@pytest.mark.parametrize("data,delim", [
-    (b"a\0b\0", 0), (b"ab\ncd\n", 10), (b"ab\ncd", 10), (b"", 10), (b"\n\n", 10),
-    (b"x", 0), (b"abc\0\0d", 0)])
-def test_load_delimited_matches_host(data, delim):
-    want = load_delimited(data, delim)
-    ds = D.load_delimited(data, delim)
-    assert ds.arena_len == len(want.buffer)
-    assert bytes(ds.arena[: ds.arena_len].cpu().numpy()) == want.buffer
-    assert np.array_equal(ds.handles.cpu().numpy(), want.handles)
-
-
-def test_load_delimited_rejects_zero_with_delimiter():
-    with pytest.raises(ValueError, match="reserved as terminator"):
-        D.load_delimited(b"a\0b\n", 10)
+@pytest.mark.parametrize("name", sorted(G.load_cases()))
+def test_load_delimited_matches_reference_golden(name):
+    """GPU load_delimited against the reference's own outputs
+    (tests/golden/golden_load.npz, made by make_golden_load.py from
+    strsort.strset.load_delimited, strset.py:113-134)."""
+    c = G.load_cases()[name]
+    data = c["input"].tobytes()
+    if c["error"]:
+        with pytest.raises(ValueError, match="reserved as terminator"):
+            D.load_delimited(data, c["delimiter"])
+        with pytest.raises(ValueError, match="reserved as terminator"):
+            load_delimited(data, c["delimiter"])
+        return
+    ds = D.load_delimited(data, c["delimiter"])
+    assert ds.arena_len == len(c["buffer"])
+    assert np.array_equal(ds.arena[: ds.arena_len].cpu().numpy(), c["buffer"])
+    assert np.array_equal(ds.handles.cpu().numpy(), c["handles"])
+    s = load_delimited(data, c["delimiter"])  # the package-level (GPU) entry
+    assert s.buffer == c["buffer"].tobytes() and np.array_equal(s.handles, c["handles"])
 
 
 def test_load_delimited_large_then_sort():
@@ -36,11 +41,12 @@ def test_load_delimited_large_then_sort():
     lines = [bytes(rng.integers(97, 123, size=int(rng.integers(0, 30)), dtype=np.uint8))
              for _ in range(200_000)]
     raw = b"\n".join(lines)
-    want = load_delimited(raw, 10)
     ds = D.load_delimited(raw, 10)
-    assert np.array_equal(ds.handles.cpu().numpy(), want.handles)
+    buf = raw.replace(b"\n", b"\0") + b"\0"
+    starts = np.concatenate(([0], np.flatnonzero(np.frombuffer(buf, np.uint8) == 0)[:-1] + 1))
+    assert np.array_equal(ds.handles.cpu().numpy(), starts)
     h, l, _ = D.sort(ds, want_lcps=True)
-    oh, ol, _ = oracle.parallel_s5(want.buffer, want.handles)
+    oh, ol, _ = oracle.parallel_s5(buf, starts)
     assert np.array_equal(h.cpu().numpy(), oh) and np.array_equal(l.cpu().numpy(), ol)
 
 

@@ -128,7 +128,7 @@ def test_lcpmerge_api_mirrors_reference():
     assert np.array_equal(h, eh) and l[0] == -1 and np.array_equal(l[1:], el[1:])
 
 
-@pytest.mark.parametrize("K", [1, 2, 4, 8, 16])
+@pytest.mark.parametrize("K", [1, 2, 4, 8, 16, 17, 40])
 @pytest.mark.parametrize("name", ["random_3000", "urls_2000", "dups_2000", "deep_prefix_1500",
                                   "suffixes_1800", "all_equal_700", "shuffled_dups_2500",
                                   "random_n17", "random_n2"])
@@ -150,3 +150,22 @@ def test_partitioned_merge_sort_scaled_configs(cfg, scale):
     res = P.partitioned_merge_sort(s, K=8, want_lcps=True)
     status, bad = oracle.certify(buf, handles, res.set.handles, res.lcps)
     assert status == 0, (oracle.CERT_STATUS[status], bad)
+
+
+def test_kway_lcp_merge_more_than_16_streams():
+    """K > 16 (the reference takes any K): merged in rounds of 16-run groups."""
+    c = G.case("random_3000")
+    s = P.StringSet(c["buffer_bytes"], c["handles"])
+    K = 37
+    cuts = np.linspace(0, len(c["handles"]), K + 1).astype(np.int64)
+    hs, ls = [], []
+    for j in range(K):
+        r = P.s5_sort(s.with_handles(c["handles"][cuts[j]:cuts[j + 1]]), want_lcps=True)
+        hs.append(r.set.handles)
+        ls.append(r.lcps)
+    H, L = np.concatenate(hs), np.concatenate(ls)
+    streams = [P.LcpStream(s, H, L, None, int(cuts[j]), int(cuts[j + 1] - cuts[j])) for j in range(K)]
+    for cached in (False, True):
+        oh, ol = P.kway_lcp_merge(streams, cached=cached)
+        assert np.array_equal(oh, c["out_handles"])
+        assert np.array_equal(ol[1:], c["lcps"][1:]) and ol[0] == -1

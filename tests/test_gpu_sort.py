@@ -212,3 +212,42 @@ def test_root_step_sizes_vs_oracle(n, alphabet):
     oh, ol, _ = oracle.parallel_s5(buf, hnd)
     assert np.array_equal(h.cpu().numpy(), oh)
     assert np.array_equal(l.cpu().numpy(), ol)
+
+
+@pytest.mark.parametrize("devices", [[0, 0], [0, 0, 0], [0] * 8])
+@pytest.mark.parametrize("name", ["random_3000", "dups_2000", "shuffled_dups_2500", "urls_2000",
+                                  "all_equal_700", "suffixes_1800", "random_n2", "random_n17"])
+def test_parallel_s5_multi_device_partition(name, devices):
+    """parallel_s5 with p parts (s5g_sort_multi): sample-sort partition by
+    string splitters with input-position ties, one sort per part, boundary
+    LCPs fixed on the host.  One GPU here, so the parts share device 0 -- the
+    partition, the per-part offsets and the boundary fix-up are what is
+    tested; the output must equal the reference's bit for bit."""
+    c = G.case(name)
+    s = P.StringSet(c["buffer_bytes"], c["handles"])
+    res = P.parallel_s5(s, want_lcps=True, want_dchar=True, devices=devices)
+    assert np.array_equal(res.set.handles, c["out_handles"])
+    assert np.array_equal(res.lcps, c["lcps"])
+    assert np.array_equal(res.dchar, c["dchar"])
+    out = P.parallel_s5(s, devices=devices)
+    assert np.array_equal(out.handles, c["out_handles"])
+
+
+def test_parallel_s5_multi_device_scaled_config():
+    buf, hnd = corpora.gen_urls(1 << 18, 7)
+    s = P.StringSet(buf.tobytes(), hnd)
+    res = P.parallel_s5(s, want_lcps=True, devices=[0, 0, 0, 0])
+    h, l, _ = oracle.parallel_s5(buf, hnd)
+    assert np.array_equal(res.set.handles, h) and np.array_equal(res.lcps, l)
+
+
+def test_parallel_s5_p_counts_gpus():
+    c = G.case("random_3000")
+    s = P.StringSet(c["buffer_bytes"], c["handles"])
+    ndev = torch.cuda.device_count()
+    res = P.parallel_s5(s, p=None, want_lcps=True)  # p=None: every visible GPU
+    assert np.array_equal(res.set.handles, c["out_handles"])
+    with pytest.raises(ValueError, match="exceeds"):
+        P.parallel_s5(s, p=ndev + 1)
+    with pytest.raises(ValueError, match="at least 1"):
+        P.parallel_s5(s, p=0)

@@ -9,7 +9,7 @@ import golden_io as G
 from paper_1403_2056_b200 import corpora
 from paper_1403_2056_b200.ssss import SplitterTree, check_set, s5_sort, tree_capacity
 from paper_1403_2056_b200.strset import (
-    StringSet, from_strings, load_delimited, shared_chars, word_terminator_pos)
+    StringSet, from_strings, shared_chars, word_terminator_pos)
 
 
 def test_unknown_variant_is_value_error():
@@ -32,11 +32,26 @@ def test_empty_set_needs_no_device():
     assert len(res.set) == 0 and len(res.lcps) == 0 and len(res.dchar) == 0
 
 
-def test_load_delimited_and_from_strings():
-    s = load_delimited(b"ab\ncd", ord("\n"))
-    assert list(s.handles) == [0, 3] and s.strings() == [b"ab", b"cd"]
+def test_from_strings():
     s = from_strings([b"x", b"", b"yz"])
     assert s.buffer == b"x\0\0yz\0" and list(s.handles) == [0, 2, 3]
+    assert from_strings([]).buffer == b"" and len(from_strings([]).handles) == 0
+    with pytest.raises(ValueError, match="terminator"):
+        from_strings([b"a\0b"])
+
+
+def test_load_delimited_golden_fixtures_are_consistent():
+    """tests/golden/golden_load.npz holds the reference's own load_delimited
+    outputs (make_golden_load.py); the GPU path is checked against them in
+    test_gpu_extras.py.  Here: every fixture is a well-formed string set."""
+    for name, c in G.load_cases().items():
+        if c["error"]:
+            assert 0 in c["input"] and c["delimiter"] != 0
+            continue
+        buf, h = c["buffer"], c["handles"]
+        assert len(buf) == 0 or buf[-1] == 0
+        assert (len(h) == 0 and len(buf) == 0) or (h[0] == 0 and (buf[h[1:] - 1] == 0).all())
+        assert int((buf == 0).sum()) == len(h)
 
 
 @pytest.mark.parametrize("name", G.kats())
@@ -109,3 +124,14 @@ def test_register_with_reference_harness():
     from paper_1403_2056_b200.bench_api import register_with_strsort
     assert register_with_strsort()
     assert "gpu-s5" in B.ALGORITHMS and "gpu-ps5" in B.ALGORITHMS
+
+
+def test_parallel_s5_p_beyond_visible_devices_is_a_value_error():
+    """p counts GPUs (parallel.py:468-492's p counts workers); more than the
+    visible devices is refused before any device work."""
+    import paper_1403_2056_b200 as P
+    s = from_strings([b"b", b"a"])
+    with pytest.raises(ValueError, match="exceeds"):
+        P.parallel_s5(s, p=P.parallel.visible_devices() + 1)
+    with pytest.raises(ValueError, match="unknown classify variant"):
+        P.parallel_s5(s, p=1, variant="bogus")

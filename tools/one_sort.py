@@ -14,8 +14,12 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c2_dna")
 ap.add_argument("--scale", type=float, default=1.0)
 a = ap.parse_args()
-buf, hnd = corpora.CONFIGS[a.config](a.scale)
-ds = D.upload(buf, hnd)
+if a.config == "c5_nodup":  # generated in HBM (same bytes as the host generator)
+    arena, alen, h = corpora.gen_nodup_device(int((1 << 28) * a.scale))
+    ds, hnd = D.DeviceStrings(arena, alen, h), h
+else:
+    buf, hnd = corpora.CONFIGS[a.config](a.scale)
+    ds = D.upload(buf, hnd)
 out = D.sort(ds, want_lcps=True)
 torch.cuda.synchronize()
 print("one sort done", a.config, len(hnd))
