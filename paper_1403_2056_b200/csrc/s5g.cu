@@ -642,61 +642,91 @@ __global__ void __launch_bounds__(SC_NT, 2) k_step_cta(
     const SegDev sg = segs[blockIdx.x];
     if (sg.n > MED_MAX) return;  // device-wide path
     const int n = sg.n;
-    const int64_t lo = sg.lo, depth = sg.depth;
+    const int64_t lo = sg.lo;
+    int64_t depth = sg.depth;
     const bool in_b = sg.flags & SEG_IN_B;
     Rec* X = (in_b ? recB : recA) + lo;
     Rec* Y = (in_b ? recA : recB) + lo;
-    const int nvalid = sg.flags & SEG_NV_MASK;
+    int nvalid = sg.flags & SEG_NV_MASK;
     const int v = (int)gpu_tree_capacity(n, vcap), L = levels_of(v), nb = 2 * v + 1;
     const int count = sample_count(v);
     int P = 1;
     while (P < count) P <<= 1;
     const int lane = threadIdx.x & 31;
     unsigned my_fetch = 0;
-    // ---- refill the cached words when the segment ran out of them --------
-    if (!nvalid) {
-        for (int i = threadIdx.x; i < n; i += SC_NT) {
-            uint64_t wv[3];
-            load_words3(arena, alen, X[i].h, depth, wv);
-            X[i].w[0] = wv[0];
-            X[i].w[1] = wv[1];
-            X[i].w[2] = wv[2];
-            my_fetch += 3;
+    __shared__ int s_all_in;  // the one bucket holding every string, or -1
+    for (;;) {
+        // ---- refill the cached words when the segment ran out of them ----
+        if (!nvalid) {
+            for (int i = threadIdx.x; i < n; i += SC_NT) {
+                uint64_t wv[3];
+                load_words3(arena, alen, X[i].h, depth, wv);
+                X[i].w[0] = wv[0];
+                X[i].w[1] = wv[1];
+                X[i].w[2] = wv[2];
+                my_fetch += 3;
+            }
+            nvalid = NCACHE;
+            __syncthreads();  // the CTA's own record writes are visible after this
         }
-        __syncthreads();  // the CTA's own record writes are visible after this
-    }
-    // ---- draw_sample + select_splitters (ssss.py:76-146) -----------------
-    const uint64_t key0 = splitmix64(seed ^ splitmix64(lo ^ splitmix64((uint64_t)n ^ splitmix64(depth))));
-    for (int j = threadIdx.x; j < P; j += SC_NT)
-        S.s[j] = j < count ? X[splitmix64(key0 + j) % (uint64_t)n].w[0] : ~0ull;
-    for (int b = threadIdx.x; b < SC_R; b += SC_NT) S.hist[b] = 0;
-    __syncthreads();
-    bitonic_u64<SC_NT>(S.s, P);
-    select_tree<SC_NT>(S.s, count, v, L, S.sa, S.sb, S.sp, S.tree, S.inorder, S.tpos, S.eqb);
-    __syncthreads();
-    // ---- classify + bucket counts (ssss.py:149-181, 292) -----------------
-    constexpr int CU = 4;  // keys in flight per thread
-    for (int base = 0; base < n; base += SC_NT * CU) {
-        uint64_t key[CU];
+        // ---- draw_sample + select_splitters (ssss.py:76-146) -------------
+        const uint64_t key0 = splitmix64(seed ^ splitmix64(lo ^ splitmix64((uint64_t)n ^ splitmix64(depth))));
+        for (int j = threadIdx.x; j < P; j += SC_NT)
+            S.s[j] = j < count ? X[splitmix64(key0 + j) % (uint64_t)n].w[0] : ~0ull;
+        for (int b = threadIdx.x; b < SC_R; b += SC_NT) S.hist[b] = 0;
+        if (threadIdx.x == 0) s_all_in = -1;
+        __syncthreads();
+        bitonic_u64<SC_NT>(S.s, P);
+        select_tree<SC_NT>(S.s, count, v, L, S.sa, S.sb, S.sp, S.tree, S.inorder, S.tpos, S.eqb);
+        __syncthreads();
+        // ---- classify + bucket counts (ssss.py:149-181, 292) -------------
+        constexpr int CU = 4;  // keys in flight per thread
+        for (int base = 0; base < n; base += SC_NT * CU) {
+            uint64_t key[CU];
 #pragma unroll
-        for (int u = 0; u < CU; u++) {
-            const int i = base + u * SC_NT + threadIdx.x;
-            key[u] = i < n ? X[i].w[0] : 0;
-        }
+            for (int u = 0; u < CU; u++) {
+                const int i = base + u * SC_NT + threadIdx.x;
+                key[u] = i < n ? X[i].w[0] : 0;
+            }
 #pragma unroll
-        for (int u = 0; u < CU; u++) {
-            const int i = base + u * SC_NT + threadIdx.x;
-            const bool ok = i < n;
-            const uint32_t b = ok ? classify_one<VARIANT>(key[u], S.tree, S.eqb, v, L) : 0;
-            const uint32_t mask = __ballot_sync(0xffffffffu, ok);
-            if (ok) {
-                S.bids[i] = (uint8_t)b;
-                const uint32_t peers = __match_any_sync(mask, b);
-                if (lane == __ffs(peers) - 1) atomicAdd(&S.hist[b], (uint32_t)__popc(peers));
+            for (int u = 0; u < CU; u++) {
+                const int i = base + u * SC_NT + threadIdx.x;
+                const bool ok = i < n;
+                const uint32_t b = ok ? classify_one<VARIANT>(key[u], S.tree, S.eqb, v, L) : 0;
+                const uint32_t mask = __ballot_sync(0xffffffffu, ok);
+                if (ok) {
+                    S.bids[i] = (uint8_t)b;
+                    const uint32_t peers = __match_any_sync(mask, b);
+                    if (lane == __ffs(peers) - 1) atomicAdd(&S.hist[b], (uint32_t)__popc(peers));
+                }
             }
         }
+        __syncthreads();
+        for (int b = threadIdx.x; b < nb; b += SC_NT)
+            if (S.hist[b] == (uint32_t)n) s_all_in = b;
+        __syncthreads();
+        // every string in ONE equality bucket whose splitter holds no
+        // terminator: the stable scatter would be the identity and the only
+        // child the whole segment one word deeper -- advance the depth in
+        // place instead (no scatter, no extra round); duplicate-heavy and
+        // shared-prefix segments (C5's vocabulary words) take this path
+        const int one = s_all_in;
+        if (one >= 0 && (one & 1) && S.tpos[one >> 1] == WORD && depth <= alen) {
+            depth += WORD;
+            if (nvalid > 1)
+                for (int i = threadIdx.x; i < n; i += SC_NT) {
+                    Rec r = X[i];
+                    r.w[0] = r.w[1];
+                    r.w[1] = r.w[2];
+                    r.w[2] = 0;
+                    X[i] = r;
+                }
+            nvalid--;
+            __syncthreads();
+            continue;
+        }
+        break;
     }
-    __syncthreads();
     // ---- bucket starts, children, boundary records (one warp) -----------
     if (threadIdx.x < 32) {
         uint32_t sz[2], run = 0;
@@ -1944,7 +1974,10 @@ struct HostCtx {
         for (size_t off = 0, c = 0; e == cudaSuccess && off < bytes; off += CHUNK, c++) {
             const int k = (int)(c % NSLOT);
             const size_t len = std::min(CHUNK, bytes - off);
-            if (c >= NSLOT) e = cudaEventSynchronize(ev[k]);  // its previous DMA is done
+            // the slot's previous DMA (this call's or an earlier copy's) must
+            // be done before the host overwrites it (a never-recorded event
+            // counts as complete)
+            e = cudaEventSynchronize(ev[k]);
             if (e != cudaSuccess) break;
             par_copy(slot[k], (const uint8_t*)src + off, len);
             e = cudaMemcpyAsync((uint8_t*)dst + off, slot[k], len, cudaMemcpyHostToDevice, st);
