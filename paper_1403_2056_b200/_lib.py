@@ -106,7 +106,10 @@ _lib = None
 def lib(path: Path | None = None):
     global _lib
     if _lib is None:
-        p = Path(path) if path else LIB_PATH
+        import os
+
+        # S5G_LIB: an alternative build of the same library (A/B tuning runs)
+        p = Path(path) if path else Path(os.environ.get("S5G_LIB") or LIB_PATH)
         if not p.exists():
             raise ImportError(
                 f"{p} is missing: build it with `python -m paper_1403_2056_b200.build` "

@@ -622,7 +622,8 @@ __global__ void __launch_bounds__(SC_NT, 2) k_scatter(
 struct StepCtaSmem {
     uint64_t s[16 * (MED_VMAX + 1)];       // sorted sample
     uint64_t tree[MED_VMAX + 1], inorder[MED_VMAX + 1];
-    uint32_t hist[SC_R], bst[SC_R], run_off[SC_R];
+    uint32_t hist[MED_NB + 1], bst[MED_NB + 1], run_off[MED_NB + 1];
+    uint32_t woff[SC_NT / 32][MED_NB + 1];  // per-warp running offsets of the scatter
     uint8_t bids[MED_MAX];  // bucket of every string (<= 63 buckets), from the count pass
     uint16_t eqb[MED_VMAX + 1];
     int16_t sa[MED_VMAX + 1], sb[MED_VMAX + 1], sp[MED_VMAX + 1];
@@ -648,8 +649,8 @@ __global__ void __launch_bounds__(SC_NT, 2) k_step_cta(
     Rec* X = (in_b ? recB : recA) + lo;
     Rec* Y = (in_b ? recA : recB) + lo;
     int nvalid = sg.flags & SEG_NV_MASK;
-    const int v = (int)gpu_tree_capacity(n, vcap), L = levels_of(v), nb = 2 * v + 1;
-    const int count = sample_count(v);
+    const int v = (int)med_tree_capacity(n, vcap), L = levels_of(v), nb = 2 * v + 1;
+    const int count = med_sample_count(v);
     int P = 1;
     while (P < count) P <<= 1;
     const int lane = threadIdx.x & 31;
@@ -673,7 +674,7 @@ __global__ void __launch_bounds__(SC_NT, 2) k_step_cta(
         const uint64_t key0 = splitmix64(seed ^ splitmix64(lo ^ splitmix64((uint64_t)n ^ splitmix64(depth))));
         for (int j = threadIdx.x; j < P; j += SC_NT)
             S.s[j] = j < count ? X[splitmix64(key0 + j) % (uint64_t)n].w[0] : ~0ull;
-        for (int b = threadIdx.x; b < SC_R; b += SC_NT) S.hist[b] = 0;
+        for (int b = threadIdx.x; b <= MED_NB; b += SC_NT) S.hist[b] = 0;
         if (threadIdx.x == 0) s_all_in = -1;
         __syncthreads();
         bitonic_u64<SC_NT>(S.s, P);
@@ -729,13 +730,14 @@ __global__ void __launch_bounds__(SC_NT, 2) k_step_cta(
     }
     // ---- bucket starts, children, boundary records (one warp) -----------
     if (threadIdx.x < 32) {
-        uint32_t sz[2], run = 0;
+        constexpr int BPL = (MED_NB + 31) / 32;  // buckets per lane
+        uint32_t sz[BPL], run = 0, mine = 0;
 #pragma unroll
-        for (int k = 0; k < 2; k++) {
-            const int b = lane * 2 + k;
+        for (int k = 0; k < BPL; k++) {
+            const int b = lane * BPL + k;
             sz[k] = b < nb ? S.hist[b] : 0;
+            mine += sz[k];
         }
-        const uint32_t mine = sz[0] + sz[1];
         uint32_t incl = mine;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -744,9 +746,9 @@ __global__ void __launch_bounds__(SC_NT, 2) k_step_cta(
         }
         run = incl - mine;
         const int nv = nvalid ? nvalid : NCACHE;
-#pragma unroll
-        for (int k = 0; k < 2; k++) {
-            const int b = lane * 2 + k;
+#pragma unroll 1
+        for (int k = 0; k < BPL; k++) {
+            const int b = lane * BPL + k;
             if (b < nb) {
                 S.bst[b] = run;
                 S.run_off[b] = run;
@@ -778,44 +780,68 @@ __global__ void __launch_bounds__(SC_NT, 2) k_step_cta(
         }
     }
     __syncthreads();
-    // ---- stable scatter: 64-string chunks update the offsets in chunk order
-    // (the turn chain of k_scatter); bucket ids are recomputed here
+    // ---- stable scatter without a turn chain: warp w owns the contiguous
+    // range [w*per, (w+1)*per) of the segment; per-warp bucket counts (from
+    // the ids in shared memory) scanned bucket-major / warp-minor give every
+    // warp its own running offsets, so warps never wait on each other
     {
+        constexpr int NW = SC_NT / 32;
         const int w = threadIdx.x >> 5;
         const uint32_t lt = lanemask_lt();
+        const int per = (n + NW - 1) / NW;
+        const int r0 = min(n, w * per), r1 = min(n, r0 + per);
+        for (int b = lane; b < nb; b += 32) S.woff[w][b] = 0;
+        __syncwarp();
+        for (int e0 = r0; e0 < r1; e0 += 32) {
+            const int e = e0 + lane;
+            const bool ok = e < r1;
+            const uint32_t m = __ballot_sync(0xffffffffu, ok);
+            if (ok) {
+                const uint32_t b = S.bids[e];
+                const uint32_t peers = __match_any_sync(m, b);
+                if (lane == __ffs(peers) - 1) S.woff[w][b] += __popc(peers);
+            }
+            __syncwarp();
+        }
         __syncthreads();
-        for (int c0 = w * SCX_CHUNK, tn = w; c0 < n; c0 += SCX_SUB, tn += SC_NT / 32) {
-            // bucket ids from shared memory: the turn never waits on a load
-            Rec rec[SCX_IT];
-            uint32_t myb[SCX_IT], peers[SCX_IT];
+        for (int b = threadIdx.x; b < nb; b += SC_NT) {
+            uint32_t run = S.bst[b];
 #pragma unroll
-            for (int j = 0; j < SCX_IT; j++) {
-                const int e = c0 + j * 32 + lane;
+            for (int q = 0; q < NW; q++) {
+                const uint32_t t = S.woff[q][b];
+                S.woff[q][b] = run;
+                run += t;
+            }
+        }
+        __syncthreads();
+        constexpr int IT = SCX_IT;  // rounds of 32 whose loads are issued together
+        for (int e0 = r0; e0 < r1; e0 += 32 * IT) {
+            Rec rec[IT];
+            uint32_t myb[IT], rel[IT];
+#pragma unroll
+            for (int j = 0; j < IT; j++) {
+                const int e = e0 + j * 32 + lane;
                 myb[j] = BID_SENTINEL;
-                if (e < n) {
+                if (e < r1) {
                     rec[j] = X[e];
                     myb[j] = S.bids[e];
                 }
             }
 #pragma unroll
-            for (int j = 0; j < SCX_IT; j++) peers[j] = __match_any_sync(0xffffffffu, myb[j]);
-            if (tn) turn_wait(w);
-            uint32_t rel[SCX_IT];
-#pragma unroll
-            for (int j = 0; j < SCX_IT; j++) {
-                const int leader = __ffs(peers[j]) - 1;
+            for (int j = 0; j < IT; j++) {
+                const uint32_t peers = __match_any_sync(0xffffffffu, myb[j]);
+                const int leader = __ffs(peers) - 1;
                 uint32_t base = 0;
                 if (lane == leader && myb[j] != BID_SENTINEL) {
-                    base = S.run_off[myb[j]];
-                    S.run_off[myb[j]] = base + __popc(peers[j]);
+                    base = S.woff[w][myb[j]];
+                    S.woff[w][myb[j]] = base + __popc(peers);
                 }
                 base = __shfl_sync(0xffffffffu, base, leader);
-                rel[j] = base + __popc(peers[j] & lt);
+                rel[j] = base + __popc(peers & lt);
                 __syncwarp();
             }
-            turn_pass(w);
 #pragma unroll
-            for (int j = 0; j < SCX_IT; j++) {
+            for (int j = 0; j < IT; j++) {
                 const uint32_t b = myb[j];
                 if (b == BID_SENTINEL) continue;
                 const uint32_t size = S.hist[b];
@@ -837,7 +863,6 @@ __global__ void __launch_bounds__(SC_NT, 2) k_step_cta(
             }
         }
     }
-    // (no __syncthreads after the turn chain: barrier 0 may hold a hand-off)
     my_fetch = __reduce_add_sync(0xffffffffu, my_fetch);
     if (lane == 0 && my_fetch) atomicAdd(&ctr->fetches, (unsigned long long)my_fetch);
 }

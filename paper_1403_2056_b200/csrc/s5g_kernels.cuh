@@ -111,7 +111,31 @@ __host__ __device__ inline int sample_count(int64_t v) {
 
 // segments a single CTA takes through a whole S^5 step (k_step_cta)
 constexpr int MED_MAX = TILE;
-constexpr int MED_VMAX = 31;   // gpu_tree_capacity(MED_MAX) -> <= 63 buckets
+#ifndef MED_VMAX_CFG
+#define MED_VMAX_CFG 31
+#endif
+#ifndef MED_TARGET_CFG
+#define MED_TARGET_CFG 1024
+#endif
+constexpr int MED_VMAX = MED_VMAX_CFG;  // <= 2*MED_VMAX+1 <= 255 buckets (uint8 ids)
+constexpr int MED_NB = 2 * MED_VMAX + 1;
+constexpr int MED_TARGET = MED_TARGET_CFG;  // strings per bucket a fused step aims at
+static_assert(MED_NB <= 255, "k_step_cta keeps bucket ids in uint8");
+
+// Splitters of a fused single-CTA step: buckets of about MED_TARGET strings,
+// so its children mostly go straight to the warp finishers (a coarser split
+// sent C5's 4096-string segments through another CTA-wide sort level).
+__host__ __device__ inline int64_t med_tree_capacity(int64_t n, int64_t vcap) {
+    int64_t want = 1;
+    while (want < MED_VMAX && (want + 1) * MED_TARGET < n) want = 2 * want + 1;
+    const int64_t t = tree_capacity(n, vcap);
+    return want < t ? want : t;
+}
+__host__ __device__ inline int med_sample_count(int64_t v) {
+    const int a = sample_count(v);
+    const int cap = 4 * (int)(v + 1) - 1;
+    return a < cap ? a : cap;
+}
 
 __host__ __device__ inline int size_class(int64_t n) {
     return n <= 32 ? 0 : n <= 64 ? 1 : n <= 128 ? 2 : n <= 256 ? 3 : n <= 512 ? 4 : n <= 1024 ? 5 : 6;

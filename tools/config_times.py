@@ -11,14 +11,18 @@ from paper_1403_2056_b200 import corpora  # noqa: E402
 from paper_1403_2056_b200 import device as D  # noqa: E402
 
 ap = argparse.ArgumentParser()
-ap.add_argument("--configs", default="c1_random,c2_dna,c3_urls,c4_suffixes,c5_nodup:0.0625")
+ap.add_argument("--configs", default="c1_random,c2_dna,c3_urls,c4_suffixes,c5_nodup")
 ap.add_argument("--reps", type=int, default=7)
 a = ap.parse_args()
 for spec in a.configs.split(","):
     name, _, sc = spec.partition(":")
     scale = float(sc) if sc else 1.0
-    buf, hnd = corpora.CONFIGS[name](scale)
-    ds = D.upload(buf, hnd)
+    if name == "c5_nodup":  # generated in HBM
+        arena, alen, hd = corpora.gen_nodup_device(int((1 << 28) * scale))
+        ds, hnd = D.DeviceStrings(arena, alen, hd), hd
+    else:
+        buf, hnd = corpora.CONFIGS[name](scale)
+        ds = D.upload(buf, hnd)
     ws = torch.empty(D.workspace_bytes(len(hnd), 1 << 20), dtype=torch.uint8, device="cuda")
     out = (torch.empty(len(hnd), dtype=torch.int64, device="cuda"),
            torch.empty(len(hnd), dtype=torch.int64, device="cuda"))
