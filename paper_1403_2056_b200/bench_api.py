@@ -12,7 +12,12 @@ def _algo_gpu_s5(sset, threads, seed, stats):
 
 
 def _algo_gpu_ps5(sset, threads, seed, stats):
-    return parallel_s5(sset, p=threads, seed=seed, stats=stats)
+    # the harness's worker count becomes the GPU count, capped at the visible
+    # devices (parallel_s5's p counts GPUs)
+    from .parallel import visible_devices
+
+    return parallel_s5(sset, p=max(1, min(int(threads or 1), visible_devices())), seed=seed,
+                       stats=stats)
 
 
 def register_with_strsort() -> bool:

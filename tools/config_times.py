@@ -13,6 +13,7 @@ from paper_1403_2056_b200 import device as D  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--configs", default="c1_random,c2_dna,c3_urls,c4_suffixes,c5_nodup")
 ap.add_argument("--reps", type=int, default=7)
+ap.add_argument("--v", type=int, default=8191, help="splitter cap (tuning only)")
 a = ap.parse_args()
 for spec in a.configs.split(","):
     name, _, sc = spec.partition(":")
@@ -27,12 +28,12 @@ for spec in a.configs.split(","):
     out = (torch.empty(len(hnd), dtype=torch.int64, device="cuda"),
            torch.empty(len(hnd), dtype=torch.int64, device="cuda"))
     for _ in range(2):
-        D.sort(ds, want_lcps=True, out=out, workspace=ws)
+        D.sort(ds, want_lcps=True, out=out, workspace=ws, v=a.v)
     ts = []
     for _ in range(a.reps):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        D.sort(ds, want_lcps=True, out=out, workspace=ws)
+        D.sort(ds, want_lcps=True, out=out, workspace=ws, v=a.v)
         e1.record()
         torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1))
