@@ -290,16 +290,38 @@ def dist_stats_device(ds, out_h, lcps):
     return DV.dist_stats(lcps)
 
 
+def load_slice(name: str, scale: float, lo: int, hi: int, dev):
+    """Strings [lo, hi) of the workload as one rank's shard: (DeviceStrings,
+    host buffer, host handles relative to the slice).  C5 is generated
+    straight into HBM from its counter-based definition (the slice only);
+    the other configs are generated on the host and cut."""
+    import torch
+
+    from paper_1403_2056_b200 import corpora
+    from paper_1403_2056_b200 import device as DV
+
+    if name == "c5_nodup":
+        arena, alen, h = corpora.gen_nodup_device(hi - lo, 4, dev, n0=lo)
+        buf = torch.empty(max(alen, 1), dtype=torch.uint8, pin_memory=True)[:alen]
+        buf.copy_(arena[:alen])
+        return DV.DeviceStrings(arena, alen, h), buf.numpy(), h.cpu().numpy()
+    buf, hnd = corpora.CONFIGS[name](scale)
+    end = int(hnd[hi]) if hi < len(hnd) else len(buf)
+    b0 = int(hnd[lo]) if lo < len(hnd) else end
+    sb, sh = buf[b0:end], hnd[lo:hi] - b0
+    return DV.upload(sb, sh, dev), sb, sh
+
+
 def run_dist(args):
-    """N > 1 (torchrun): weak scaling -- every rank owns a 2^24-string shard of
-    the workload (seed + rank); one step is the full multi-GPU sort (sample,
-    partition, NCCL all-to-all, local S^5, boundary LCP), timed on the device
-    and reported as the max over ranks."""
+    """N > 1 (torchrun): STRONG scaling of one global corpus -- rank r owns
+    the contiguous slice [r n / N, (r+1) n / N) of the workload (C5: generated
+    on its own GPU); one step is the whole multi-GPU sort (sample, partition,
+    NCCL all-to-all of bytes + global indices over NVLink, local S^5,
+    boundary LCP), timed on the device and reported as the max over ranks."""
     import torch
     import torch.distributed as dist
 
     from paper_1403_2056_b200 import _lib
-    from paper_1403_2056_b200 import corpora
     from paper_1403_2056_b200 import device as DV
     from paper_1403_2056_b200.dist import GpuBackend, Shard, distributed_merge_sort, distributed_sort
 
@@ -307,25 +329,26 @@ def run_dist(args):
     torch.cuda.set_device(local)
     dist.init_process_group("nccl")
     dev = torch.device("cuda", local)
-    gen = {"c1_random": lambda s: corpora.gen_random(int(1_000_000 * args.scale), s),
-           "c2_dna": lambda s: corpora.gen_dna(int((1 << 24) * args.scale), 100, s),
-           "c3_urls": lambda s: corpora.gen_urls(int((1 << 23) * args.scale), s),
-           "c5_nodup": lambda s: corpora.gen_nodup(int((1 << 28) * args.scale), s)}[args.config]
-    seed0 = {"c1_random": 0, "c2_dna": 1, "c3_urls": 2, "c5_nodup": 4}[args.config]
-    buf, hnd = gen(seed0 + rank)
-    n = len(hnd)
-    ds = DV.upload(buf, hnd, dev)
-    shard = Shard(ds, hnd, rank * n)
+    n_total = config_n(args.config, args.scale)
+    lo, hi = rank * n_total // world, (rank + 1) * n_total // world
+    ds, hbuf, hhnd = load_slice(args.config, args.scale, lo, hi, dev)
     be = GpuBackend(dev)
+    xstats: dict = {}
 
-    def step():
+    def step(shard):
         if args.strategy == "merge":  # partitioned_merge_sort across ranks
             return distributed_merge_sort(shard, be)
-        return distributed_sort(shard, be, want_lcps=True)
+        return distributed_sort(shard, be, want_lcps=True, stats=xstats)
 
+    shard = Shard(ds, hhnd, lo)
     for _ in range(args.warmup):
-        step()
+        res = step(shard)
     torch.cuda.synchronize()
+    # D of the whole job from the ranks' exact LCP arrays (strset.py:290-309)
+    D_loc, L_loc = DV.dist_stats(res.lcps.clamp(min=0)) if res.lcps is not None and res.lcps.numel() else (0, 0)
+    red = torch.tensor([D_loc, L_loc, xstats.get("sent_bytes", 0)], dtype=torch.int64, device=dev)
+    dist.all_reduce(red)
+    D_all, L_all, sent_all = (int(x) for x in red.tolist())
     l0 = _lib.launch_count()
     with ClockSampler(local) as clk:
         dist.barrier()
@@ -334,7 +357,7 @@ def run_dist(args):
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
         for _ in range(args.steps):
-            res = step()
+            res = step(shard)
         e1.record()
         torch.cuda.synchronize()
         dist.barrier()
@@ -342,24 +365,71 @@ def run_dist(args):
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     ms_step = float(ms.item()) / args.steps
     launches = _lib.launch_count() - l0
-    total = res.n_total
     peak, peak_src = hbm_peak()
+    t = ms_step / 1000.0
+    sort_gbs = b_alg(n_total, D_all) / t / 1e9
+
+    # end to end through the public API on host buffers: every step uploads
+    # each rank's slice from pinned memory, sorts across the ranks and reads
+    # back the sorted global indices and LCPs
+    e2e = None
+    if not args.no_e2e:
+        pin_h = torch.empty(max(len(hhnd), 1), dtype=torch.int64, pin_memory=True)[:len(hhnd)]
+        pin_h.numpy()[:] = hhnd
+        ts = []
+        for it in range(max(1, min(args.steps, 3)) + 1):
+            dist.barrier()
+            torch.cuda.synchronize()
+            s0 = torch.cuda.Event(enable_timing=True)
+            s1 = torch.cuda.Event(enable_timing=True)
+            s0.record()
+            dsh = DV.upload(hbuf, pin_h.numpy(), dev)
+            r2 = step(Shard(dsh, hhnd, lo))
+            g_host, l_host = r2.gidx.cpu(), r2.lcps.cpu()
+            s1.record()
+            torch.cuda.synchronize()
+            tt = torch.tensor([s0.elapsed_time(s1)], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            if it:
+                ts.append(float(tt.item()))
+            del dsh, r2
+        e2e = {"value": n_total / (statistics.median(ts) / 1000.0), "unit": UNIT,
+               "h2d_bytes_per_step": int(len(hbuf) + 8 * len(hhnd)),
+               "d2h_bytes_per_step": int(16 * res.gidx.numel()),
+               "ms_per_step": statistics.median(ts), "per": "rank 0's bytes; time = max over ranks",
+               "call": "dist.distributed_sort on each rank's uploaded shard (NCCL)"}
+    cpu_line = None
+    if rank == 0 and not args.no_cpu_baseline:
+        # the same CPU leg as at N = 1 (the oracle port on all host cores)
+        threads = os.cpu_count() or 1
+        buf_all, hnd_all = load_config(args.config, args.scale)
+        rate, times = cpu_reference(buf_all, hnd_all, len(hnd_all), 1, threads)
+        cpu_line = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
+                    "sample": f"all {len(hnd_all)} strings of {args.config}, 1 rep, {times[0]:.2f} s "
+                              f"(oracle/s5_oracle.c parallel_s5, {threads} OpenMP threads)"}
+        del buf_all, hnd_all
     line = {
-        "metric": METRIC, "value": total / (ms_step / 1000.0), "unit": UNIT, "n_gpus": world,
+        "metric": METRIC, "value": n_total / t, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8",
         "data": "synthetic",
-        "config": {"workload": args.config, "n_per_rank": n, "n_total": total,
+        "config": {"workload": args.config, "n": n_total, "n_per_rank": hi - lo, "scale": args.scale,
+                   "D": D_all, "L": L_all,
                    "parallelism": f"dp{world} (" + ("local S^5 + sampled cuts + NCCL all-to-all of "
                                                      "sorted pieces + K-way LCP merge"
                                                      if args.strategy == "merge" else
                                                      "sample-sort partition + NCCL all-to-all") + ")",
                    "l2": "inputs larger than L2 (arena > 126 MB), no flush"},
-        "roofline": {"bound": "hbm", "kernel": "whole multi-GPU sort", "achieved": None,
-                     "peak": peak, "unit": "GB/s", "frac": None, "traffic": None,
-                     "peak_source": peak_src},
-        "gpu_launches": int(launches), "clocks": clk.summary(), "cpu_baseline": None,
-        "e2e": None,
+        "roofline": {"bound": "hbm", "kernel": "whole multi-GPU sort",
+                     "achieved": sort_gbs / world, "peak": peak, "unit": "GB/s per GPU",
+                     "frac": sort_gbs / world / peak, "traffic": None, "peak_source": peak_src,
+                     "bytes_model": "B_alg = 24 (floor(D/8) + n) + 8 n over all ranks (SURVEY 8d)"},
+        "nvlink": {"sent_bytes_per_step": sent_all, "peak_gbs_per_gpu": 900.0,
+                   "frac": (sent_all / world / 900e9) / t if t > 0 else None,
+                   "model": "X = bytes each rank sends to the others (strings + 24 B/string); "
+                            "frac = X / (N * 900 GB/s) / step time"},
+        "gpu_launches": int(launches), "clocks": clk.summary(), "cpu_baseline": cpu_line,
+        "e2e": e2e,
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -549,10 +619,12 @@ def main(argv=None):
     ap.add_argument("--l2-fetch", type=int, default=32)
     ap.add_argument("--strategy", choices=["sample", "merge"], default="sample",
                     help="N > 1: sample-sort exchange (default) or local sort + LCP merge")
+    ap.add_argument("--dist", action="store_true",
+                    help="run the multi-GPU (torchrun) code path even at N = 1 (checks)")
     args = ap.parse_args(argv)
     if args.impl == "reference":
         return run_reference(args)
-    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1 or args.dist:
         return run_dist(args)
     return run_ours(args)
 

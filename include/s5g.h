@@ -172,7 +172,8 @@ int s5g_lengths(const uint8_t *arena, int64_t arena_len, const int64_t *handles,
                 int64_t *out_len, void *stream);
 
 /* Pack strings with their terminators into dst at dst_off[i] (the send
- * buffer of the multi-GPU exchange). */
+ * buffer of the multi-GPU exchange).  lengths may be NULL when dst_off has
+ * n + 1 entries (sizes = offset differences, as s5g_pack_plan writes). */
 int s5g_pack(const uint8_t *arena, int64_t arena_len, const int64_t *handles,
              const int64_t *lengths, const int64_t *dst_off, int64_t n, uint8_t *dst,
              void *stream);
@@ -201,6 +202,31 @@ int s5g_group_by_dest(const int32_t *dest, int64_t n, int32_t G, int64_t *out_or
  * then out_pos[j] = map[query[j]].  Device pointers. */
 int s5g_positions(const int64_t *handles, int64_t n, const int64_t *query, int64_t m,
                   int32_t *map, int64_t map_len, int64_t *out_pos, void *stream);
+
+/* Input position of every sorted handle: out_pos[j] = i with
+ * in_handles[i] the string at out_handles[j], for a stable sort's output
+ * (equal handles -- the same string -- are matched in input order, so
+ * repeated handles are fine).  Two stable radix sorts by handle; O(n), no
+ * per-byte map.  max_handle bounds the handles (e.g. arena_len).  Device
+ * pointers; workspace: s5g_input_positions_workspace_bytes(n). */
+size_t s5g_input_positions_workspace_bytes(int64_t n);
+int s5g_input_positions(const int64_t *in_handles, const int64_t *out_handles, int64_t n,
+                        int64_t max_handle, int64_t *out_pos, void *workspace,
+                        size_t workspace_bytes, void *stream);
+
+/* out[k] = src[idx[k]] (device int64 arrays). */
+int s5g_gather_i64(const int64_t *src, const int64_t *idx, int64_t n, int64_t *out, void *stream);
+
+/* Send plan of the multi-GPU exchange: for the strings in send order
+ * (handles[order[k]]): out_handles[k], out_off[0..n] (exclusive byte offsets
+ * incl. terminators; out_off[n] = total) and out_dest_bytes[g] = bytes for
+ * destination g, given counts[g] strings per destination (all device).
+ * Workspace: s5g_pack_plan_workspace_bytes(n). */
+size_t s5g_pack_plan_workspace_bytes(int64_t n);
+int s5g_pack_plan(const uint8_t *arena, int64_t arena_len, const int64_t *handles,
+                  const int64_t *order, int64_t n, const int64_t *counts, int32_t G,
+                  int64_t *out_handles, int64_t *out_off, int64_t *out_dest_bytes,
+                  void *workspace, size_t workspace_bytes, void *stream);
 
 /* dist_stats (strset.py:290-309) of a sorted set from its exact LCP array
  * (device): D and L. */

@@ -89,6 +89,11 @@ SIGNATURES = {
     "s5g_group_workspace_bytes": (C.c_size_t, [_i64, _i32]),
     "s5g_group_by_dest": (C.c_int, [_p, _i64, _i32, _p, _p, _p, C.c_size_t, _p]),
     "s5g_positions": (C.c_int, [_p, _i64, _p, _i64, _p, _i64, _p, _p]),
+    "s5g_input_positions_workspace_bytes": (C.c_size_t, [_i64]),
+    "s5g_input_positions": (C.c_int, [_p, _p, _i64, _i64, _p, _p, C.c_size_t, _p]),
+    "s5g_gather_i64": (C.c_int, [_p, _p, _i64, _p, _p]),
+    "s5g_pack_plan_workspace_bytes": (C.c_size_t, [_i64]),
+    "s5g_pack_plan": (C.c_int, [_p, _i64, _p, _p, _i64, _p, _i32, _p, _p, _p, _p, C.c_size_t, _p]),
     "s5g_kway_merge": (C.c_int, [_p, _i64, _i32, C.POINTER(_i64), _p, _p, _p, _i64, _p, _p, _p,
                                  C.c_size_t, _p, C.POINTER(Stats)]),
     "s5g_last_error": (C.c_char_p, []),

@@ -222,23 +222,24 @@ def gen_nodup(n: int = 1 << 28, seed: int = 4, out: np.ndarray | None = None):
     return buf, hnd
 
 
-def gen_nodup_device(n: int = 1 << 28, seed: int = 4, device=None):
-    """C5 generated directly in HBM (same bytes as gen_nodup): returns
+def gen_nodup_device(n: int = 1 << 28, seed: int = 4, device=None, n0: int = 0):
+    """C5 generated directly in HBM (same bytes as gen_nodup): strings
+    n0 .. n0+n-1 (a rank's contiguous slice of the corpus when n0 > 0), as
     (arena uint8 tensor padded with zeros past arena_len, arena_len, handles
-    int64 tensor) -- the device.DeviceStrings fields."""
+    int64 tensor relative to the slice) -- the device.DeviceStrings fields."""
     import torch
 
     from ._lib import S5G_ARENA_PAD
 
     dev = device or torch.device("cuda", torch.cuda.current_device())
-    total = nodup_bytes(n, seed)
+    total = int(_gen().s5gen_nodup_bytes(n0, n, seed))
     cap = (total + S5G_ARENA_PAD + 15) // 16 * 16
     arena = torch.empty(cap, dtype=torch.uint8, device=dev)
     arena[total:].zero_()
     hnd = torch.empty(max(n, 1), dtype=torch.int64, device=dev)[:n]
     with torch.cuda.device(dev):
         st = torch.cuda.current_stream(dev).cuda_stream
-        _gen_check(_gen().s5gen_nodup_device(0, n, seed, arena.data_ptr(), hnd.data_ptr(), st))
+        _gen_check(_gen().s5gen_nodup_device(n0, n, seed, arena.data_ptr(), hnd.data_ptr(), st))
     return arena, total, hnd
 
 

@@ -18,6 +18,9 @@
 #include <thread>
 #include <vector>
 
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
 #include "s5g.h"
 #include "s5g_kernels.cuh"
 #include "s5g_warpsort.cuh"
@@ -948,7 +951,10 @@ __global__ void k_pack(const uint8_t* __restrict__ arena, int64_t alen,
     const int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (i >= n) return;
-    const int64_t h = handles[i], L = lens[i] + 1, o = dst_off[i];
+    // lens == NULL: sizes from the exclusive offsets (s5g_pack_plan's)
+    const int64_t h = handles[i], o = dst_off[i];
+    const int64_t L = lens ? lens[i] + 1 : dst_off[i + 1] - o;
+    // one warp per string, byte-wise (strings end at arbitrary alignments)
     for (int64_t b = lane; b < L; b += 32) dst[o + b] = b < L - 1 && h + b < alen ? arena[h + b] : 0;
 }
 
@@ -1099,6 +1105,41 @@ __global__ void k_pos_gather(const int64_t* __restrict__ query, int64_t m,
                              const int32_t* __restrict__ map, int64_t* __restrict__ out) {
     const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (j < m) out[j] = map[query[j]];
+}
+
+__global__ void k_iota_i32(int32_t* __restrict__ out, int64_t n) {
+    const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (j < n) out[j] = (int32_t)j;
+}
+__global__ void k_pos_match(const int32_t* __restrict__ in_pos, const int32_t* __restrict__ out_idx,
+                            int64_t n, int64_t* __restrict__ out_pos) {
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k < n) out_pos[out_idx[k]] = in_pos[k];
+}
+// exchange plan: handle and size (with terminator) of the k-th string in
+// send order
+__global__ void k_plan_sizes(const uint8_t* __restrict__ arena, int64_t alen,
+                             const int64_t* __restrict__ handles, const int64_t* __restrict__ order,
+                             int64_t n, int64_t* __restrict__ out_h, int64_t* __restrict__ size) {
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const int64_t h = handles[order[k]];
+    out_h[k] = h;
+    int64_t e = h;
+    while (e < alen && arena[e]) e++;
+    size[k] = e - h + 1;
+}
+// bytes per destination from the exclusive offsets (off[n] = total)
+__global__ void k_plan_dest(const int64_t* __restrict__ off, int64_t n,
+                            const int64_t* __restrict__ counts, int32_t G,
+                            int64_t* __restrict__ dest_bytes) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    int64_t a = 0;
+    for (int g = 0; g < G; g++) {
+        const int64_t b = a + counts[g];
+        dest_bytes[g] = off[b] - off[a];
+        a = b;
+    }
 }
 
 __global__ void k_gather_i64(const int64_t* __restrict__ src, const int64_t* __restrict__ idx,
@@ -2525,6 +2566,90 @@ int s5g_positions(const int64_t* handles, int64_t n, const int64_t* query, int64
     g_launches += 2;
     if (n) k_pos_scatter<<<blocks_for(n, 256), 256, 0, st>>>(handles, n, map);
     if (m) k_pos_gather<<<blocks_for(m, 256), 256, 0, st>>>(query, m, map, out_pos);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(st));
+    return 0;
+}
+
+static int bits_for(int64_t x) {
+    int b = 1;
+    while (b < 63 && (x >> b)) b++;
+    return b;
+}
+
+size_t s5g_input_positions_workspace_bytes(int64_t n) {
+    const int64_t nn = std::max<int64_t>(n, 1);
+    size_t t1 = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, t1, (const int64_t*)nullptr, (int64_t*)nullptr,
+                                    (const int32_t*)nullptr, (int32_t*)nullptr, (int)std::min<int64_t>(nn, INT32_MAX));
+    return 2 * 8 * (size_t)nn + 3 * 4 * (size_t)nn + t1 + 4 * 256;
+}
+
+int s5g_input_positions(const int64_t* in_handles, const int64_t* out_handles, int64_t n,
+                        int64_t max_handle, int64_t* out_pos, void* workspace,
+                        size_t workspace_bytes, void* stream) {
+    if (n < 0) return fail(S5G_E_INVALID, "negative n");
+    if (n > INT32_MAX) return fail(S5G_E_INVALID, "n exceeds 2^31-1");
+    if (n == 0) return 0;
+    if (workspace_bytes < s5g_input_positions_workspace_bytes(n))
+        return fail(S5G_E_WORKSPACE, "workspace too small");
+    cudaStream_t st = (cudaStream_t)stream;
+    uint8_t* w = (uint8_t*)workspace;
+    auto take = [&](size_t b) { uint8_t* p = w; w += (b + 255) & ~size_t(255); return p; };
+    int64_t* k_in = (int64_t*)take(8 * n);
+    int64_t* k_out = (int64_t*)take(8 * n);
+    int32_t* iota = (int32_t*)take(4 * n);
+    int32_t* v_in = (int32_t*)take(4 * n);
+    int32_t* v_out = (int32_t*)take(4 * n);
+    size_t tb = 0;
+    const int end_bit = bits_for(std::max<int64_t>(max_handle, 1));
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, in_handles, k_in, iota, v_in, (int)n, 0, end_bit, st));
+    void* tmp = take(tb);
+    g_launches += 6;
+    k_iota_i32<<<blocks_for(n, 256), 256, 0, st>>>(iota, n);
+    // stable sorts by handle: the k-th occurrence of a handle in input order
+    // and the k-th in output order are the same string (equal handles are
+    // equal strings, kept in input order by the stable sort)
+    CK(cub::DeviceRadixSort::SortPairs(tmp, tb, in_handles, k_in, iota, v_in, (int)n, 0, end_bit, st));
+    CK(cub::DeviceRadixSort::SortPairs(tmp, tb, out_handles, k_out, iota, v_out, (int)n, 0, end_bit, st));
+    k_pos_match<<<blocks_for(n, 256), 256, 0, st>>>(v_in, v_out, n, out_pos);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(st));
+    return 0;
+}
+
+int s5g_gather_i64(const int64_t* src, const int64_t* idx, int64_t n, int64_t* out, void* stream) {
+    if (n <= 0) return n < 0 ? fail(S5G_E_INVALID, "negative n") : 0;
+    cudaStream_t st = (cudaStream_t)stream;
+    g_launches++;
+    k_gather_i64<<<blocks_for(n, 256), 256, 0, st>>>(src, idx, n, out);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(st));
+    return 0;
+}
+
+size_t s5g_pack_plan_workspace_bytes(int64_t n) {
+    size_t t = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, t, (int64_t*)nullptr, (int64_t*)nullptr,
+                                  std::max<int64_t>(n, 1) + 1);
+    return 8 * (size_t)(std::max<int64_t>(n, 1) + 1) + t + 256;
+}
+
+int s5g_pack_plan(const uint8_t* arena, int64_t arena_len, const int64_t* handles,
+                  const int64_t* order, int64_t n, const int64_t* counts, int32_t G,
+                  int64_t* out_handles, int64_t* out_off, int64_t* out_dest_bytes,
+                  void* workspace, size_t workspace_bytes, void* stream) {
+    if (n < 0 || G < 1) return fail(S5G_E_INVALID, "bad size");
+    if (workspace_bytes < s5g_pack_plan_workspace_bytes(n)) return fail(S5G_E_WORKSPACE, "workspace too small");
+    cudaStream_t st = (cudaStream_t)stream;
+    int64_t* size = (int64_t*)workspace;
+    void* tmp = (uint8_t*)workspace + ((8 * (size_t)(std::max<int64_t>(n, 1) + 1) + 255) & ~size_t(255));
+    size_t tb = workspace_bytes - ((8 * (size_t)(std::max<int64_t>(n, 1) + 1) + 255) & ~size_t(255));
+    g_launches += 3;
+    CK(cudaMemsetAsync(size + n, 0, 8, st));
+    if (n) k_plan_sizes<<<blocks_for(n, 256), 256, 0, st>>>(arena, arena_len, handles, order, n, out_handles, size);
+    CK(cub::DeviceScan::ExclusiveSum(tmp, tb, size, out_off, n + 1, st));
+    k_plan_dest<<<1, 32, 0, st>>>(out_off, n, counts, G, out_dest_bytes);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(st));
     return 0;

@@ -318,3 +318,54 @@ def positions(handles: torch.Tensor, query: torch.Tensor, map_len: int) -> torch
                               mp.data_ptr(), map_len, out.data_ptr(),
                               torch.cuda.current_stream(dev).cuda_stream))
     return out
+
+
+def input_positions(in_handles: torch.Tensor, out_handles: torch.Tensor, max_handle: int) -> torch.Tensor:
+    """Input position of every sorted handle of a stable sort's output
+    (s5g_input_positions: two stable radix sorts by handle; repeated handles
+    -- the same string -- are matched in input order)."""
+    n = in_handles.numel()
+    dev = in_handles.device
+    out = torch.empty(n, dtype=torch.int64, device=dev)
+    if n == 0:
+        return out
+    ws = torch.empty(int(lib().s5g_input_positions_workspace_bytes(n)), dtype=torch.uint8, device=dev)
+    check(lib().s5g_input_positions(in_handles.data_ptr(), out_handles.data_ptr(), n,
+                                    int(max(max_handle, 1)), out.data_ptr(), ws.data_ptr(),
+                                    ws.numel(), torch.cuda.current_stream(dev).cuda_stream))
+    return out
+
+
+def gather_i64(src: torch.Tensor, idx: torch.Tensor) -> torch.Tensor:
+    """src[idx] for int64 device arrays (s5g_gather_i64)."""
+    out = torch.empty(idx.numel(), dtype=torch.int64, device=src.device)
+    if idx.numel():
+        check(lib().s5g_gather_i64(src.data_ptr(), idx.contiguous().data_ptr(), idx.numel(),
+                                   out.data_ptr(), torch.cuda.current_stream(src.device).cuda_stream))
+    return out
+
+
+def pack_order(ds: DeviceStrings, order: torch.Tensor, counts: list[int]):
+    """The exchange's send buffer: strings handles[order[k]] (with their
+    terminators) back to back, and the bytes per destination
+    (s5g_pack_plan + s5g_pack)."""
+    n = order.numel()
+    dev = ds.handles.device
+    G = len(counts)
+    cnt = torch.tensor(counts, dtype=torch.int64, device=dev)
+    h = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
+    off = torch.empty(n + 1, dtype=torch.int64, device=dev)
+    dest = torch.empty(G, dtype=torch.int64, device=dev)
+    ws = torch.empty(int(lib().s5g_pack_plan_workspace_bytes(n)), dtype=torch.uint8, device=dev)
+    st = torch.cuda.current_stream(dev).cuda_stream
+    check(lib().s5g_pack_plan(ds.arena.data_ptr(), ds.arena_len, ds.handles.data_ptr(),
+                              order.contiguous().data_ptr() if n else None, n, cnt.data_ptr(), G,
+                              h.data_ptr(), off.data_ptr(), dest.data_ptr(), ws.data_ptr(),
+                              ws.numel(), st))
+    dest_h = dest.cpu().tolist()
+    total = int(sum(dest_h))
+    payload = torch.empty(max(total, 1), dtype=torch.uint8, device=dev)
+    if n:
+        check(lib().s5g_pack(ds.arena.data_ptr(), ds.arena_len, h.data_ptr(), None, off.data_ptr(),
+                             n, payload.data_ptr(), st))
+    return payload[:total], [int(x) for x in dest_h]

@@ -93,6 +93,47 @@ def _alltoallv(send: torch.Tensor, send_counts: list[int], recv_counts: list[int
     return recv
 
 
+def _all_gather_strings(items: list[tuple[bytes, int]], device, group) -> list[tuple[bytes, int]]:
+    """All-gather every rank's (string, global index) list through plain
+    tensors (NCCL / gloo buffers, no pickling): counts first, then one
+    fixed-width record per string -- [length, index, bytes padded to the
+    longest string of the job]."""
+    G = dist.get_world_size(group)
+    k = torch.tensor([len(items), max((len(b) for b, _ in items), default=0)],
+                     dtype=torch.int64, device=device)
+    ks = [torch.empty_like(k) for _ in range(G)]
+    dist.all_gather(ks, k, group=group)
+    kmax = max(int(x[0]) for x in ks)
+    width = max(int(x[1]) for x in ks)
+    if kmax == 0:
+        return []
+    rec = 16 + width
+    buf = np.zeros((kmax, rec), dtype=np.uint8)
+    for i, (b, g) in enumerate(items):
+        buf[i, :16] = np.array([len(b), g], dtype=np.int64).view(np.uint8)
+        buf[i, 16:16 + len(b)] = np.frombuffer(b, dtype=np.uint8)
+    t = torch.from_numpy(buf.reshape(-1)).to(device)
+    out = [torch.empty_like(t) for _ in range(G)]
+    dist.all_gather(out, t, group=group)
+    res = []
+    for q in range(G):
+        a = out[q].cpu().numpy().reshape(kmax, rec)
+        for i in range(int(ks[q][0])):
+            L, g = a[i, :16].view(np.int64)
+            res.append((a[i, 16:16 + int(L)].tobytes(), int(g)))
+    return res
+
+
+def sample_positions(n: int, k: int, seed: int, rank: int) -> np.ndarray:
+    """k uniformly random positions of a shard of n strings (seeded by
+    (seed, rank); draw_sample's role, ssss.py:76-82, at the partition level)
+    -- regular positions of an unsorted shard would follow its input order."""
+    if n == 0:
+        return np.zeros(0, dtype=np.int64)
+    rng = np.random.default_rng((seed, rank, n))
+    return np.unique(rng.integers(0, n, size=min(k, n), dtype=np.int64))
+
+
 def pick_splitters(samples: list[tuple[bytes, int]], G: int) -> tuple[list[bytes], list[int]]:
     """G-1 equally spaced splitters from the sorted (string, global index) samples."""
     samples = sorted(samples)
@@ -104,17 +145,16 @@ def pick_splitters(samples: list[tuple[bytes, int]], G: int) -> tuple[list[bytes
 
 def distributed_sort(shard: Shard, backend, group=None, samples_per_rank: int = 1024,
                      max_splitter_len: int = 64, want_lcps: bool = True,
-                     mode: str = "packed", **sort_kw) -> DistResult:
+                     mode: str = "packed", seed: int = 1, stats: dict | None = None,
+                     **sort_kw) -> DistResult:
     """Globally stable sort of the union of all ranks' shards (see module doc)."""
     G = dist.get_world_size(group)
     r = dist.get_rank(group)
     local = backend.prepare(shard)
     n_local = len(shard.handles)
     # 1. samples -> identical splitters on every rank
-    mine = backend.sample(local, shard, samples_per_rank, max_splitter_len)
-    gathered: list = [None] * G
-    dist.all_gather_object(gathered, mine, group=group)
-    sp, sp_g = pick_splitters([s for part in gathered for s in part], G)
+    mine = backend.sample(local, shard, samples_per_rank, max_splitter_len, seed=seed, rank=r)
+    sp, sp_g = pick_splitters(_all_gather_strings(mine, backend.comm_device, group), G)
     # 2. destination rank of every local string (stable within a destination)
     dest = backend.partition(local, shard, sp, sp_g)
     order, counts = backend.group_by_dest(dest, G)
@@ -138,12 +178,15 @@ def distributed_sort(shard: Shard, backend, group=None, samples_per_rank: int = 
             _gather_counts(bcnt, rbcnt, group)
         rbytes = _alltoallv(payload, byte_counts, [int(x) for x in rbcnt.tolist()], group)
         arena, handles = backend.unpack(rbytes)
+        if stats is not None:  # bytes this rank sends to other ranks (NVLink traffic)
+            stats["sent_bytes"] = int(sum(b for q, b in enumerate(byte_counts) if q != r) +
+                                      24 * sum(c for q, c in enumerate(counts) if q != r))
     else:
         raise ValueError(f"unknown exchange mode: {mode}")
     # 4. local sort: received in global input order -> stable local sort
     perm, lcps = backend.local_sort(arena, handles, want_lcps, **sort_kw)
-    sorted_h = handles[perm]
-    sorted_g = gidx[perm]
+    sorted_h = backend.take(handles, perm)
+    sorted_g = backend.take(gidx, perm)
     # 5. LCP at the rank boundary
     if want_lcps:
         _boundary_lcp(backend, arena, sorted_h, lcps, G, r, group)
@@ -167,8 +210,10 @@ def _boundary_lcp(backend, arena, sorted_h, lcps, G, r, group):
     non-empty rank (rank 0 keeps -1): _boundary_lcps, parallel.py:447-455."""
     first = backend.string_bytes(arena, sorted_h[:1]) if len(sorted_h) else None
     last = backend.string_bytes(arena, sorted_h[-1:]) if len(sorted_h) else None
-    ends: list = [None] * G
-    dist.all_gather_object(ends, last, group=group)
+    # every rank's last string (rank q -> global index q marks it), no pickling
+    got = dict((g, b) for b, g in _all_gather_strings([] if last is None else [(last, r)],
+                                                      backend.comm_device, group))
+    ends = [got.get(q) for q in range(G)]
     prev = next((ends[q] for q in range(r - 1, -1, -1) if ends[q] is not None), None)
     if len(sorted_h):
         lcps[0] = LCP_UNDEF if prev is None else _lcp_bytes(prev, first)
@@ -192,13 +237,11 @@ def distributed_merge_sort(shard: Shard, backend, group=None, samples_per_rank: 
     n_local = len(shard.handles)
     hnd = backend.handles_of(local, shard)
     perm, lcps = backend.local_sort(local, hnd, True, **sort_kw)
-    sorted_h = hnd[perm]
+    sorted_h = backend.take(hnd, perm)
     gidx = perm.to(torch.int64) + shard.base_index
     # 1. regular samples of the sorted run -> identical splitters everywhere
     mine = backend.sample_run(local, sorted_h, gidx, samples_per_rank, max_splitter_len)
-    gathered: list = [None] * G
-    dist.all_gather_object(gathered, mine, group=group)
-    sp, sp_g = pick_splitters([x for part in gathered for x in part], G)
+    sp, sp_g = pick_splitters(_all_gather_strings(mine, backend.comm_device, group), G)
     # 2. cut the sorted run (destinations are non-decreasing along it)
     dest = backend.partition(local, shard, sp, sp_g, handles=sorted_h, gidx=gidx)
     counts = backend.dest_counts(dest, G) if n_local else [0] * G
@@ -218,7 +261,7 @@ def distributed_merge_sort(shard: Shard, backend, group=None, samples_per_rank: 
     run_off = np.r_[0, np.cumsum(recv_counts)].astype(np.int64)
     mh, ml = backend.kway_merge(arena, run_off, starts, lcp_r, dchar_r)
     pos = backend.positions(arena, starts, mh)
-    out_g = gidx_r[pos]
+    out_g = backend.take(gidx_r, pos)
     # 5. LCP at the rank boundary
     _boundary_lcp(backend, arena, mh, ml, G, r, group)
     total = torch.tensor([n_local], dtype=torch.int64, device=backend.comm_device)
@@ -262,20 +305,29 @@ class GpuBackend:
             return shard.buffer
         return D.upload(shard.buffer, shard.handles, self.comm_device)
 
-    def sample(self, ds, shard: Shard, k: int, maxlen: int):
-        n = ds.n
-        if n == 0:
+    def sample(self, ds, shard: Shard, k: int, maxlen: int, seed: int = 1, rank: int = 0):
+        """k random strings of the shard (prefixes <= maxlen) with their
+        global indices; the strings are packed on the device."""
+        from . import device as D
+
+        pos = sample_positions(ds.n, k, seed, rank)
+        if len(pos) == 0:
             return []
-        pos = np.unique(np.linspace(0, n - 1, num=min(k, n)).astype(np.int64))
-        h = ds.handles[torch.as_tensor(pos, device=ds.handles.device)]
-        idx = h[:, None] + torch.arange(maxlen, device=h.device)[None, :]
-        idx = idx.clamp_(max=ds.arena.numel() - 1)
-        chunk = ds.arena[idx].cpu().numpy()
-        out = []
-        for row, p in zip(chunk, pos):
-            z = np.flatnonzero(row == 0)
-            out.append((row[: z[0] if len(z) else maxlen].tobytes(), int(shard.base_index + p)))
-        return out
+        order = torch.as_tensor(pos, device=ds.handles.device)
+        return self._strings(ds, order, [int(shard.base_index + p) for p in pos], maxlen)
+
+    def _strings(self, ds, order, gidx, maxlen):
+        from . import device as D
+
+        payload, _ = D.pack_order(ds, order, [int(order.numel())])
+        raw = payload.cpu().numpy().tobytes()
+        out = raw.split(b"\0")[: len(gidx)]
+        return [(x[:maxlen], g) for x, g in zip(out, gidx)]
+
+    def take(self, src: torch.Tensor, idx: torch.Tensor) -> torch.Tensor:
+        from . import device as D
+
+        return D.gather_i64(src, idx)
 
     def partition(self, ds, shard: Shard, sp, sp_g, handles=None, gidx=None):
         from . import device as D
@@ -293,24 +345,22 @@ class GpuBackend:
     def positions(self, ds, handles: torch.Tensor, query: torch.Tensor) -> torch.Tensor:
         from . import device as D
 
-        return D.positions(handles, query, ds.arena_len)
+        return D.input_positions(handles, query, ds.arena_len)
 
     def sample_run(self, ds, handles, gidx, k: int, maxlen: int):
         """Equally spaced strings of a sorted run (prefixes <= maxlen) with
-        their global indices."""
+        their global indices (regular sampling of a sorted run, the merge
+        strategy's splitters)."""
+        from . import device as D
+
         n = handles.numel()
         if n == 0:
             return []
         pos = torch.as_tensor(np.unique(np.linspace(0, n - 1, num=min(k, n)).astype(np.int64)),
                               device=handles.device)
-        h = handles[pos]
-        idx = (h[:, None] + torch.arange(maxlen, device=h.device)[None, :]).clamp_(max=ds.arena.numel() - 1)
-        chunk = ds.arena[idx].cpu().numpy()
-        out = []
-        for row, g in zip(chunk, gidx[pos].cpu().numpy()):
-            z = np.flatnonzero(row == 0)
-            out.append((row[: z[0] if len(z) else maxlen].tobytes(), int(g)))
-        return out
+        sub = D.DeviceStrings(ds.arena, ds.arena_len, handles)
+        return self._strings(sub, pos, [int(x) for x in D.gather_i64(gidx, pos).cpu().tolist()],
+                             maxlen)
 
     def fill_dchar(self, ds, sorted_h, lcps):
         from . import device as D
@@ -332,21 +382,16 @@ class GpuBackend:
         return order.to(torch.int64) + shard.base_index
 
     def take_handles(self, ds, order):
-        return ds.handles[order]
-
-    def pack(self, ds, order, counts):
         from . import device as D
 
-        h = ds.handles[order]
-        lens = D.lengths(D.DeviceStrings(ds.arena, ds.arena_len, h))
-        off = torch.cumsum(lens + 1, 0) - (lens + 1)
-        total = int((lens + 1).sum().item()) if len(lens) else 0
-        payload = D.pack(ds, h, lens, off, total)[:total]
-        bounds = np.r_[0, np.cumsum(counts)]
-        cum = torch.cat([torch.zeros(1, dtype=torch.int64, device=lens.device),
-                         torch.cumsum(lens + 1, 0)])
-        byte_counts = [int(cum[bounds[q + 1]] - cum[bounds[q]]) for q in range(len(counts))]
-        return payload, byte_counts
+        return D.gather_i64(ds.handles, order)
+
+    def pack(self, ds, order, counts):
+        """Send buffer in destination order and bytes per destination, all
+        in library kernels (s5g_pack_plan + s5g_pack)."""
+        from . import device as D
+
+        return D.pack_order(ds, order, list(counts))
 
     def unpack(self, rbytes: torch.Tensor):
         """Received zero-terminated strings -> arena + string starts
@@ -371,13 +416,14 @@ class GpuBackend:
         return D.DeviceStrings(arena, alen, starts), starts
 
     def local_sort(self, ds, handles, want_lcps, **kw):
-        """Sorted permutation of `handles` (unique offsets) and the LCPs:
-        s5g_sort, then s5g_positions (handle -> input position map)."""
+        """Sorted permutation of `handles` and the LCPs: s5g_sort, then
+        s5g_input_positions (two stable radix sorts by handle: O(n), repeated
+        handles allowed -- no per-arena-byte map)."""
         from . import device as D
 
         local = D.DeviceStrings(ds.arena, ds.arena_len, handles)
         out_h, lcps, _ = D.sort(local, want_lcps=want_lcps, **kw)
-        return D.positions(handles, out_h, ds.arena_len), lcps
+        return D.input_positions(handles, out_h, ds.arena_len), lcps
 
     def string_bytes(self, ds, h1: torch.Tensor) -> bytes:
         from . import device as D

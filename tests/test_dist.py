@@ -21,6 +21,7 @@ from paper_1403_2056_b200.dist import (
     distributed_sort,
     handle_positions,
     pick_splitters,
+    sample_positions,
 )
 
 
@@ -38,13 +39,13 @@ class CpuBackend:
             e += 1
         return buf[h:e].tobytes()
 
-    def sample(self, buf, shard, k, maxlen):
-        n = len(shard.handles)
-        if n == 0:
-            return []
-        pos = np.unique(np.linspace(0, n - 1, num=min(k, n)).astype(np.int64))
+    def sample(self, buf, shard, k, maxlen, seed=1, rank=0):
+        pos = sample_positions(len(shard.handles), k, seed, rank)
         return [(self._str(buf, int(shard.handles[p]), maxlen), int(shard.base_index + p))
                 for p in pos]
+
+    def take(self, src, idx):
+        return src[idx]
 
     def partition(self, buf, shard, sp, sp_g, handles=None, gidx=None):
         import bisect

@@ -100,3 +100,37 @@ def test_positions_inverts_unique_handles():
     pos = D.positions(h, q, 1 << 20)
     assert torch.equal(h[pos], q)
     assert torch.equal(pos.cpu(), handle_positions(h.cpu(), q.cpu()))
+
+
+@pytest.mark.parametrize("n,dups", [(1, False), (1000, False), (200_000, False), (50_000, True)])
+def test_input_positions_with_repeated_handles(n, dups):
+    """s5g_input_positions: the input position of every output string of a
+    stable sort, repeated handles (the same string) matched in input order --
+    what local_sort needs without an arena-sized map."""
+    rng = np.random.default_rng(n)
+    items = [bytes(rng.integers(97, 100, size=int(rng.integers(0, 6)), dtype=np.uint8))
+             for _ in range(max(1, n // 4 if dups else n))]
+    buf = b"".join(x + b"\0" for x in items)
+    starts = np.concatenate(([0], np.cumsum([len(x) + 1 for x in items])[:-1])).astype(np.int64)
+    hnd = rng.choice(starts, size=n) if dups else rng.permutation(starts)[:n]
+    ds = D.upload(buf, hnd)
+    out_h, _, _ = D.sort(ds, want_lcps=False)
+    pos = D.input_positions(ds.handles, out_h, ds.arena_len).cpu().numpy()
+    assert np.array_equal(np.sort(pos), np.arange(n))          # a permutation
+    assert np.array_equal(hnd[pos], out_h.cpu().numpy())       # of the right strings
+    oh, _, _ = oracle.parallel_s5(buf, hnd)
+    # stable: equal strings keep input order -> the oracle's order of positions
+    want = np.argsort(np.array([buf[h:buf.index(b"\0", h)] for h in hnd], dtype=object), kind="stable")
+    assert np.array_equal(pos, want)
+
+
+def test_pack_order_matches_host_packing():
+    buf, hnd = corpora.gen_urls(5000, 3)
+    ds = D.upload(buf, hnd)
+    order = torch.as_tensor(np.random.default_rng(1).permutation(len(hnd)), device="cuda")
+    counts = [1200, 0, 3800]
+    payload, bc = D.pack_order(ds, order, counts)
+    o = order.cpu().numpy()
+    parts = [buf[h:np.flatnonzero(buf[h:] == 0)[0] + h].tobytes() + b"\0" for h in hnd[o]]
+    assert payload.cpu().numpy().tobytes() == b"".join(parts)
+    assert bc == [sum(len(p) for p in parts[:1200]), 0, sum(len(p) for p in parts[1200:])]
