@@ -308,6 +308,7 @@ __global__ void __launch_bounds__(CLS_NT) k_classify(
             int64_t i = base + u * CLS_NT + threadIdx.x;
             uint32_t mask = __ballot_sync(0xffffffffu, ok[u]);
             if (ok[u]) {
+                S5G_CHECK(b[u] < (uint32_t)nb);
                 bid[i] = (uint16_t)b[u];
                 uint32_t peers = __match_any_sync(mask, b[u]);
                 if (lane == __ffs(peers) - 1)
@@ -593,6 +594,7 @@ __global__ void __launch_bounds__(SC_NT, 2) k_scatter(
         for (int j = 0; j < SCX_IT; j++) {
             const uint32_t b = myb[j];
             if (b == BID_SENTINEL) continue;
+            S5G_CHECK(rel[j] < (uint32_t)sd.n && b < (uint32_t)nb);
             const int64_t pos = sd.lo + rel[j];
             const uint32_t f = bfact[b];
             const bool odd = b & 1;
@@ -847,6 +849,7 @@ __global__ void __launch_bounds__(SC_NT, 2) k_step_cta(
             for (int j = 0; j < IT; j++) {
                 const uint32_t b = myb[j];
                 if (b == BID_SENTINEL) continue;
+                S5G_CHECK(rel[j] < (uint32_t)n && b < (uint32_t)nb);
                 const uint32_t size = S.hist[b];
                 const bool odd = b & 1;
                 const int tpv = odd ? S.tpos[b >> 1] : WORD;

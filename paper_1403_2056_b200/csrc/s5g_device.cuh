@@ -7,6 +7,26 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+// Checked builds (-DS5G_CHECKED, tools/build_variant.sh checked ...): device
+// bounds checks on arena addresses, record / slot indices and output
+// positions; a failed check prints its line and traps (the launch then
+// fails with a CUDA error).  compute-sanitizer is not available on the GPU
+// pool this repo is measured on; this is the stand-in.
+#ifdef S5G_CHECKED
+#include <cstdio>
+#define S5G_CHECK(c)                                                                  \
+    do {                                                                              \
+        if (!(c)) {                                                                   \
+            printf("s5g check failed: %s (%s:%d)\n", #c, __FILE__, __LINE__);         \
+            __trap();                                                                 \
+        }                                                                             \
+    } while (0)
+#else
+#define S5G_CHECK(c) \
+    do {             \
+    } while (0)
+#endif
+
 namespace s5g {
 
 constexpr int WORD = 8;
@@ -56,6 +76,7 @@ __device__ __forceinline__ uint64_t load_word_le(const uint8_t* __restrict__ are
                                                  int64_t arena_len, int64_t pos) {
     int64_t a = pos & ~int64_t(7);
     int sh = (int)(pos & 7);
+    S5G_CHECK(pos >= 0);
     uint64_t w0 = a < arena_len ? __ldg(reinterpret_cast<const unsigned long long*>(arena + a)) : 0ull;
     if (!sh) return w0;
     uint64_t w1 = (a + 8) < arena_len
@@ -72,6 +93,7 @@ __device__ __forceinline__ uint64_t load_key(const uint8_t* __restrict__ arena, 
 
 __device__ __forceinline__ uint64_t ld8_guard(const uint8_t* __restrict__ arena, int64_t alen,
                                               int64_t a) {
+    S5G_CHECK(a >= 0);
     return a < alen ? __ldg(reinterpret_cast<const unsigned long long*>(arena + a)) : 0ull;
 }
 

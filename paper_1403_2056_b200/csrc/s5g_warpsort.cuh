@@ -143,6 +143,7 @@ __device__ __forceinline__ void rekey(uint64_t (&key)[N], const uint32_t (&meta)
     for (int q = tid; q < nslots; q += nthreads) {
         const uint64_t t = scratch[q];
         if (t != ~0ull) {
+            S5G_CHECK(t < (uint64_t)nslots);
             uint64_t w3[3];
             load_words3(arena, alen, hbt[t], depth, w3);
             segrec[t].w[0] = w3[0];
@@ -688,7 +689,10 @@ __global__ void __launch_bounds__(ws_nt(ITEMS), WS_MINB) k_warp_sort(
 #pragma unroll
     for (int e = 0; e < ITEMS; e++) {
         const int i = e * 32 + lane;
-        if (i < m) out_h[lo + i] = wh[wo[i]];
+        if (i < m) {
+            S5G_CHECK(wo[i] < m);
+            out_h[lo + i] = wh[wo[i]];
+        }
     }
     fetches = __reduce_add_sync(0xffffffffu, fetches);
     if (lane == 0) {
@@ -1213,7 +1217,10 @@ __global__ void __launch_bounds__(32 * W, 24 / W) k_cta_sort(
         }
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < m; i += NT) out_h[lo + i] = S.h[S.ord[i]];
+    for (int i = threadIdx.x; i < m; i += NT) {
+        S5G_CHECK(S.ord[i] < m);
+        out_h[lo + i] = S.h[S.ord[i]];
+    }
     fetches = __reduce_add_sync(0xffffffffu, fetches);
     if (lane == 0 && fetches) atomicAdd(&ctr->seg_fetches, (unsigned long long)fetches);
     if (threadIdx.x == 0) {
