@@ -624,11 +624,16 @@ __global__ void __launch_bounds__(SC_NT, 2) k_scatter(
 // Bucket ids (<= 63 buckets) are kept in shared memory by the count pass,
 // so the scatter's turn chain never waits on a record load.  Same outputs as
 // the device-wide step (ssss.py:281-358).
+#ifndef STEP_NT_CFG
+#define STEP_NT_CFG 512
+#endif
+constexpr int STEP_NT = STEP_NT_CFG;                  // threads of a fused single-CTA step
+constexpr int STEP_MINB = 1024 / STEP_NT;             // resident CTAs per SM (32 warps)
 struct StepCtaSmem {
     uint64_t s[16 * (MED_VMAX + 1)];       // sorted sample
     uint64_t tree[MED_VMAX + 1], inorder[MED_VMAX + 1];
     uint32_t hist[MED_NB + 1], bst[MED_NB + 1], run_off[MED_NB + 1];
-    uint32_t woff[SC_NT / 32][MED_NB + 1];  // per-warp running offsets of the scatter
+    uint32_t woff[STEP_NT / 32][MED_NB + 1];  // per-warp running offsets of the scatter
     uint8_t bids[MED_MAX];  // bucket of every string (<= 63 buckets), from the count pass
     uint16_t eqb[MED_VMAX + 1];
     int16_t sa[MED_VMAX + 1], sb[MED_VMAX + 1], sp[MED_VMAX + 1];
@@ -637,7 +642,7 @@ struct StepCtaSmem {
 };
 
 template <int VARIANT>
-__global__ void __launch_bounds__(SC_NT, 2) k_step_cta(
+__global__ void __launch_bounds__(STEP_NT, STEP_MINB) k_step_cta(
     const SegDev* __restrict__ segs, Rec* __restrict__ recA, Rec* __restrict__ recB,
     const uint8_t* __restrict__ arena, int64_t alen, uint64_t seed, int64_t vcap,
     int64_t small_max, SegDev* __restrict__ large_out, SegDev* __restrict__ small_out,
@@ -664,7 +669,7 @@ __global__ void __launch_bounds__(SC_NT, 2) k_step_cta(
     for (;;) {
         // ---- refill the cached words when the segment ran out of them ----
         if (!nvalid) {
-            for (int i = threadIdx.x; i < n; i += SC_NT) {
+            for (int i = threadIdx.x; i < n; i += STEP_NT) {
                 uint64_t wv[3];
                 load_words3(arena, alen, X[i].h, depth, wv);
                 X[i].w[0] = wv[0];
@@ -677,26 +682,26 @@ __global__ void __launch_bounds__(SC_NT, 2) k_step_cta(
         }
         // ---- draw_sample + select_splitters (ssss.py:76-146) -------------
         const uint64_t key0 = splitmix64(seed ^ splitmix64(lo ^ splitmix64((uint64_t)n ^ splitmix64(depth))));
-        for (int j = threadIdx.x; j < P; j += SC_NT)
+        for (int j = threadIdx.x; j < P; j += STEP_NT)
             S.s[j] = j < count ? X[splitmix64(key0 + j) % (uint64_t)n].w[0] : ~0ull;
-        for (int b = threadIdx.x; b <= MED_NB; b += SC_NT) S.hist[b] = 0;
+        for (int b = threadIdx.x; b <= MED_NB; b += STEP_NT) S.hist[b] = 0;
         if (threadIdx.x == 0) s_all_in = -1;
         __syncthreads();
-        bitonic_u64<SC_NT>(S.s, P);
-        select_tree<SC_NT>(S.s, count, v, L, S.sa, S.sb, S.sp, S.tree, S.inorder, S.tpos, S.eqb);
+        bitonic_u64<STEP_NT>(S.s, P);
+        select_tree<STEP_NT>(S.s, count, v, L, S.sa, S.sb, S.sp, S.tree, S.inorder, S.tpos, S.eqb);
         __syncthreads();
         // ---- classify + bucket counts (ssss.py:149-181, 292) -------------
         constexpr int CU = 4;  // keys in flight per thread
-        for (int base = 0; base < n; base += SC_NT * CU) {
+        for (int base = 0; base < n; base += STEP_NT * CU) {
             uint64_t key[CU];
 #pragma unroll
             for (int u = 0; u < CU; u++) {
-                const int i = base + u * SC_NT + threadIdx.x;
+                const int i = base + u * STEP_NT + threadIdx.x;
                 key[u] = i < n ? X[i].w[0] : 0;
             }
 #pragma unroll
             for (int u = 0; u < CU; u++) {
-                const int i = base + u * SC_NT + threadIdx.x;
+                const int i = base + u * STEP_NT + threadIdx.x;
                 const bool ok = i < n;
                 const uint32_t b = ok ? classify_one<VARIANT>(key[u], S.tree, S.eqb, v, L) : 0;
                 const uint32_t mask = __ballot_sync(0xffffffffu, ok);
@@ -708,7 +713,7 @@ __global__ void __launch_bounds__(SC_NT, 2) k_step_cta(
             }
         }
         __syncthreads();
-        for (int b = threadIdx.x; b < nb; b += SC_NT)
+        for (int b = threadIdx.x; b < nb; b += STEP_NT)
             if (S.hist[b] == (uint32_t)n) s_all_in = b;
         __syncthreads();
         // every string in ONE equality bucket whose splitter holds no
@@ -720,7 +725,7 @@ __global__ void __launch_bounds__(SC_NT, 2) k_step_cta(
         if (one >= 0 && (one & 1) && S.tpos[one >> 1] == WORD && depth <= alen) {
             depth += WORD;
             if (nvalid > 1)
-                for (int i = threadIdx.x; i < n; i += SC_NT) {
+                for (int i = threadIdx.x; i < n; i += STEP_NT) {
                     Rec r = X[i];
                     r.w[0] = r.w[1];
                     r.w[1] = r.w[2];
@@ -790,7 +795,7 @@ __global__ void __launch_bounds__(SC_NT, 2) k_step_cta(
     // the ids in shared memory) scanned bucket-major / warp-minor give every
     // warp its own running offsets, so warps never wait on each other
     {
-        constexpr int NW = SC_NT / 32;
+        constexpr int NW = STEP_NT / 32;
         const int w = threadIdx.x >> 5;
         const uint32_t lt = lanemask_lt();
         const int per = (n + NW - 1) / NW;
@@ -809,7 +814,7 @@ __global__ void __launch_bounds__(SC_NT, 2) k_step_cta(
             __syncwarp();
         }
         __syncthreads();
-        for (int b = threadIdx.x; b < nb; b += SC_NT) {
+        for (int b = threadIdx.x; b < nb; b += STEP_NT) {
             uint32_t run = S.bst[b];
 #pragma unroll
             for (int q = 0; q < NW; q++) {
@@ -1736,13 +1741,13 @@ static int sort_impl_body(const s5g_sort_args* a, int dev_id) {
             n_jobs += n_med;
             if (a->variant == S5G_VARIANT_UNROLL)
                 PROF(K_STEP_CTA, med_elems, 66LL * med_elems,
-                     (k_step_cta<S5G_VARIANT_UNROLL><<<(unsigned)large.size(), SC_NT, sizeof(StepCtaSmem), st>>>(
+                     (k_step_cta<S5G_VARIANT_UNROLL><<<(unsigned)large.size(), STEP_NT, sizeof(StepCtaSmem), st>>>(
                          w.large[round & 1], w.recA, w.recB, a->arena, a->arena_len, a->seed, vcap,
                          small_max, w.large[(round + 1) & 1], w.small, cls_lists, w.blist,
                          a->out_handles, lcps, w.ctr)));
             else
                 PROF(K_STEP_CTA, med_elems, 66LL * med_elems,
-                     (k_step_cta<S5G_VARIANT_EQUAL><<<(unsigned)large.size(), SC_NT, sizeof(StepCtaSmem), st>>>(
+                     (k_step_cta<S5G_VARIANT_EQUAL><<<(unsigned)large.size(), STEP_NT, sizeof(StepCtaSmem), st>>>(
                          w.large[round & 1], w.recA, w.recB, a->arena, a->arena_len, a->seed, vcap,
                          small_max, w.large[(round + 1) & 1], w.small, cls_lists, w.blist,
                          a->out_handles, lcps, w.ctr)));

@@ -110,7 +110,10 @@ __host__ __device__ inline int sample_count(int64_t v) {
 }
 
 // segments a single CTA takes through a whole S^5 step (k_step_cta)
-constexpr int MED_MAX = TILE;
+#ifndef MED_MAX_CFG
+#define MED_MAX_CFG 32768
+#endif
+constexpr int MED_MAX = MED_MAX_CFG;
 #ifndef MED_VMAX_CFG
 #define MED_VMAX_CFG 31
 #endif
