@@ -11,6 +11,10 @@
 
 #include <algorithm>
 #include <atomic>
+#include <sys/mman.h>
+
+#include <chrono>
+#include <cstdlib>
 #include <cstdio>
 #include <mutex>
 #include <cstring>
@@ -756,7 +760,7 @@ __global__ void __launch_bounds__(STEP_NT, STEP_MINB) k_step_cta(
         }
         run = incl - mine;
         const int nv = nvalid ? nvalid : NCACHE;
-#pragma unroll 1
+#pragma unroll
         for (int k = 0; k < BPL; k++) {
             const int b = lane * BPL + k;
             if (b < nb) {
@@ -953,17 +957,35 @@ __global__ void k_lengths(const uint8_t* __restrict__ arena, int64_t alen,
 
 // Pack strings (terminator included) to dst[dst_off[i] ..]: the send buffer
 // of the multi-GPU exchange.  One warp per string, 8-byte chunks.
+// One thread per string (its bytes and terminator, arena[h .. h+L]): the
+// source is read as aligned words with funnel shifts (load_word_le), the
+// destination written as aligned 8-byte words with byte stores only at the
+// two edges it shares with its neighbours (a warp per string with byte
+// stores was a chain of dependent round trips per string).
 __global__ void k_pack(const uint8_t* __restrict__ arena, int64_t alen,
                        const int64_t* __restrict__ handles, const int64_t* __restrict__ lens,
                        const int64_t* __restrict__ dst_off, int64_t n, uint8_t* __restrict__ dst) {
-    const int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
     // lens == NULL: sizes from the exclusive offsets (s5g_pack_plan's)
     const int64_t h = handles[i], o = dst_off[i];
-    const int64_t L = lens ? lens[i] + 1 : dst_off[i + 1] - o;
-    // one warp per string, byte-wise (strings end at arbitrary alignments)
-    for (int64_t b = lane; b < L; b += 32) dst[o + b] = b < L - 1 && h + b < alen ? arena[h + b] : 0;
+    const int64_t L = lens ? lens[i] + 1 : dst_off[i + 1] - o;  // with the terminator
+    const int64_t e = o + L;
+    int64_t a = (o + 7) & ~int64_t(7);
+    if (a > e) a = e;
+    const int64_t z = e & ~int64_t(7);
+    auto byte_at = [&](int64_t q) -> uint8_t {
+        const int64_t s = h + (q - o);
+        return q - o < L - 1 && s < alen ? arena[s] : 0;
+    };
+    for (int64_t q = o; q < a; q++) dst[q] = byte_at(q);
+    for (int64_t q = a; q < z; q += 8) {
+        uint64_t w = load_word_le(arena, alen, h + (q - o));
+        const int64_t left = L - 1 - (q - o);  // string bytes left at q (the rest is 0)
+        if (left < 8) w &= left > 0 ? (~0ull >> (64 - 8 * left)) : 0ull;
+        *reinterpret_cast<uint64_t*>(dst + q) = w;
+    }
+    for (int64_t q = (z > a ? z : a); q < e; q++) dst[q] = byte_at(q);
 }
 
 // ---------------------------------------------------------------------------
@@ -972,18 +994,49 @@ __global__ void k_pack(const uint8_t* __restrict__ arena, int64_t alen,
 // chunk; a single CTA scans the chunk counts; pass 2 writes the string starts.
 constexpr int LD_NT = 256, LD_CHUNK = LD_NT * 64;
 
+// Each thread owns 64 contiguous bytes of a 16 KB chunk, read and written as
+// four 16-byte vectors (the byte-at-a-time version ran at ~250 GB/s); the
+// zero bytes of a word are found with zero_bytes (exact, no carries).
+// data is 16-byte aligned and readable (and writable) for round_up(len, 16)
+// bytes: the arena pads past len (S5G_ARENA_PAD).
+__device__ __forceinline__ uint64_t ld_zero_mask(uint64_t w, int64_t base, int64_t len) {
+    uint64_t z = zero_bytes(w);  // bit 7 of every zero byte
+    if (base + 8 > len) {        // bytes past the end do not count
+        const int keep = base >= len ? 0 : (int)(len - base);
+        z &= keep ? (~0ull >> (64 - 8 * keep)) : 0ull;
+    }
+    return z;
+}
+
 __global__ void k_ld_count(uint8_t* __restrict__ data, int64_t len, int delim,
                            uint32_t* __restrict__ chunk_cnt, int* __restrict__ bad) {
     __shared__ uint32_t wsum[32];
-    const int64_t c0 = (int64_t)blockIdx.x * LD_CHUNK;
+    const int64_t t0 = (int64_t)blockIdx.x * LD_CHUNK + (int64_t)threadIdx.x * 64;
     uint32_t cntv = 0;
-    for (int64_t i = c0 + threadIdx.x; i < min(c0 + LD_CHUNK, len); i += LD_NT) {
-        uint8_t b = data[i];
-        if (delim != 0) {
-            if (b == 0) *bad = 1;  // input contains byte 0, reserved as terminator
-            if (b == (uint8_t)delim) { b = 0; data[i] = 0; }
+    const uint64_t dpat = (uint64_t)(uint8_t)delim * ONES;
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+        const int64_t o = t0 + 16 * q;
+        if (o >= len) break;
+        uint4* p = reinterpret_cast<uint4*>(data + o);
+        uint4 v = *p;
+        uint64_t w[2] = {(uint64_t)v.x | (uint64_t)v.y << 32, (uint64_t)v.z | (uint64_t)v.w << 32};
+        bool changed = false;
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            const int64_t base = o + 8 * h;
+            if (delim != 0) {
+                if (ld_zero_mask(w[h], base, len)) *bad = 1;  // byte 0 is reserved as terminator
+                const uint64_t m = ld_zero_mask(w[h] ^ dpat, base, len);  // delimiter bytes
+                if (m) {
+                    w[h] &= ~((m >> 7) * 0xffull);  // remap them to 0
+                    changed = true;
+                }
+            }
+            cntv += __popcll(ld_zero_mask(w[h], base, len));
         }
-        cntv += b == 0;
+        if (changed)
+            *p = make_uint4((uint32_t)w[0], (uint32_t)(w[0] >> 32), (uint32_t)w[1], (uint32_t)(w[1] >> 32));
     }
     uint32_t total;
     block_excl_sum<LD_NT>(cntv, wsum, &total);
@@ -1011,15 +1064,26 @@ __global__ void k_ld_scan(uint32_t* __restrict__ chunk_cnt, int64_t nchunks, int
 __global__ void k_ld_write(const uint8_t* __restrict__ data, int64_t len,
                            const uint32_t* __restrict__ chunk_off, int64_t* __restrict__ handles) {
     __shared__ uint32_t wsum[32];
-    const int64_t c0 = (int64_t)blockIdx.x * LD_CHUNK;
-    const int64_t per = LD_CHUNK / LD_NT;  // contiguous run per thread keeps order
-    const int64_t t0 = c0 + (int64_t)threadIdx.x * per, t1 = min(t0 + per, len);
+    const int64_t t0 = (int64_t)blockIdx.x * LD_CHUNK + (int64_t)threadIdx.x * 64;
+    uint64_t z[8];  // zero-byte masks of the thread's 64 bytes, in order
     uint32_t cntv = 0;
-    for (int64_t i = t0; i < t1; i++) cntv += data[i] == 0;
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+        const int64_t o = t0 + 16 * q;
+        z[2 * q] = z[2 * q + 1] = 0;
+        if (o < len) {
+            const uint4 v = *reinterpret_cast<const uint4*>(data + o);
+            z[2 * q] = ld_zero_mask((uint64_t)v.x | (uint64_t)v.y << 32, o, len);
+            z[2 * q + 1] = ld_zero_mask((uint64_t)v.z | (uint64_t)v.w << 32, o + 8, len);
+        }
+        cntv += __popcll(z[2 * q]) + __popcll(z[2 * q + 1]);
+    }
     uint32_t k = chunk_off[blockIdx.x] + block_excl_sum<LD_NT>(cntv, wsum, nullptr);
-    for (int64_t i = t0; i < t1; i++)
-        if (data[i] == 0) {
-            if (k == 0) handles[0] = 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) handles[0] = 0;
+#pragma unroll
+    for (int j = 0; j < 8; j++)
+        for (uint64_t m = z[j]; m; m &= m - 1) {
+            const int64_t i = t0 + 8 * j + (__ffsll((long long)m) - 1) / 8;
             handles[k + 1] = i + 1;  // start of the next string (dropped if past the end)
             k++;
         }
@@ -1133,9 +1197,16 @@ __global__ void k_plan_sizes(const uint8_t* __restrict__ arena, int64_t alen,
     if (k >= n) return;
     const int64_t h = handles[order[k]];
     out_h[k] = h;
-    int64_t e = h;
-    while (e < alen && arena[e]) e++;
-    size[k] = e - h + 1;
+    int64_t e = h;  // terminator: a word at a time
+    for (;; e += WORD) {
+        const uint64_t z = zero_bytes(load_word_le(arena, alen, e));
+        if (z) {
+            e += (__ffsll((long long)z) - 1) >> 3;
+            break;
+        }
+        if (e >= alen) break;
+    }
+    size[k] = min(e, alen) - h + 1;
 }
 // bytes per destination from the exclusive offsets (off[n] = total)
 __global__ void k_plan_dest(const int64_t* __restrict__ off, int64_t n,
@@ -1147,6 +1218,25 @@ __global__ void k_plan_dest(const int64_t* __restrict__ off, int64_t n,
         const int64_t b = a + counts[g];
         dest_bytes[g] = off[b] - off[a];
         a = b;
+    }
+}
+
+__global__ void k_minmax_i64(const int64_t* __restrict__ x, int64_t n, int64_t* __restrict__ mm) {
+    int64_t lo = INT64_MAX, hi = INT64_MIN;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v = x[i];
+        lo = v < lo ? v : lo;
+        hi = v > hi ? v : hi;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(reinterpret_cast<long long*>(mm), (long long)lo);
+        atomicMax(reinterpret_cast<long long*>(mm) + 1, (long long)hi);
     }
 }
 
@@ -1310,6 +1400,8 @@ struct Profiler {
         launch;                                    \
         prof.end(slot_, kid, (units_), (bytes_));  \
     } while (0)
+
+static int g_sms_of() { return g_sms; }
 
 static int fail(int code, const std::string& msg) {
     g_err = msg;
@@ -2033,6 +2125,21 @@ struct HostCtx {
         cudaGetLastError();
         return ok && at.type == cudaMemoryTypeHost;
     }
+    // first-touch every page of a pageable host buffer (all host threads)
+    static void prefault(void* p, size_t bytes) {
+        if (!p || !bytes || pinned(p)) return;
+        {
+            // transparent huge pages for the 2 MB-aligned interior (THP in
+            // "madvise" mode): 512x fewer faults
+            const uintptr_t a = ((uintptr_t)p + (2u << 20) - 1) & ~(uintptr_t)((2u << 20) - 1);
+            const uintptr_t e = ((uintptr_t)p + bytes) & ~(uintptr_t)((2u << 20) - 1);
+            if (e > a) madvise((void*)a, e - a, MADV_HUGEPAGE);
+        }
+        volatile uint8_t* b = (volatile uint8_t*)p;
+        const int64_t pages = (int64_t)((bytes + 4095) >> 12);
+#pragma omp parallel for schedule(static)
+        for (int64_t q = 0; q < pages; q++) b[q << 12] = 0;
+    }
     static void par_copy(void* dst, const void* src, size_t bytes) {
         const int64_t parts = (int64_t)std::min<size_t>(64, (bytes + (1 << 20) - 1) >> 20);
 #pragma omp parallel for schedule(static)
@@ -2084,6 +2191,7 @@ struct HostCtx {
     }
 };
 static HostCtx g_host[MAX_DEV];
+
 
 }  // namespace s5g
 
@@ -2197,19 +2305,61 @@ int s5g_sort_host(const uint8_t* arena, int64_t arena_len, const int64_t* handle
     if (out_lcps || out_dchar) CKH(cudaMallocFromPoolAsync((void**)&d_lcp, 8 * n, hx.pool, st));
     if (out_dchar) CKH(cudaMallocFromPoolAsync((void**)&d_dchar, n, hx.pool, st));
     CKH(cudaMemsetAsync(d_arena + arena_len, 0, alen_pad - arena_len, st));
+    // S5G_HOST_TIMING=1: phase times of this call on stderr (tuning aid)
+    static const bool timing = getenv("S5G_HOST_TIMING") != nullptr;
+    auto now = []() { return std::chrono::steady_clock::now(); };
+    auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+    auto t0 = now();
     CKH(hx.h2d(d_h, handles, 8 * n));
     CKH(hx.h2d(d_arena, arena, arena_len));
+    auto t1 = now();
+    // handles must lie in the arena (the reference's "handle outside the
+    // buffer" / "not zero-terminated" checks, strset.py:64-78, done here on
+    // the device: one pass over the uploaded handles instead of two numpy
+    // passes over the host array)
+    int64_t* d_mm = nullptr;
+    CKH(cudaMallocFromPoolAsync((void**)&d_mm, 16, hx.pool, st));
+    {
+        const int64_t init[2] = {INT64_MAX, INT64_MIN};
+        CKH(cudaMemcpyAsync(d_mm, init, 16, cudaMemcpyHostToDevice, st));
+        g_launches++;
+        k_minmax_i64<<<std::min<int64_t>(2 * g_sms_of(), blocks_for(n, 256)), 256, 0, st>>>(d_h, n, d_mm);
+        CKH(cudaGetLastError());
+    }
+    // fresh pageable output arrays fault in page by page on first write
+    // (~0.6 s for C5's 4.3 GB on one thread, after the sort): fault them in
+    // now, as huge pages where the kernel allows, on all host threads, while
+    // the input DMA runs (page-locking them in place instead was slower:
+    // cudaHostRegister / Unregister of 4.3 GB cost ~0.6 s)
+    HostCtx::prefault(out_handles, 8 * (size_t)n);
+    HostCtx::prefault(out_lcps, 8 * (size_t)n);
+    HostCtx::prefault(out_dchar, (size_t)n);
+    int64_t mm[2];
+    CKH(cudaMemcpyAsync(mm, d_mm, 16, cudaMemcpyDeviceToHost, st));
+    CKH(cudaFreeAsync(d_mm, st));
+    CKH(cudaStreamSynchronize(st));  // the input is on the device; mm is valid
+    if (mm[0] < 0 || mm[1] >= arena_len) {
+        cleanup();
+        return fail(S5G_E_INVALID, "handle outside the buffer");
+    }
     s5g_sort_args a{};
     a.arena = d_arena; a.arena_len = arena_len; a.handles = d_h; a.n = n; a.depth = depth;
     a.out_handles = d_out; a.out_lcps = d_lcp; a.out_dchar = d_dchar;
     a.workspace = d_ws; a.workspace_bytes = ws; a.stream = st;
     a.variant = variant; a.v = v; a.seed = seed; a.t_medium = tm; a.stats = stats;
+    auto t2 = now();
     rc = sort_impl(&a);
     if (rc) { std::string keep = g_err; cleanup(); g_err = keep; return rc; }
+    auto t3 = now();
     CKH(hx.d2h(out_handles, d_out, 8 * n));
     if (out_lcps) CKH(hx.d2h(out_lcps, d_lcp, 8 * n));
     if (out_dchar) CKH(hx.d2h(out_dchar, d_dchar, n));
     CKH(cudaStreamSynchronize(st));
+    auto t4 = now();
+    if (timing)
+        fprintf(stderr, "s5g_sort_host: issue H2D %.1f ms, prefault + H2D wait %.1f ms, sort %.1f ms, "
+                        "D2H %.1f ms (input %s)\n", ms(t0, t1), ms(t1, t2), ms(t2, t3), ms(t3, t4),
+                HostCtx::pinned(arena) ? "pinned" : "pageable");
     cleanup();
 #undef CKH
     return 0;
@@ -2504,8 +2654,8 @@ int s5g_pack(const uint8_t* arena, int64_t arena_len, const int64_t* handles,
     if (n <= 0) return n < 0 ? fail(S5G_E_INVALID, "negative n") : 0;
     cudaStream_t st = (cudaStream_t)stream;
     g_launches++;
-    k_pack<<<blocks_for(n * 32, 256), 256, 0, st>>>(arena, arena_len, handles, lengths, dst_off,
-                                                    n, dst);
+    k_pack<<<blocks_for(n, 256), 256, 0, st>>>(arena, arena_len, handles, lengths, dst_off, n,
+                                                dst);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(st));
     return 0;

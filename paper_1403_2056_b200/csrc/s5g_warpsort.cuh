@@ -865,8 +865,11 @@ __device__ void cta_bitonic_generic(uint64_t (&key)[8], uint32_t (&meta)[8], int
     }
 }
 
+#ifndef CTA_SORT_WARPS_PER_SM
+#define CTA_SORT_WARPS_PER_SM 24  // 80 registers per thread
+#endif
 template <int W>
-__global__ void __launch_bounds__(32 * W, 24 / W) k_cta_sort(
+__global__ void __launch_bounds__(32 * W, CTA_SORT_WARPS_PER_SM / W) k_cta_sort(
     const SegDev* __restrict__ segs, int64_t nsegs, Rec* __restrict__ recA,
     Rec* __restrict__ recB, const uint8_t* __restrict__ arena, int64_t alen,
     int64_t* __restrict__ out_h, int64_t* __restrict__ lcps, Counters* __restrict__ ctr) {

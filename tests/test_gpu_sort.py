@@ -251,3 +251,17 @@ def test_parallel_s5_p_counts_gpus():
         P.parallel_s5(s, p=ndev + 1)
     with pytest.raises(ValueError, match="at least 1"):
         P.parallel_s5(s, p=0)
+
+
+def test_host_entry_rejects_handles_outside_the_buffer():
+    """The reference's input errors through the host entry (s5g_sort_host
+    checks handle bounds on the device): ValueError, no crash."""
+    s = P.StringSet(b"ab\0cd\0", np.array([0, 3, 6], dtype=np.int64))
+    with pytest.raises(ValueError, match="outside the buffer"):
+        P.s5_sort(s, want_lcps=True)
+    s = P.StringSet(b"ab\0cd\0", np.array([0, -1], dtype=np.int64))
+    with pytest.raises(ValueError, match="outside the buffer"):
+        P.s5_sort(s)
+    s = P.StringSet(b"ab\0cd", np.array([0, 3], dtype=np.int64))
+    with pytest.raises(ValueError, match="not zero-terminated"):
+        P.s5_sort(s)
