@@ -667,9 +667,13 @@ __global__ void __launch_bounds__(STEP_NT, STEP_MINB) k_step_cta(
     const int count = med_sample_count(v);
     int P = 1;
     while (P < count) P <<= 1;
-    const int lane = threadIdx.x & 31;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     unsigned my_fetch = 0;
-    __shared__ int s_all_in;  // the one bucket holding every string, or -1
+    // cached words consumed in place: X[i].w[wo] is the word at `depth`,
+    // nvalid words from wo on are valid
+    int wo = 0;
+    __shared__ uint64_t s_red[2][STEP_NT / 32][NCACHE];
+    __shared__ int s_flag;
     for (;;) {
         // ---- refill the cached words when the segment ran out of them ----
         if (!nvalid) {
@@ -682,15 +686,93 @@ __global__ void __launch_bounds__(STEP_NT, STEP_MINB) k_step_cta(
                 my_fetch += 3;
             }
             nvalid = NCACHE;
+            wo = 0;
             __syncthreads();  // the CTA's own record writes are visible after this
         }
-        // ---- draw_sample + select_splitters (ssss.py:76-146) -------------
+        // ---- draw_sample (ssss.py:76-82) ----------------------------------
         const uint64_t key0 = splitmix64(seed ^ splitmix64(lo ^ splitmix64((uint64_t)n ^ splitmix64(depth))));
-        for (int j = threadIdx.x; j < P; j += STEP_NT)
-            S.s[j] = j < count ? X[splitmix64(key0 + j) % (uint64_t)n].w[0] : ~0ull;
+        uint64_t so = 0, sa = ~0ull;
+        for (int j = threadIdx.x; j < P; j += STEP_NT) {
+            uint64_t x = ~0ull;
+            if (j < count) {
+                x = X[splitmix64(key0 + j) % (uint64_t)n].w[wo];
+                so |= x;
+                sa &= x;
+            }
+            S.s[j] = x;
+        }
         for (int b = threadIdx.x; b <= MED_NB; b += STEP_NT) S.hist[b] = 0;
-        if (threadIdx.x == 0) s_all_in = -1;
+        // ---- a constant sample: are the leading cached words equal over
+        // the whole segment?  Then no step is needed -- the stable scatter
+        // would be the identity and the only child the segment itself a word
+        // deeper -- so the depth advances in place, up to all cached words
+        // at once (duplicate-heavy and shared-prefix segments: C5's 16-
+        // character vocabulary words)
+        so = warp_or64(so);
+        sa = warp_and64(sa);
+        if (lane == 0) {
+            s_red[0][warp][0] = so;
+            s_red[1][warp][0] = sa;
+        }
         __syncthreads();
+        if (threadIdx.x == 0) {
+            uint64_t o = 0, x = ~0ull;
+            for (int q = 0; q < STEP_NT / 32; q++) {
+                o |= s_red[0][q][0];
+                x &= s_red[1][q][0];
+            }
+            s_flag = o == x && term_pos(o) == WORD;
+        }
+        __syncthreads();
+        if (s_flag) {
+            uint64_t wor[NCACHE], wand[NCACHE];
+#pragma unroll
+            for (int k = 0; k < NCACHE; k++) {
+                wor[k] = 0;
+                wand[k] = ~0ull;
+            }
+            for (int i = threadIdx.x; i < n; i += STEP_NT) {
+                const Rec r = X[i];
+#pragma unroll
+                for (int k = 0; k < NCACHE; k++) {
+                    wor[k] |= r.w[k];
+                    wand[k] &= r.w[k];
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < NCACHE; k++) {
+                wor[k] = warp_or64(wor[k]);
+                wand[k] = warp_and64(wand[k]);
+                if (lane == 0) {
+                    s_red[0][warp][k] = wor[k];
+                    s_red[1][warp][k] = wand[k];
+                }
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                int k0 = 0;  // leading cached words equal everywhere, no terminator
+                for (int k = wo; k < wo + nvalid; k++) {
+                    uint64_t o = 0, x = ~0ull;
+                    for (int q = 0; q < STEP_NT / 32; q++) {
+                        o |= s_red[0][q][k];
+                        x &= s_red[1][q][k];
+                    }
+                    if (o != x || term_pos(o) < WORD) break;
+                    k0++;
+                }
+                s_flag = k0;
+            }
+            __syncthreads();
+            const int k0 = s_flag;
+            __syncthreads();
+            if (k0 && depth <= alen) {
+                depth += (int64_t)WORD * k0;
+                wo += k0;
+                nvalid -= k0;
+                continue;
+            }
+        }
+        // ---- select_splitters (ssss.py:85-146) ------------------------------
         bitonic_u64<STEP_NT>(S.s, P);
         select_tree<STEP_NT>(S.s, count, v, L, S.sa, S.sb, S.sp, S.tree, S.inorder, S.tpos, S.eqb);
         __syncthreads();
@@ -701,7 +783,7 @@ __global__ void __launch_bounds__(STEP_NT, STEP_MINB) k_step_cta(
 #pragma unroll
             for (int u = 0; u < CU; u++) {
                 const int i = base + u * STEP_NT + threadIdx.x;
-                key[u] = i < n ? X[i].w[0] : 0;
+                key[u] = i < n ? X[i].w[wo] : 0;
             }
 #pragma unroll
             for (int u = 0; u < CU; u++) {
@@ -717,29 +799,6 @@ __global__ void __launch_bounds__(STEP_NT, STEP_MINB) k_step_cta(
             }
         }
         __syncthreads();
-        for (int b = threadIdx.x; b < nb; b += STEP_NT)
-            if (S.hist[b] == (uint32_t)n) s_all_in = b;
-        __syncthreads();
-        // every string in ONE equality bucket whose splitter holds no
-        // terminator: the stable scatter would be the identity and the only
-        // child the whole segment one word deeper -- advance the depth in
-        // place instead (no scatter, no extra round); duplicate-heavy and
-        // shared-prefix segments (C5's vocabulary words) take this path
-        const int one = s_all_in;
-        if (one >= 0 && (one & 1) && S.tpos[one >> 1] == WORD && depth <= alen) {
-            depth += WORD;
-            if (nvalid > 1)
-                for (int i = threadIdx.x; i < n; i += STEP_NT) {
-                    Rec r = X[i];
-                    r.w[0] = r.w[1];
-                    r.w[1] = r.w[2];
-                    r.w[2] = 0;
-                    X[i] = r;
-                }
-            nvalid--;
-            __syncthreads();
-            continue;
-        }
         break;
     }
     // ---- bucket starts, children, boundary records (one warp) -----------
@@ -865,15 +924,21 @@ __global__ void __launch_bounds__(STEP_NT, STEP_MINB) k_step_cta(
                 if (size == 1 || (odd && tpv < WORD)) {
                     out_h[lo + rel[j]] = rec[j].h;
                     if (lcps && size > 1 && rel[j] != S.bst[b]) lcps[lo + rel[j]] = depth + tpv;
-                } else if (odd) {
+                } else {
+                    // the child's cached words start one further for an
+                    // equality bucket, after the wo words consumed in place
+                    const int sh = wo + (odd ? 1 : 0);
                     Rec o;
                     o.h = rec[j].h;
-                    o.w[0] = rec[j].w[1];
-                    o.w[1] = rec[j].w[2];
-                    o.w[2] = 0;
+#pragma unroll
+                    for (int k = 0; k < NCACHE; k++) {
+                        uint64_t x = 0;
+#pragma unroll
+                        for (int q = 0; q < NCACHE; q++)
+                            if (q == k + sh) x = rec[j].w[q];
+                        o.w[k] = x;
+                    }
                     Y[rel[j]] = o;
-                } else {
-                    Y[rel[j]] = rec[j];
                 }
             }
         }
