@@ -38,7 +38,13 @@ PEAKS = ROOT / "MEASURED_PEAKS.json"
 FALLBACK_HBM = 6650.0  # GB/s, B200_PROFILING.md fallback
 
 
-TRAFFIC = ROOT / "profiles" / "r01i_traffic.json"
+TRAFFIC = ROOT / "profiles" / "r01i_traffic.json"  # replaced per config in main()
+
+
+def traffic_file(config: str):
+    """The committed ncu per-kernel traffic of this workload (full size)."""
+    p = ROOT / "profiles" / f"r02_{config}_traffic.json"
+    return p if p.exists() else (ROOT / "profiles" / "r01i_traffic.json" if config == "c2_dna" else None)
 PASS_BYTES = 24  # SURVEY 8(d): algorithmic bytes per string per distribution pass
 
 
@@ -49,7 +55,7 @@ def ncu_traffic(kernel: str):
         d = json.loads(TRAFFIC.read_text())["kernels"]
     except Exception:
         return None
-    k = d.get(kernel) or d.get(kernel.replace("<", "<").strip())
+    k = d.get(kernel)
     if k is None:  # ncu names templates with their argument values
         k = next((v for n, v in d.items() if n.split("<")[0] == kernel.split("<")[0]), None)
     return k["dram_bytes_per_launch"] if k else None
@@ -622,6 +628,8 @@ def main(argv=None):
     ap.add_argument("--dist", action="store_true",
                     help="run the multi-GPU (torchrun) code path even at N = 1 (checks)")
     args = ap.parse_args(argv)
+    global TRAFFIC
+    TRAFFIC = traffic_file(args.config)
     if args.impl == "reference":
         return run_reference(args)
     if int(os.environ.get("WORLD_SIZE", "1")) > 1 or args.dist:

@@ -1,5 +1,8 @@
 """Top stall-sampled SASS windows per kernel from an `ncu --page source
---csv --print-source sass` export (one block per captured launch)."""
+--csv --print-source sass` export.  ncu exports one block per captured
+launch; blocks of the same kernel are merged (printed once), optionally only
+kernels whose name contains FILTER.
+usage: python tools/sass_hot.py SASS.csv [FILTER]"""
 import csv
 import sys
 
@@ -13,10 +16,23 @@ for r in rows:
         cur["h"] = r
     elif cur is not None:
         cur["rows"].append(r)
+want = sys.argv[2] if len(sys.argv) > 2 else ""
+merged = {}
 for b in blocks:
-    h = b.get("h")
-    if not h:
+    if not b.get("h") or want not in b["name"]:
         continue
+    m = merged.get(b["name"])
+    if m is None or len(m["rows"]) != len(b["rows"]):
+        merged.setdefault(b["name"], b)
+        continue
+    si = b["h"].index("Warp Stall Sampling (All Samples)")
+    ie = b["h"].index("Instructions Executed")
+    for r0, r1 in zip(m["rows"], b["rows"]):  # same SASS: add the counts
+        if len(r0) == len(b["h"]) and len(r1) == len(b["h"]):
+            r0[si] = str(int(r0[si]) + int(r1[si]))
+            r0[ie] = str(float(r0[ie] or 0) + float(r1[ie] or 0))
+for b in merged.values():
+    h = b.get("h")
     si = h.index("Warp Stall Sampling (All Samples)")
     ie = h.index("Instructions Executed")
     d = [r for r in b["rows"] if len(r) == len(h)]
