@@ -49,7 +49,9 @@ extern "C" {
 /* Mirror of strsort.counters.SortStats (counters.py:13-36). */
 typedef struct s5g_stats {
     int64_t char_cmps;
-    int64_t word_fetches;      /* 8-byte arena word loads actually issued */
+    int64_t word_fetches;      /* 8-byte words fetched from the arena (cache fills
+                                  of 3 words per string and refill, and the words
+                                  of direct comparisons) -- the Theorem-6 counter */
     int64_t merge_buffer_cmps;
     int64_t scratch_words;
     int64_t jobs_enqueued;     /* segments queued (S^5 steps + CTA segments) */

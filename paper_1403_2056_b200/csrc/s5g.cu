@@ -2140,7 +2140,9 @@ static int sort_impl_body(const s5g_sort_args* a, int dev_id) {
     // register finishers: record (32 B) in per string, handle + lcp (16 B) out;
     // modelled as 32 B/string in the launches above
     if (a->stats) {
-        a->stats->word_fetches += n + (int64_t)hc.fetches + (int64_t)hc.seg_fetches;
+        // the initial cache fill (k_init / the root classify: 3 words per
+        // string) + every refill and direct comparison counted on the device
+        a->stats->word_fetches += NCACHE * n + (int64_t)hc.fetches + (int64_t)hc.seg_fetches;
         a->stats->jobs_enqueued += n_jobs + n_small;
         a->stats->jobs_executed += n_jobs + n_small;
     }

@@ -8,9 +8,12 @@
 //   k_scan_cols    tile-minor prefix per bucket      (parallel.py:379-385)
 //   k_scan_buckets bucket-major exclusive scan, children, boundary records
 //   k_scatter      stable scatter (argsort(kind=stable) + gather, ssss.py:295)
-// Small segments finish in one CTA each (k_seg_sort): the GPU stand-in for
-// the MKQS / insertion leaves (mkqs.py:196-253, basecase.py:67-116) --
-// repeated stable sorts on 8-byte keys with depth advancing by a word.
+// Segments of up to MED_MAX strings take a whole step in one CTA
+// (k_step_cta); segments of up to SMALL_MAX strings are finished by the
+// register finishers k_warp_sort / k_cta_sort (s5g_warpsort.cuh): the GPU
+// stand-in for the MKQS / insertion leaves (mkqs.py:196-253,
+// basecase.py:67-116) -- repeated stable sorts on 8-byte keys with depth
+// advancing by a word.
 #pragma once
 #include "s5g_device.cuh"
 
