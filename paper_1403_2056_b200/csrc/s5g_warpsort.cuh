@@ -886,8 +886,6 @@ __global__ void __launch_bounds__(32 * W, CTA_SORT_WARPS_PER_SM / W) k_cta_sort(
     int64_t* lcp_seg = lcps ? lcps + lo : nullptr;
     int64_t depth = sg.depth;
     unsigned fetches = 0;
-    for (int i = threadIdx.x; i < m; i += NT) S.h[i] = segrec[i].h;
-    __syncthreads();
     uint64_t key[ITEMS];
     uint32_t meta[ITEMS];
     const int base = threadIdx.x * ITEMS;  // first slot of this thread
@@ -899,8 +897,27 @@ __global__ void __launch_bounds__(32 * W, CTA_SORT_WARPS_PER_SM / W) k_cta_sort(
         key[e] = ~0ull;
         meta[e] = i < m ? (1u << 22) | (uint32_t)i : ((uint32_t)i << 11) | (uint32_t)i;
     }
-    rekey<ITEMS, true>(key, meta, segrec, S.h, cd, cnv, depth, arena, alen, fetches, S.xk, base,
-                       256 * W, threadIdx.x, NT);
+    if (nv >= 1) {
+        // one 32-byte load per string brings its handle, the word at the
+        // segment's depth and the next one (the first round's two-word
+        // window) -- instead of three dependent rounds of loads
+#pragma unroll
+        for (int e = 0; e < ITEMS; e++) {
+            const int i = base + e;
+            if (i < m) {
+                const Rec r = segrec[i];
+                S.h[i] = r.h;
+                key[e] = r.w[0];
+                if (nv >= 2) S.kb1[i] = r.w[1];
+            }
+        }
+        __syncthreads();
+    } else {
+        for (int i = threadIdx.x; i < m; i += NT) S.h[i] = segrec[i].h;
+        __syncthreads();
+        rekey<ITEMS, true>(key, meta, segrec, S.h, cd, cnv, depth, arena, alen, fetches, S.xk, base,
+                           256 * W, threadIdx.x, NT);
+    }
     bool group_mode = false, first_round = true, used_two = false;
     int rounds = 0;
     uint64_t k1[ITEMS];  // second word of the slot in a two-word round
@@ -921,7 +938,7 @@ __global__ void __launch_bounds__(32 * W, CTA_SORT_WARPS_PER_SM / W) k_cta_sort(
                     o |= key[e];
                     a &= key[e];
                     if (try_two) {
-                        k1[e] = segrec[base + e].w[1];
+                        k1[e] = nv >= 2 ? S.kb1[base + e] : segrec[base + e].w[1];
                         o1 |= k1[e];
                         a1 &= k1[e];
                     }
