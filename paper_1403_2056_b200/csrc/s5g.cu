@@ -1487,6 +1487,10 @@ static int64_t small_max_of(int64_t t_medium) {
     return std::min<int64_t>(SMALL_MAX, std::max<int64_t>(1, t_medium - 1));
 }
 
+#ifndef WIDE_TILE
+#define WIDE_TILE 32768  // strings per classify / scatter CTA of a big full-width step (8192: scatter -13 %, count matrix scan +300 %)
+#endif
+
 struct Workspace {
     Rec *recA, *recB;
     uint16_t* bid;
@@ -1518,9 +1522,10 @@ static size_t carve(Workspace* w, uint8_t* base, int64_t n, int64_t t_medium) {
     const int64_t large_min = small_max_of(t_medium) + 1;
     w->steps_cap = nn / large_min + 2;
     // big steps round their tile count up to whole waves: <= 2x the tiles
-    w->tiles_cap = 2 * (nn / TILE) + w->steps_cap + 1 + (nn + 2 * w->steps_cap) / 32 +
+    const int64_t ctile = std::min<int64_t>(MIN_TILE, WIDE_TILE);  // the smallest tile a step uses
+    w->tiles_cap = 2 * (nn / ctile) + w->steps_cap + 1 + (nn + 2 * w->steps_cap) / 32 +
                    (nn + 2 * w->steps_cap) / 1024 + 2 * w->steps_cap + 2;
-    w->cnt_cap = nn * (2 * (int64_t)NBMAX / TILE + 2) + w->steps_cap * 2 +
+    w->cnt_cap = nn * (2 * (int64_t)NBMAX / ctile + 2) + w->steps_cap * 2 +
                  2 * (int64_t)NBMAX;  // a small root's MIN_TILE tiles: <= (n / MIN_TILE + 1) * NBMAX
     w->bk_cap = nn + 2 * w->steps_cap;
     w->tree_cap = nn / 2 + 4 * w->steps_cap + 2;
@@ -1936,6 +1941,15 @@ static int sort_impl_body(const s5g_sort_args* a, int dev_id) {
                 d.nb = 2 * d.v + 1;
                 d.nvalid = s.flags & SEG_NV_MASK;
                 d.ntiles = (int32_t)((s.n + TILE - 1) / TILE);
+                if (d.nb >= NBMAX && s.n >= (int64_t)WIDE_TILE * 4 * g_sms)
+                    // a full-width (16 383-bucket) step over many strings: tiles
+                    // of WIDE_TILE, so a tile holds ~WIDE_TILE / 16 383 strings
+                    // per bucket and the ~2 x g_sms tiles in flight keep each
+                    // bucket's write frontier (all buckets: ~16 383 x 2 g_sms x
+                    // WIDE_TILE / 16 383 records) inside the L2 -- a bucket's
+                    // 128-byte lines are completed there instead of leaving as
+                    // scattered 32-byte sector writes
+                    d.ntiles = (int32_t)((s.n + WIDE_TILE - 1) / WIDE_TILE);
                 if (round == 0 && d.ntiles < 2 * g_sms)
                     // a small root (C1: 10^6 strings = 31 tiles) would run on a
                     // fifth of the SMs: spread it over up to two CTAs per SM
