@@ -1570,6 +1570,13 @@ static constexpr size_t SMEM_SAMPLE_ROOT =
 static constexpr size_t SMEM_CLS_UNROLL = (size_t)(VMAX + 1) * 8 + (size_t)(NBMAX + 1) / 2 * 4;
 static constexpr size_t SMEM_CLS = SMEM_CLS_UNROLL + (size_t)(VMAX + 1) * 2;
 static constexpr size_t SMEM_SC = (size_t)(NBMAX + 1) * 5;
+// A single full-width step over many tiles (the root) scatters with ONE CTA
+// per SM (this much shared memory prevents a second): half the tiles in
+// flight halve every bucket's write frontier, so more of a bucket's 128-byte
+// lines are completed in the L2 before they are written back (C5 root
+// scatter 7.3 -> 6.5 ms, C2 0.48 -> 0.41 ms); batched later steps keep two
+// CTAs per SM (one is slower there: 1.6 -> 2.4 ms).
+static constexpr size_t SMEM_SC_WIDE = SMEM_SC + 40000;
 
 static int set_smem_attrs() {
     // per device: kernel attributes + the byte-PEXT table of the finishers
@@ -1605,7 +1612,7 @@ static int set_smem_attrs() {
                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_CLS_UNROLL));
     CK(cudaFuncSetAttribute(k_classify<S5G_VARIANT_EQUAL>,
                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_CLS));
-    CK(cudaFuncSetAttribute(k_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_SC));
+    CK(cudaFuncSetAttribute(k_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_SC_WIDE));
     CK(cudaFuncSetAttribute(k_step_cta<S5G_VARIANT_UNROLL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)sizeof(StepCtaSmem)));
     CK(cudaFuncSetAttribute(k_step_cta<S5G_VARIANT_EQUAL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -2068,7 +2075,9 @@ static int sort_impl_body(const s5g_sort_args* a, int dev_id) {
                                                          w.ctr)));
             CK(cudaGetLastError());
             PROF(K_SCATTER, round_elems, 66LL * round_elems,
-                 (k_scatter<<<ntiles, SC_NT, SMEM_SC, st>>>(w.steps, w.tile_step, recX, w.bid,
+                 (k_scatter<<<ntiles, SC_NT,
+                              nsteps == 1 && steps[0].nb >= NBMAX && ntiles >= 4u * g_sms ? SMEM_SC_WIDE : SMEM_SC,
+                              st>>>(w.steps, w.tile_step, recX, w.bid,
                                                            w.cnt, w.tot, w.bstart, w.tpos, recY,
                                                            a->out_handles, lcps)));
             CK(cudaGetLastError());
