@@ -633,6 +633,9 @@ __global__ void __launch_bounds__(SC_NT, 2) k_scatter(
 #endif
 constexpr int STEP_NT = STEP_NT_CFG;                  // threads of a fused single-CTA step
 constexpr int STEP_MINB = 1024 / STEP_NT;             // resident CTAs per SM (32 warps)
+#ifndef STEP_STACK
+#define STEP_STACK 64  // children a fused step keeps for itself (depth-first)
+#endif
 struct StepCtaSmem {
     uint64_t s[16 * (MED_VMAX + 1)];       // sorted sample
     uint64_t tree[MED_VMAX + 1], inorder[MED_VMAX + 1];
@@ -654,8 +657,21 @@ __global__ void __launch_bounds__(STEP_NT, STEP_MINB) k_step_cta(
     int64_t* __restrict__ lcps, Counters* __restrict__ ctr) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     StepCtaSmem& S = *reinterpret_cast<StepCtaSmem*>(smem_raw);
-    const SegDev sg = segs[blockIdx.x];
+    SegDev sg = segs[blockIdx.x];
     if (sg.n > MED_MAX) return;  // device-wide path
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned my_fetch = 0;
+    __shared__ uint64_t s_red[2][STEP_NT / 32][NCACHE];
+    __shared__ int s_flag;
+    // Depth-first: children too big for the finishers are pushed on a
+    // CTA-local stack and stepped by this CTA right away, while their records
+    // (just written by this CTA) are still in the L2 -- instead of a round
+    // trip through the next round's launch and HBM.
+    __shared__ SegDev s_stk[STEP_STACK];
+    __shared__ int s_top;
+    if (threadIdx.x == 0) s_top = 0;
+    __syncthreads();
+    for (;;) {
     const int n = sg.n;
     const int64_t lo = sg.lo;
     int64_t depth = sg.depth;
@@ -667,13 +683,9 @@ __global__ void __launch_bounds__(STEP_NT, STEP_MINB) k_step_cta(
     const int count = med_sample_count(v);
     int P = 1;
     while (P < count) P <<= 1;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    unsigned my_fetch = 0;
     // cached words consumed in place: X[i].w[wo] is the word at `depth`,
     // nvalid words from wo on are valid
     int wo = 0;
-    __shared__ uint64_t s_red[2][STEP_NT / 32][NCACHE];
-    __shared__ int s_flag;
     for (;;) {
         // ---- refill the cached words when the segment ran out of them ----
         if (!nvalid) {
@@ -844,7 +856,13 @@ __global__ void __launch_bounds__(STEP_NT, STEP_MINB) k_step_cta(
                             small_out[cls.off[ci] + atomicAdd(&ctr->n_cls[ci], 1ull)] = c;
                             atomicAdd(&ctr->cls_elems[ci], (unsigned long long)size);
                         } else {
-                            large_out[atomicAdd(&ctr->n_large, 1ull)] = c;
+                            // a child of a fused step fits one (<= MED_MAX):
+                            // this CTA steps it next while it is L2-hot
+                            const int slot = atomicAdd(&s_top, 1);
+                            if (slot < STEP_STACK)
+                                s_stk[slot] = c;
+                            else
+                                large_out[atomicAdd(&ctr->n_large, 1ull)] = c;
                         }
                     }
                 }
@@ -942,6 +960,15 @@ __global__ void __launch_bounds__(STEP_NT, STEP_MINB) k_step_cta(
                 }
             }
         }
+    }
+    // ---- next segment of this CTA: the most recently pushed child ----------
+    __syncthreads();  // the scatter's writes and the children pushes are done
+    const int top = min(s_top, STEP_STACK);
+    if (top == 0) break;
+    sg = s_stk[top - 1];
+    __syncthreads();
+    if (threadIdx.x == 0) s_top = top - 1;
+    __syncthreads();
     }
     my_fetch = __reduce_add_sync(0xffffffffu, my_fetch);
     if (lane == 0 && my_fetch) atomicAdd(&ctr->fetches, (unsigned long long)my_fetch);
