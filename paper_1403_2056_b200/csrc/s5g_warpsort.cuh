@@ -501,16 +501,20 @@ __device__ void warp_finish(const int64_t* __restrict__ hbt, uint16_t* __restric
                             Rec* __restrict__ segrec, int64_t cd,
                             int cnv, int g0, int gn, int64_t depth, uint64_t (&key)[IT],
                             const uint8_t* __restrict__ arena, int64_t alen,
-                            int64_t* __restrict__ lcp_seg, unsigned& fetches, int lane) {
+                            int64_t* __restrict__ lcp_seg, unsigned& fetches, int lane,
+                            bool have_keys = false) {
+    // have_keys: key[] already holds the words at depth of slots lane*IT+e
+    // (k_warp_sort's one-load prologue)
     uint32_t meta[IT];
 #pragma unroll
     for (int e = 0; e < IT; e++) {
         const int i = lane * IT + e;
-        key[e] = ~0ull;
+        if (!have_keys || i >= gn) key[e] = ~0ull;
         meta[e] = i < gn ? (1u << 22) | ord[g0 + i] : (uint32_t)i << 11;
     }
-    rekey<IT, false>(key, meta, segrec, hbt, cd, cnv, depth, arena, alen, fetches, xs + g0,
-                     lane * IT, gn, lane, 32);
+    if (!have_keys)
+        rekey<IT, false>(key, meta, segrec, hbt, cd, cnv, depth, arena, alen, fetches, xs + g0,
+                         lane * IT, gn, lane, 32);
     int wrounds = 0;
     for (;;) {
         // ---- sort the active slots by (group, word, tag) ------------------
@@ -673,18 +677,22 @@ __global__ void __launch_bounds__(ws_nt(ITEMS), WS_MINB) k_warp_sort(
     int64_t* wh = s_h[w];
     uint16_t* wo = s_o[w];
     unsigned fetches = 0;
+    // one 32-byte load per string: its handle and, when cached, the word at
+    // the segment's depth (slot = tag = lane * ITEMS + e)
+    uint64_t key[ITEMS];
 #pragma unroll
     for (int e = 0; e < ITEMS; e++) {
-        const int i = e * 32 + lane;
+        const int i = lane * ITEMS + e;
         if (i < m) {
-            wh[i] = segrec[i].h;
+            const Rec r = segrec[i];
+            wh[i] = r.h;
             wo[i] = (uint16_t)i;
+            key[e] = r.w[0];
         }
     }
     __syncwarp();
-    uint64_t key[ITEMS];
     warp_finish<ITEMS>(wh, wo, s_k[w], s_x[w], segrec, sg.depth, nv, 0, m, sg.depth, key, arena, alen,
-                       lcps ? lcps + lo : nullptr, fetches, lane);
+                       lcps ? lcps + lo : nullptr, fetches, lane, nv >= 1);
     __syncwarp();
 #pragma unroll
     for (int e = 0; e < ITEMS; e++) {
