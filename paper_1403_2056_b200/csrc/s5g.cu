@@ -1549,7 +1549,9 @@ static size_t carve(Workspace* w, uint8_t* base, int64_t n, int64_t t_medium) {
     const int64_t large_min = small_max_of(t_medium) + 1;
     w->steps_cap = nn / large_min + 2;
     // big steps round their tile count up to whole waves: <= 2x the tiles
-    const int64_t ctile = std::min<int64_t>(MIN_TILE, WIDE_TILE);  // the smallest tile a step uses
+    // the smallest tile of a step over more than 2 x g_sms tiles (a small root's
+    // MIN_TILE tiles are bounded by the 2 * NBMAX term of cnt_cap)
+    const int64_t ctile = std::min<int64_t>(TILE, WIDE_TILE);
     w->tiles_cap = 2 * (nn / ctile) + w->steps_cap + 1 + (nn + 2 * w->steps_cap) / 32 +
                    (nn + 2 * w->steps_cap) / 1024 + 2 * w->steps_cap + 2;
     w->cnt_cap = nn * (2 * (int64_t)NBMAX / ctile + 2) + w->steps_cap * 2 +
