@@ -1048,7 +1048,7 @@ __global__ void k_lengths(const uint8_t* __restrict__ arena, int64_t alen,
 }
 
 // Pack strings (terminator included) to dst[dst_off[i] ..]: the send buffer
-// of the multi-GPU exchange.  One warp per string, 8-byte chunks.
+// of the multi-GPU exchange.
 // One thread per string (its bytes and terminator, arena[h .. h+L]): the
 // source is read as aligned words with funnel shifts (load_word_le), the
 // destination written as aligned 8-byte words with byte stores only at the
@@ -2187,8 +2187,6 @@ static int sort_impl_body(const s5g_sort_args* a, int dev_id) {
     }
     CK(cudaMemcpyAsync(&hc, w.ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    // k_seg_sort: (h, key) in, (handle, lcp) out per element; (handle, word)
-    // per re-keyed element
     // register finishers: record (32 B) in per string, handle + lcp (16 B) out;
     // modelled as 32 B/string in the launches above
     if (a->stats) {
