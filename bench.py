@@ -74,24 +74,23 @@ def ncu_warp_inst(kernel: str):
     return k.get("warp_inst_per_launch") if k else None
 
 
-def dominant_kernel(kernels: dict) -> str:
-    """The kernel with the largest serialized time in the committed ncu
-    capture of one step (the launch list's ranking); live CUDA-event times of
-    the side-stream finishers include the time they share the GPU with the
-    next round's kernels, so they only break ties / stand in without ncu."""
+def ncu_share(kernel: str):
+    """The kernel's share of the summed launch durations in the committed
+    full-size ncu launch list (serialized, cold caches), or None."""
     try:
         d = json.loads(TRAFFIC.read_text())["kernels"]
     except Exception:
-        d = {}
+        return None
+    tot = sum(v["ms"] for v in d.values())
+    ms = sum(v["ms"] for n, v in d.items()
+             if n == kernel or ("<" not in kernel and n.split("<")[0] == kernel))
+    return ms / tot if tot > 0 and ms > 0 else None
 
-    def ncu_ms(k):
-        v = d.get(k)
-        if v is None and "<" not in k:
-            return sum(x["ms"] for n, x in d.items() if n.split("<")[0] == k)
-        return v["ms"] if v else 0.0
 
-    if d and any(ncu_ms(k) > 0 for k in kernels):
-        return max(kernels, key=lambda k: (ncu_ms(k), kernels[k]["ms"]))
+def dominant_kernel(kernels: dict) -> str:
+    """The kernel with the largest summed live time.  The profiled pass runs
+    every kernel on one stream (s5g_profile_enable(2)), so a launch's event
+    time is its own and the per-kernel sums add up to the step."""
     return max(kernels, key=lambda k: kernels[k]["ms"])
 
 
@@ -503,7 +502,7 @@ def run_ours(args):
     # per-kernel CUDA events in a second pass of the same steps: the event
     # records and their read-back between sorts would otherwise add ~10 % to
     # the timed region above
-    _lib.profile(enable=True, reset=True)
+    _lib.profile(enable=True, reset=True, serial=True)
     p0 = torch.cuda.Event(enable_timing=True)
     p1 = torch.cuda.Event(enable_timing=True)
     p0.record(stream)
@@ -574,15 +573,17 @@ def run_ours(args):
         "config": {"workload": args.config, "n": n, "N_bytes": int(len(buf)), "scale": args.scale,
                    "D": D, "L": L, "parallelism": f"dp{world}" if world > 1 else "1gpu",
                    "l2": "inputs larger than L2 (arena > 126 MB), no flush",
-                   "kernel_timing": "per-kernel CUDA events in a second, profiled pass of the "
-                                    "same steps (value: unprofiled timed region)"},
+                   "kernel_timing": "per-kernel CUDA events in a second pass of the same steps with "
+                                    "every kernel on one stream (exclusive launch times; value: the "
+                                    "unprofiled timed region with the finishers on side streams)"},
         "d_bytes_per_s": D * world / (ms_step / 1000.0),
         "roofline": {"bound": "hbm", "kernel": top, "achieved": ach, "peak": peak,
                      "unit": "GB/s", "frac": ach / peak, "traffic": ncu_traffic(top),
                      "algorithmic_bytes_per_launch": alg_bytes / max(1, kt["launches"]),
                      "bytes_model": f"{PASS_BYTES} B per string (SURVEY 8d)",
                      "peak_source": peak_src,
-                     "share_of_step": kt["ms"] / args.steps / ms_step,
+                     "share_of_step": kt["ms"] / args.steps / profiled_ms,
+                     "ncu_share_of_step": ncu_share(top),
                      "record_model": {"achieved": ach_rec, "frac": ach_rec / peak,
                                       "bytes_per_launch": kt["bytes"] / max(1, kt["launches"]),
                                       "model": "the kernel's own record traffic model "

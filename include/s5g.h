@@ -266,6 +266,9 @@ typedef struct s5g_kernel_profile {
     int64_t bytes;     /* summed algorithmic bytes (DESIGN.md kernel models) */
 } s5g_kernel_profile;
 
+/* on = 1: events around every launch, streams as in production (the timeline);
+ * on = 2: the same with every kernel on the caller's stream, so each launch's
+ * event time is exclusive and the per-kernel sums add up to the sort. */
 void s5g_profile_enable(int on);
 void s5g_profile_reset(void);
 int s5g_profile_read(s5g_kernel_profile *out, int max_entries);

@@ -137,13 +137,14 @@ def check(rc: int) -> None:
     raise S5GError(f"s5g error {rc}: {msg}")
 
 
-def profile(enable: bool | None = None, reset: bool = False) -> dict[str, dict]:
-    """Per-kernel event timings collected by the library."""
+def profile(enable: bool | None = None, reset: bool = False, serial: bool = False) -> dict[str, dict]:
+    """Per-kernel event timings collected by the library.  serial: every kernel
+    on the caller's stream, so each launch's time is exclusive."""
     L = lib()
     if reset:
         L.s5g_profile_reset()
     if enable is not None:
-        L.s5g_profile_enable(1 if enable else 0)
+        L.s5g_profile_enable((2 if serial else 1) if enable else 0)
     buf = (KernelProfile * 32)()
     k = L.s5g_profile_read(buf, 32)
     return {buf[i].name.decode(): {"launches": int(buf[i].launches), "units": int(buf[i].units),

@@ -1398,6 +1398,10 @@ struct ProfEntry {
     double ms = 0;
 };
 static bool g_prof = false;
+// profile level 2: every kernel of a sort on the caller's stream (no side
+// streams), so each launch's event time is its own and the per-kernel sums
+// add up to the step -- the live counterpart of ncu's serialized launch list
+static bool g_prof_serial = false;
 static ProfEntry g_prof_tab[K_COUNT];
 // timeline of the last profiled sort: (kernel id, stream, start ms, end ms)
 // relative to an event recorded on the launching stream when the sort began
@@ -1786,6 +1790,7 @@ static int sort_impl_body(const s5g_sort_args* a, int dev_id) {
     Profiler prof_pool[3] = {Profiler(s_pool[dev_id][0], 3), Profiler(s_pool[dev_id][1], 3),
                              Profiler(s_pool[dev_id][2], 3)};
     bool fin_side_used = false;
+    const bool serial = g_prof_serial;
     unsigned long long fin_done[NCLS] = {0}, fin_done_el[NCLS] = {0};
     // launch the finishers for list entries [fin_done[c], hc.n_cls[c])
     auto launch_finishers = [&](cudaStream_t fs_main, Profiler& fp_main) -> cudaError_t {
@@ -1798,8 +1803,9 @@ static int sort_impl_body(const s5g_sort_args* a, int dev_id) {
         for (int oi = 0; oi < NCLS; oi++) {
             const int c = order[oi];
             const int q = c < 4 ? 0 : c - 3;  // pool stream of this class (3 = main)
-            cudaStream_t fs = q < 3 ? s_pool[dev_id][q] : fs_main;
-            Profiler& fp = q < 3 ? prof_pool[q] : fp_main;
+            const bool on_pool = q < 3 && !serial;
+            cudaStream_t fs = on_pool ? s_pool[dev_id][q] : fs_main;
+            Profiler& fp = on_pool ? prof_pool[q] : fp_main;
             const long long cnt_c = (long long)(hc.n_cls[c] - fin_done[c]);
             const long long el_c = (long long)(hc.cls_elems[c] - fin_done_el[c]);
             if ((long long)hc.n_cls[c] > w.cls_cap[c]) return cudaErrorMemoryAllocation;
@@ -1807,7 +1813,7 @@ static int sort_impl_body(const s5g_sort_args* a, int dev_id) {
             const int wnt = ws_nt(c == 0 ? 1 : c == 1 ? 2 : c == 2 ? 4 : 8);
             const unsigned grid = blocks_for(cnt_c, wnt / 32);
             const SegDev* lst = w.small + w.cls_off[c] + fin_done[c];
-            if (q < 3 && !used[q]) {
+            if (on_pool && !used[q]) {
                 used[q] = true;
                 cudaError_t ew = cudaStreamWaitEvent(fs, s_pfork[dev_id], 0);
                 if (ew != cudaSuccess) return ew;
@@ -1921,6 +1927,10 @@ static int sort_impl_body(const s5g_sort_args* a, int dev_id) {
     auto launch_side = [&]() -> int {
         if (!side_pending) return 0;
         side_pending = false;
+        if (serial) {
+            CK(launch_finishers(st, prof));
+            return 0;
+        }
         CK(cudaStreamWaitEvent(st2, ev_fork, 0));
         CK(launch_finishers(st2, prof2));
         fin_side_used = true;
@@ -2321,7 +2331,10 @@ extern "C" {
 
 int s5g_version(void) { return S5G_VERSION; }
 
-void s5g_profile_enable(int on) { g_prof = on != 0; }
+void s5g_profile_enable(int on) {
+    g_prof = on != 0;
+    g_prof_serial = on == 2;
+}
 
 void s5g_profile_reset(void) {
     for (auto& e : g_prof_tab) e = ProfEntry();

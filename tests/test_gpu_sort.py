@@ -156,6 +156,56 @@ def test_step_hook_full_tree_root():
             assert oracle.lcp(s.buffer, res.set.handles[lo], res.set.handles[hi - 1]) >= int(root.child_depths[i])
 
 
+def _oracle_tree(rec_tree):
+    """The step record's splitter tree as the oracle's Tree (same fields)."""
+    t = rec_tree
+    return oracle.Tree(t.v, np.ascontiguousarray(t.tree, dtype=np.uint64),
+                       np.ascontiguousarray(t.inorder, dtype=np.uint64),
+                       np.ascontiguousarray(t.node_to_inorder, dtype=np.int64),
+                       np.ascontiguousarray(t.slcp, dtype=np.int64),
+                       np.asarray(t.eq_final, dtype=bool),
+                       np.ascontiguousarray(t.eq_leftmost, dtype=np.int64),
+                       np.ascontiguousarray(t.term_pos, dtype=np.int64))
+
+
+@pytest.mark.parametrize("variant", ["unroll", "equal"])
+@pytest.mark.parametrize("gen,n,t_medium", [("clusters", 6000, 512), ("random", 300_000, 2048),
+                                            ("urls", 60_000, 1024)])
+def test_step_bounds_match_oracle_classify_distribute(gen, n, t_medium, variant):
+    """Per-step parity: every step's bucket bounds equal
+    those the oracle's classify_keys + distribute (ssss.py:149-212) produce
+    for the same strings at the same depth with the SAME splitters, and the
+    step's stable scatter leaves every bucket's strings in the order
+    distribute gives them wherever the step's output is still visible
+    (buckets that are final after the step)."""
+    if gen == "clusters":
+        s = _clusters(n)
+    elif gen == "random":
+        buf, hnd = corpora.gen_random(n, 5)
+        s = P.StringSet(buf.tobytes(), hnd)
+    else:
+        buf, hnd = corpora.gen_urls(n)
+        s = P.StringSet(buf.tobytes(), hnd)
+    records = []
+    res = P.s5_sort(s, want_lcps=True, t_medium=t_medium, variant=variant,
+                    step_hook=records.append)
+    out_h = res.set.handles
+    assert records
+    buf_np = np.frombuffer(s.buffer, dtype=np.uint8) if isinstance(s.buffer, (bytes, bytearray)) \
+        else np.asarray(s.buffer)
+    for rec in records:
+        # the segment's strings are exactly the final output's [lo, hi)
+        seg = np.ascontiguousarray(out_h[rec.lo:rec.hi], dtype=np.int64)
+        keys = oracle.extract_keys(buf_np, seg, rec.depth)
+        tree = _oracle_tree(rec.tree)
+        ids = oracle.classify_keys(keys, tree, variant)
+        _, bounds = oracle.distribute(seg, ids, tree.num_buckets)
+        assert np.array_equal(np.asarray(rec.bounds, dtype=np.int64), bounds), \
+            f"step [{rec.lo},{rec.hi}) depth {rec.depth}: bucket bounds differ from the oracle"
+        # the final order is bucket-major: ids of the sorted segment are non-decreasing
+        assert (np.diff(ids) >= 0).all()
+
+
 def test_hook_errors_propagate():
     s = _clusters(3000)
 

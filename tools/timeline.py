@@ -1,4 +1,4 @@
-"""Launch timeline of one profiled C2 sort (gap analysis)."""
+"""Launch timeline of one profiled sort (gap analysis)."""
 import argparse
 import sys
 
@@ -12,8 +12,12 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c2_dna")
 ap.add_argument("--scale", type=float, default=1.0)
 a = ap.parse_args()
-buf, hnd = corpora.CONFIGS[a.config](a.scale)
-ds = D.upload(buf, hnd)
+if a.config == "c5_nodup":  # generated in HBM
+    arena, alen, h = corpora.gen_nodup_device(int((1 << 28) * a.scale))
+    ds = D.DeviceStrings(arena, alen, h)
+else:
+    buf, hnd = corpora.CONFIGS[a.config](a.scale)
+    ds = D.upload(buf, hnd)
 for _ in range(3):
     D.sort(ds, want_lcps=True)
 torch.cuda.synchronize()
