@@ -1519,8 +1519,14 @@ static int64_t small_max_of(int64_t t_medium) {
 }
 
 #ifndef WIDE_TILE
-#define WIDE_TILE 32768  // strings per classify / scatter CTA of a big full-width step (8192: scatter -13 %, count matrix scan +300 %)
+// strings per classify / scatter CTA of a big full-width step.  The tile x
+// bucket count matrix (and its column scan) shrinks with the tile, the
+// scatter's time does not depend on it (C5 root: 6.6 / 6.5 / 6.6 / 6.8 ms at
+// 65280 / 32768 / 16384 / 8192, column scan 0.30 / 0.72 / 1.50 / 3.02 ms).
+// k_classify packs a tile's bucket counts as u16: a tile stays below 65536.
+#define WIDE_TILE 65280
 #endif
+static_assert(WIDE_TILE < 65536, "k_classify's per-tile bucket counts are u16");
 
 struct Workspace {
     Rec *recA, *recB;
@@ -1744,22 +1750,6 @@ static int sort_impl_body(const s5g_sort_args* a, int dev_id) {
         CK(cudaStreamSynchronize(st));
         return 0;
     }
-    if (g_prof) {
-        if (!g_tl_base) CK(cudaEventCreate(&g_tl_base));
-        g_timeline.clear();
-        CK(cudaEventRecord(g_tl_base, st));
-    }
-    Profiler prof(st);
-    Workspace w;
-    size_t need = carve(&w, nullptr, n, t_medium);
-    if (!a->workspace || a->workspace_bytes < need)
-        return fail(S5G_E_WORKSPACE, "workspace too small: need " + std::to_string(need));
-    carve(&w, (uint8_t*)a->workspace, n, t_medium);
-    const int64_t small_max = small_max_of(t_medium);
-    ClassLists cls_lists;
-    for (int c = 0; c < NCLS; c++) cls_lists.off[c] = w.cls_off[c];
-
-    Counters hc{};
     // side stream (per device, created once): finishers of earlier rounds run
     // there concurrently with the next round's device-wide step
     // and a high-priority stream for the root step's sample, drawn from the
@@ -1781,6 +1771,22 @@ static int sort_impl_body(const s5g_sort_args* a, int dev_id) {
             CK(cudaEventCreateWithFlags(&s_pjoin[dev_id][q], cudaEventDisableTiming));
         }
     }
+    if (g_prof) {
+        if (!g_tl_base) CK(cudaEventCreate(&g_tl_base));
+        g_timeline.clear();
+        CK(cudaEventRecord(g_tl_base, st));
+    }
+    Profiler prof(st);
+    Workspace w;
+    size_t need = carve(&w, nullptr, n, t_medium);
+    if (!a->workspace || a->workspace_bytes < need)
+        return fail(S5G_E_WORKSPACE, "workspace too small: need " + std::to_string(need));
+    carve(&w, (uint8_t*)a->workspace, n, t_medium);
+    const int64_t small_max = small_max_of(t_medium);
+    ClassLists cls_lists;
+    for (int c = 0; c < NCLS; c++) cls_lists.off[c] = w.cls_off[c];
+
+    Counters hc{};
     cudaStream_t st2 = s_st2[dev_id], st_hi = s_hi[dev_id];
     cudaEvent_t ev_fork = s_fork[dev_id], ev_join = s_join[dev_id], ev_samp = s_samp[dev_id];
     Profiler prof2(st2, 1), prof_hi(st_hi, 2);
@@ -2065,6 +2071,20 @@ static int sort_impl_body(const s5g_sort_args* a, int dev_id) {
                 maxv = std::max(maxv, d.v);
                 while (maxP < d.count) maxP <<= 1;
                 sample_bytes += (long long)d.count * (d.nvalid ? 8 : 16) + 27LL * d.v;
+            }
+            static const bool trace = getenv("S5G_TRACE") != nullptr;
+            if (trace) {
+                int64_t nmax = 0, tot = 0;
+                int nv0 = 0;
+                for (auto& d : steps) {
+                    nmax = std::max<int64_t>(nmax, d.n);
+                    tot += d.n;
+                    nv0 += d.nvalid == 0;
+                }
+                fprintf(stderr, "[s5g] round %d: %d device-wide steps (%lld strings, largest %lld, %d refill), "
+                                "maxP %d maxv %d, %lld fused segments (%lld strings)\n",
+                        round, nsteps, (long long)tot, (long long)nmax, nv0, maxP, maxv,
+                        (long long)n_med, (long long)med_elems);
             }
             if (round == 0 && early_root) {
                 CK(cudaStreamWaitEvent(st, ev_samp, 0));  // root tree drawn on st_hi

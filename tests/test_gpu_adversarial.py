@@ -87,3 +87,18 @@ def test_heavy_duplication_shuffled_handles():
     buf = np.frombuffer(b"".join(w + b"\0" for w in items), dtype=np.uint8)
     off = np.r_[0, np.cumsum([len(w) + 1 for w in items])[:-1]].astype(np.int64)
     _check(buf, rng.permutation(off))
+
+
+def test_full_width_tiles_with_one_bucket():
+    """A full-width (16 383-bucket) root over enough strings for the widest
+    classify / scatter tiles (WIDE_TILE = 65 280 strings, n >= 4 x 148 tiles)
+    whose strings nearly all fall into ONE equality bucket: every tile's
+    count of that bucket is the tile size, the largest value the packed u16
+    per-tile counts must hold."""
+    n = 65280 * 4 * 148 + 12345
+    rng = np.random.default_rng(7)
+    buf = np.zeros((n, 4), dtype=np.uint8)
+    buf[:, :3] = np.frombuffer(b"abc", dtype=np.uint8)
+    odd = rng.integers(0, n, size=5000)
+    buf[odd, :3] = rng.integers(97, 123, size=(5000, 3), dtype=np.uint8)
+    _check(buf.reshape(-1), np.arange(n, dtype=np.int64) * 4)
