@@ -666,7 +666,7 @@ __global__ void __launch_bounds__(SC_NT, 2) k_scatter(
 // so the scatter's turn chain never waits on a record load.  Same outputs as
 // the device-wide step (ssss.py:281-358).
 #ifndef STEP_NT_CFG
-#define STEP_NT_CFG 512
+#define STEP_NT_CFG 256  // 4 CTAs per SM: more independent CTAs fill the step's barrier stalls (C5 37.6 -> 36.4 ms, C2 2.28 -> 2.23; 512: 2 CTAs, 1024: 41.8 ms)
 #endif
 constexpr int STEP_NT = STEP_NT_CFG;                  // threads of a fused single-CTA step
 constexpr int STEP_MINB = 1024 / STEP_NT;             // resident CTAs per SM (32 warps)
