@@ -511,7 +511,10 @@ __global__ void __launch_bounds__(1024) k_scan_buckets(
 // round.  Everything else (record loads for the next chunk, the ranks, the
 // 32-byte record writes) runs outside the turn, so the chain costs one
 // shared read-modify-write per distinct bucket of a round.
-constexpr int SCX_IT = 4;                             // rounds of 32 per chunk
+#ifndef SCX_IT_CFG
+#define SCX_IT_CFG 4
+#endif
+constexpr int SCX_IT = SCX_IT_CFG;                             // rounds of 32 per chunk
 constexpr int SCX_CHUNK = 32 * SCX_IT;                // strings per warp turn
 constexpr int SCX_SUB = SCX_CHUNK * (SC_NT / 32);     // 2048 strings per CTA pass
 static_assert(SC_NT / 32 == 16, "named-barrier turn chain assumes 16 warps");
@@ -670,6 +673,9 @@ __global__ void __launch_bounds__(SC_NT, 2) k_scatter(
 #endif
 constexpr int STEP_NT = STEP_NT_CFG;                  // threads of a fused single-CTA step
 constexpr int STEP_MINB = 1024 / STEP_NT;             // resident CTAs per SM (32 warps)
+#ifndef STEP_SC_IT
+#define STEP_SC_IT 2
+#endif
 #ifndef STEP_STACK
 #define STEP_STACK 64  // children a fused step keeps for itself (depth-first)
 #endif
@@ -942,7 +948,7 @@ __global__ void __launch_bounds__(STEP_NT, STEP_MINB) k_step_cta(
             }
         }
         __syncthreads();
-        constexpr int IT = SCX_IT;  // rounds of 32 whose loads are issued together
+        constexpr int IT = STEP_SC_IT;  // rounds of 32 whose loads are issued together
         for (int e0 = r0; e0 < r1; e0 += 32 * IT) {
             Rec rec[IT];
             uint32_t myb[IT], rel[IT];
@@ -1652,7 +1658,10 @@ static constexpr size_t SMEM_SC = (size_t)(NBMAX + 1) * 5;
 // lines are completed in the L2 before they are written back (C5 root
 // scatter 7.3 -> 6.5 ms, C2 0.48 -> 0.41 ms); batched later steps keep two
 // CTAs per SM (one is slower there: 1.6 -> 2.4 ms).
-static constexpr size_t SMEM_SC_WIDE = SMEM_SC + 40000;
+#ifndef SC_WIDE_PAD
+#define SC_WIDE_PAD 40000
+#endif
+static constexpr size_t SMEM_SC_WIDE = SMEM_SC + SC_WIDE_PAD;
 
 static int set_smem_attrs() {
     // per device: kernel attributes + the byte-PEXT table of the finishers
