@@ -190,6 +190,13 @@ int s5g_pack(const uint8_t *arena, int64_t arena_len, const int64_t *handles,
  * 16384) bytes. */
 int s5g_load_delimited(uint8_t *data, int64_t len, int32_t delimiter, int64_t *out_handles,
                        int64_t *out_n, void *workspace, size_t workspace_bytes, void *stream);
+/* The same with out_handles sized by the caller: room for `capacity` entries,
+ * of which terminators + 1 are written (a receiver that knows that n strings
+ * arrived passes n + 1 instead of reserving len + 1 entries);
+ * S5G_E_INVALID, with nothing written, if the data holds more. */
+int s5g_load_delimited_n(uint8_t *data, int64_t len, int32_t delimiter, int64_t *out_handles,
+                         int64_t capacity, int64_t *out_n, void *workspace,
+                         size_t workspace_bytes, void *stream);
 
 /* Stable grouping by destination rank for the all-to-all send buffer
  * (device): out_order[k] = index of the k-th string when strings are ordered
@@ -209,7 +216,9 @@ int s5g_positions(const int64_t *handles, int64_t n, const int64_t *query, int64
  * in_handles[i] the string at out_handles[j], for a stable sort's output
  * (equal handles -- the same string -- are matched in input order, so
  * repeated handles are fine).  Two stable radix sorts by handle; O(n), no
- * per-byte map.  max_handle bounds the handles (e.g. arena_len).  Device
+ * per-byte map -- or, when in_handles is strictly ascending (the string
+ * starts of a received arena; checked on the device), one binary search per
+ * string.  max_handle bounds the handles (e.g. arena_len).  Device
  * pointers; workspace: s5g_input_positions_workspace_bytes(n). */
 size_t s5g_input_positions_workspace_bytes(int64_t n);
 int s5g_input_positions(const int64_t *in_handles, const int64_t *out_handles, int64_t n,

@@ -1092,35 +1092,71 @@ __global__ void k_lengths(const uint8_t* __restrict__ arena, int64_t alen,
 
 // Pack strings (terminator included) to dst[dst_off[i] ..]: the send buffer
 // of the multi-GPU exchange.
-// One thread per string (its bytes and terminator, arena[h .. h+L]): the
+// Eight lanes per string (its bytes and terminator, arena[h .. h+L]): the
 // source is read as aligned words with funnel shifts (load_word_le), the
-// destination written as aligned 8-byte words with byte stores only at the
-// two edges it shares with its neighbours (a warp per string with byte
-// stores was a chain of dependent round trips per string).
+// destination written as aligned 8-byte words -- the eight lanes of a string
+// write 64 contiguous bytes per round -- with byte stores only at the two
+// edges a string shares with its neighbours (one lane per edge byte).  (One
+// thread per string walked its ~15 words alone: 1 TB/s on C5's strings; a
+// warp per string with byte stores was a chain of dependent round trips.)
+constexpr int PACK_G = 8;
+constexpr int PACK_S = 4;  // strings per lane group: their loads are issued together
 __global__ void k_pack(const uint8_t* __restrict__ arena, int64_t alen,
                        const int64_t* __restrict__ handles, const int64_t* __restrict__ lens,
                        const int64_t* __restrict__ dst_off, int64_t n, uint8_t* __restrict__ dst) {
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    // lens == NULL: sizes from the exclusive offsets (s5g_pack_plan's)
-    const int64_t h = handles[i], o = dst_off[i];
-    const int64_t L = lens ? lens[i] + 1 : dst_off[i + 1] - o;  // with the terminator
-    const int64_t e = o + L;
-    int64_t a = (o + 7) & ~int64_t(7);
-    if (a > e) a = e;
-    const int64_t z = e & ~int64_t(7);
-    auto byte_at = [&](int64_t q) -> uint8_t {
-        const int64_t s = h + (q - o);
-        return q - o < L - 1 && s < alen ? arena[s] : 0;
-    };
-    for (int64_t q = o; q < a; q++) dst[q] = byte_at(q);
-    for (int64_t q = a; q < z; q += 8) {
-        uint64_t w = load_word_le(arena, alen, h + (q - o));
-        const int64_t left = L - 1 - (q - o);  // string bytes left at q (the rest is 0)
-        if (left < 8) w &= left > 0 ? (~0ull >> (64 - 8 * left)) : 0ull;
-        *reinterpret_cast<uint64_t*>(dst + q) = w;
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t grp = t / PACK_G;
+    const int sub = (int)(t % PACK_G);
+    int64_t h[PACK_S], o[PACK_S], e[PACK_S], a[PACK_S], z[PACK_S];
+#pragma unroll
+    for (int u = 0; u < PACK_S; u++) {
+        const int64_t i = grp * PACK_S + u;
+        h[u] = o[u] = e[u] = 0;  // (an empty copy)
+        if (i < n) {
+            h[u] = handles[i];
+            o[u] = dst_off[i];
+            // lens == NULL: sizes from the exclusive offsets (s5g_pack_plan's)
+            e[u] = lens ? o[u] + lens[i] + 1 : dst_off[i + 1];  // with the terminator
+        }
     }
-    for (int64_t q = (z > a ? z : a); q < e; q++) dst[q] = byte_at(q);
+#pragma unroll
+    for (int u = 0; u < PACK_S; u++) {
+        a[u] = min((o[u] + 7) & ~int64_t(7), e[u]);
+        z[u] = max(e[u] & ~int64_t(7), a[u]);
+    }
+    // the word at dst offset q of string u: its bytes, then zeros
+    auto word_at = [&](int u, int64_t q) -> uint64_t {
+        uint64_t w = load_word_le(arena, alen, h[u] + (q - o[u]));
+        const int64_t left = e[u] - 1 - q;  // string bytes left at q (the rest is 0)
+        if (left < 8) w &= left > 0 ? (~0ull >> (64 - 8 * left)) : 0ull;
+        return w;
+    };
+    auto byte_at = [&](int u, int64_t q) -> uint8_t {
+        const int64_t sp = h[u] + (q - o[u]);
+        return q < e[u] - 1 && sp < alen ? arena[sp] : 0;
+    };
+    // two rounds of 64 bytes per string with all the group's loads in flight
+#pragma unroll
+    for (int r = 0; r < 2; r++) {
+        uint64_t w[PACK_S];
+#pragma unroll
+        for (int u = 0; u < PACK_S; u++) {
+            const int64_t q = a[u] + 8 * (sub + PACK_G * r);
+            w[u] = q < z[u] ? word_at(u, q) : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < PACK_S; u++) {
+            const int64_t q = a[u] + 8 * (sub + PACK_G * r);
+            if (q < z[u]) *reinterpret_cast<uint64_t*>(dst + q) = w[u];
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < PACK_S; u++) {
+        for (int64_t q = a[u] + 8 * (sub + PACK_G * 2); q < z[u]; q += 8 * PACK_G)
+            *reinterpret_cast<uint64_t*>(dst + q) = word_at(u, q);
+        if (o[u] + sub < a[u]) dst[o[u] + sub] = byte_at(u, o[u] + sub);  // < 8 head bytes
+        if (z[u] + sub < e[u]) dst[z[u] + sub] = byte_at(u, z[u] + sub);  // < 8 tail bytes
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -1318,30 +1354,103 @@ __global__ void k_iota_i32(int32_t* __restrict__ out, int64_t n) {
     const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (j < n) out[j] = (int32_t)j;
 }
+// in_handles strictly ascending (the string starts of a received arena): the
+// input position of a sorted handle is its rank -- a binary search whose top
+// levels stay in the L2 -- instead of two radix sorts of (handle, index).
+__global__ void k_pos_ascending(const int64_t* __restrict__ h, int64_t n, int* __restrict__ bad) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i + 1 < n && h[i] >= h[i + 1]) *bad = 1;
+}
+// Four queries per thread, branch-free (every query walks the same
+// ceil(log2(n + 1)) levels): four independent loads in flight per thread --
+// with one query per thread the search was a chain of ~25 dependent loads.
+constexpr int POS_Q = 4;
+__global__ void k_pos_search(const int64_t* __restrict__ in_h, const int64_t* __restrict__ out_h,
+                             int64_t n, int64_t top, int64_t* __restrict__ out_pos) {
+    const int64_t j0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x);
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    int64_t q[POS_Q], pos[POS_Q];
+#pragma unroll
+    for (int u = 0; u < POS_Q; u++) {
+        const int64_t j = j0 + u * stride;
+        q[u] = j < n ? out_h[j] : 0;
+        pos[u] = 0;  // elements below q[u] found so far
+    }
+    for (int64_t step = top; step > 0; step >>= 1) {
+#pragma unroll
+        for (int u = 0; u < POS_Q; u++) {
+            const int64_t p = pos[u] + step;
+            if (p <= n && __ldg(in_h + p - 1) < q[u]) pos[u] = p;
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < POS_Q; u++) {
+        const int64_t j = j0 + u * stride;
+        if (j < n) {
+            S5G_CHECK(pos[u] < n && in_h[pos[u]] == q[u]);
+            out_pos[j] = pos[u];
+        }
+    }
+}
 __global__ void k_pos_match(const int32_t* __restrict__ in_pos, const int32_t* __restrict__ out_idx,
                             int64_t n, int64_t* __restrict__ out_pos) {
     const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (k < n) out_pos[out_idx[k]] = in_pos[k];
 }
 // exchange plan: handle and size (with terminator) of the k-th string in
-// send order
+// send order.  Eight lanes per string look at eight consecutive aligned words
+// per round and vote for the first terminator (one thread per string walked
+// its words alone, a chain of dependent loads per string).
 __global__ void k_plan_sizes(const uint8_t* __restrict__ arena, int64_t alen,
                              const int64_t* __restrict__ handles, const int64_t* __restrict__ order,
                              int64_t n, int64_t* __restrict__ out_h, int64_t* __restrict__ size) {
-    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (k >= n) return;
-    const int64_t h = handles[order[k]];
-    out_h[k] = h;
-    int64_t e = h;  // terminator: a word at a time
-    for (;; e += WORD) {
-        const uint64_t z = zero_bytes(load_word_le(arena, alen, e));
-        if (z) {
-            e += (__ffsll((long long)z) - 1) >> 3;
-            break;
-        }
-        if (e >= alen) break;
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t grp = t / PACK_G;
+    const int sub = (int)(t % PACK_G), lane = threadIdx.x & 31, g0 = lane & ~(PACK_G - 1);
+    // PACK_S strings per lane group: handles, then the first 128 bytes of
+    // each, are fetched with all loads in flight
+    int64_t h[PACK_S];
+    uint64_t w0[PACK_S], w1[PACK_S];
+#pragma unroll
+    for (int u = 0; u < PACK_S; u++) {
+        const int64_t k = grp * PACK_S + u;
+        h[u] = k < n ? handles[order[k]] : -1;
     }
-    size[k] = min(e, alen) - h + 1;
+#pragma unroll
+    for (int u = 0; u < PACK_S; u++) {
+        const int64_t a = (h[u] & ~int64_t(7)) + 8 * sub;  // this lane's aligned word
+        w0[u] = h[u] >= 0 ? ld8_guard(arena, alen, a) : 0;  // (0 at or past alen: ends the string)
+        w1[u] = h[u] >= 0 ? ld8_guard(arena, alen, a + 8 * PACK_G) : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < PACK_S; u++) {
+        const int64_t k = grp * PACK_S + u;
+        const bool live = h[u] >= 0;
+        int64_t a = (h[u] & ~int64_t(7)) + 8 * sub;
+        bool done = !live;
+        int64_t e = alen;
+        for (int r = 0;; r++) {
+            uint64_t z = 0;
+            if (!done) {
+                uint64_t w = r == 0 ? w0[u] : r == 1 ? w1[u] : ld8_guard(arena, alen, a);
+                if (a < h[u]) w |= ~0ull >> (64 - 8 * (h[u] - a));  // bytes before the string
+                z = zero_bytes(w);
+            }
+            const unsigned vote = (__ballot_sync(0xffffffffu, z != 0) >> g0) & ((1u << PACK_G) - 1);
+            const int first = vote ? __ffs(vote) - 1 : 0;
+            const uint64_t zf = __shfl_sync(0xffffffffu, z, g0 + first);
+            if (!done && vote) {
+                e = (a - 8 * sub) + 8 * first + ((__ffsll((long long)zf) - 1) >> 3);
+                done = true;
+            }
+            a += 8 * PACK_G;
+            if (__all_sync(0xffffffffu, done)) break;
+        }
+        if (live && sub == 0) {
+            out_h[k] = h[u];
+            size[k] = min(e, alen) - h[u] + 1;
+        }
+    }
 }
 // bytes per destination from the exclusive offsets (off[n] = total)
 __global__ void k_plan_dest(const int64_t* __restrict__ off, int64_t n,
@@ -2850,7 +2959,7 @@ int s5g_pack(const uint8_t* arena, int64_t arena_len, const int64_t* handles,
     if (n <= 0) return n < 0 ? fail(S5G_E_INVALID, "negative n") : 0;
     cudaStream_t st = (cudaStream_t)stream;
     g_launches++;
-    k_pack<<<blocks_for(n, 256), 256, 0, st>>>(arena, arena_len, handles, lengths, dst_off, n,
+    k_pack<<<blocks_for((n + PACK_S - 1) / PACK_S * PACK_G, 256), 256, 0, st>>>(arena, arena_len, handles, lengths, dst_off, n,
                                                 dst);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(st));
@@ -2859,7 +2968,15 @@ int s5g_pack(const uint8_t* arena, int64_t arena_len, const int64_t* handles,
 
 int s5g_load_delimited(uint8_t* data, int64_t len, int32_t delimiter, int64_t* out_handles,
                        int64_t* out_n, void* workspace, size_t workspace_bytes, void* stream) {
+    return s5g_load_delimited_n(data, len, delimiter, out_handles, len + 1, out_n, workspace,
+                                workspace_bytes, stream);
+}
+
+int s5g_load_delimited_n(uint8_t* data, int64_t len, int32_t delimiter, int64_t* out_handles,
+                         int64_t capacity, int64_t* out_n, void* workspace,
+                         size_t workspace_bytes, void* stream) {
     if (len < 0 || delimiter < 0 || delimiter > 255) return fail(S5G_E_INVALID, "delimiter must be a byte value");
+    if (capacity < 0) return fail(S5G_E_INVALID, "negative capacity");
     cudaStream_t st = (cudaStream_t)stream;
     const int64_t nchunks = (len + LD_CHUNK - 1) / LD_CHUNK;
     if (workspace_bytes < (size_t)nchunks * 4 + 16) return fail(S5G_E_WORKSPACE, "workspace too small");
@@ -2874,14 +2991,18 @@ int s5g_load_delimited(uint8_t* data, int64_t len, int32_t delimiter, int64_t* o
     g_launches += 3;
     k_ld_count<<<(unsigned)nchunks, LD_NT, 0, st>>>(data, len, delimiter, chunk, bad);
     k_ld_scan<<<1, 1024, 0, st>>>(chunk, nchunks, d_n);
-    k_ld_write<<<(unsigned)nchunks, LD_NT, 0, st>>>(data, len, chunk, out_handles);
     CK(cudaGetLastError());
     int hbad = 0;
     int64_t hn = 0;
     CK(cudaMemcpyAsync(&hbad, bad, 4, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(&hn, d_n, 8, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
+    CK(cudaStreamSynchronize(st));  // the count, before any start is written
     if (hbad) return fail(S5G_E_INVALID, "input contains byte 0, which is reserved as terminator");
+    // (k_ld_write stores a start after every terminator: count + 1 entries)
+    if (hn + 1 > capacity) return fail(S5G_E_INVALID, "more strings than out_handles has room for");
+    k_ld_write<<<(unsigned)nchunks, LD_NT, 0, st>>>(data, len, chunk, out_handles);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(st));
     *out_n = hn;
     return 0;
 }
@@ -2955,6 +3076,27 @@ int s5g_input_positions(const int64_t* in_handles, const int64_t* out_handles, i
     int32_t* iota = (int32_t*)take(4 * n);
     int32_t* v_in = (int32_t*)take(4 * n);
     int32_t* v_out = (int32_t*)take(4 * n);
+    {
+        // strictly ascending input handles (a received arena's string starts):
+        // rank by binary search
+        int* bad = (int*)iota;
+        int hbad = 0;
+        CK(cudaMemsetAsync(bad, 0, 4, st));
+        g_launches++;
+        k_pos_ascending<<<blocks_for(n, 256), 256, 0, st>>>(in_handles, n, bad);
+        CK(cudaMemcpyAsync(&hbad, bad, 4, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (!hbad) {
+            g_launches++;
+            int64_t top = 1;
+            while (top * 2 <= n) top *= 2;
+            k_pos_search<<<blocks_for((n + POS_Q - 1) / POS_Q, 256), 256, 0, st>>>(in_handles, out_handles, n,
+                                                                                 top, out_pos);
+            CK(cudaGetLastError());
+            CK(cudaStreamSynchronize(st));
+            return 0;
+        }
+    }
     size_t tb = 0;
     const int end_bit = bits_for(std::max<int64_t>(max_handle, 1));
     CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, in_handles, k_in, iota, v_in, (int)n, 0, end_bit, st));
@@ -3001,7 +3143,7 @@ int s5g_pack_plan(const uint8_t* arena, int64_t arena_len, const int64_t* handle
     size_t tb = workspace_bytes - ((8 * (size_t)(std::max<int64_t>(n, 1) + 1) + 255) & ~size_t(255));
     g_launches += 3;
     CK(cudaMemsetAsync(size + n, 0, 8, st));
-    if (n) k_plan_sizes<<<blocks_for(n, 256), 256, 0, st>>>(arena, arena_len, handles, order, n, out_handles, size);
+    if (n) k_plan_sizes<<<blocks_for((n + PACK_S - 1) / PACK_S * PACK_G, 256), 256, 0, st>>>(arena, arena_len, handles, order, n, out_handles, size);
     CK(cub::DeviceScan::ExclusiveSum(tmp, tb, size, out_off, n + 1, st));
     k_plan_dest<<<1, 32, 0, st>>>(out_off, n, counts, G, out_dest_bytes);
     CK(cudaGetLastError());

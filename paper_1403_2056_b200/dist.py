@@ -64,12 +64,16 @@ class DistResult:
     n_total: int
 
 
-def _alltoallv(send: torch.Tensor, send_counts: list[int], recv_counts: list[int], group):
+def _alltoallv(send: torch.Tensor, send_counts: list[int], recv_counts: list[int], group,
+               out: torch.Tensor | None = None):
     """Variable-size all-to-all of a 1-D tensor (NCCL all_to_all_single;
-    point-to-point pairs on backends without all-to-all, e.g. gloo)."""
+    point-to-point pairs on backends without all-to-all, e.g. gloo).  `out`:
+    receive in place (sum(recv_counts) elements), e.g. straight into the
+    arena the received strings will live in."""
     G = dist.get_world_size(group)
     r = dist.get_rank(group)
-    recv = torch.empty(sum(recv_counts), dtype=send.dtype, device=send.device)
+    recv = out if out is not None else torch.empty(sum(recv_counts), dtype=send.dtype,
+                                                   device=send.device)
     if dist.get_backend(group) == "nccl":
         dist.all_to_all_single(recv, send, recv_counts, send_counts, group=group)
         return recv
@@ -103,24 +107,39 @@ def _all_gather_strings(items: list[tuple[bytes, int]], device, group) -> list[t
                      dtype=torch.int64, device=device)
     ks = [torch.empty_like(k) for _ in range(G)]
     dist.all_gather(ks, k, group=group)
-    kmax = max(int(x[0]) for x in ks)
-    width = max(int(x[1]) for x in ks)
+    ks = torch.stack(ks).cpu().tolist()  # one device read for all ranks' counts
+    kmax = max(x[0] for x in ks)
+    width = max(x[1] for x in ks)
     if kmax == 0:
         return []
     rec = 16 + width
+    # records built and taken apart with whole-array operations (a numpy call
+    # per string cost ~3 ms per gather of 1024 samples)
     buf = np.zeros((kmax, rec), dtype=np.uint8)
-    for i, (b, g) in enumerate(items):
-        buf[i, :16] = np.array([len(b), g], dtype=np.int64).view(np.uint8)
-        buf[i, 16:16 + len(b)] = np.frombuffer(b, dtype=np.uint8)
+    if items:
+        k_mine = len(items)
+        meta = np.empty((k_mine, 2), dtype=np.int64)
+        meta[:, 0] = [len(b) for b, _ in items]
+        meta[:, 1] = [g for _, g in items]
+        buf[:k_mine, :16] = meta.view(np.uint8).reshape(k_mine, 16)
+        if width:
+            body = b"".join(b.ljust(width, b"\0") for b, _ in items)
+            buf[:k_mine, 16:] = np.frombuffer(body, dtype=np.uint8).reshape(k_mine, width)
     t = torch.from_numpy(buf.reshape(-1)).to(device)
-    out = [torch.empty_like(t) for _ in range(G)]
-    dist.all_gather(out, t, group=group)
+    out = torch.empty(G * t.numel(), dtype=torch.uint8, device=device)
+    dist.all_gather_into_tensor(out, t, group=group) if dist.get_backend(group) == "nccl" else \
+        dist.all_gather(list(out.view(G, -1).unbind(0)), t, group=group)
+    allrec = out.cpu().numpy().reshape(G, kmax, rec)
     res = []
     for q in range(G):
-        a = out[q].cpu().numpy().reshape(kmax, rec)
-        for i in range(int(ks[q][0])):
-            L, g = a[i, :16].view(np.int64)
-            res.append((a[i, 16:16 + int(L)].tobytes(), int(g)))
+        kq = ks[q][0]
+        if not kq:
+            continue
+        a = allrec[q, :kq]
+        meta = np.ascontiguousarray(a[:, :16]).view(np.int64)
+        body = np.ascontiguousarray(a[:, 16:]).tobytes()
+        lens, gs = meta[:, 0].tolist(), meta[:, 1].tolist()
+        res.extend((body[i * width: i * width + lens[i]], gs[i]) for i in range(kq))
     return res
 
 
@@ -176,8 +195,14 @@ def distributed_sort(shard: Shard, backend, group=None, samples_per_rank: int = 
         rbcnt = torch.empty_like(bcnt)
         dist.all_to_all_single(rbcnt, bcnt, group=group) if dist.get_backend(group) == "nccl" else \
             _gather_counts(bcnt, rbcnt, group)
-        rbytes = _alltoallv(payload, byte_counts, [int(x) for x in rbcnt.tolist()], group)
-        arena, handles = backend.unpack(rbytes)
+        rb = [int(x) for x in rbcnt.tolist()]
+        # received straight into the arena the strings will live in, when the
+        # backend offers one (no second copy of the shard)
+        into = backend.recv_arena(sum(rb)) if hasattr(backend, "recv_arena") else None
+        rbytes = _alltoallv(payload, byte_counts, rb, group, out=into)
+        del payload
+        arena, handles = backend.unpack(rbytes, sum(recv_counts)) if into is not None else \
+            backend.unpack(rbytes)
         if stats is not None:  # bytes this rank sends to other ranks (NVLink traffic)
             stats["sent_bytes"] = int(sum(b for q, b in enumerate(byte_counts) if q != r) +
                                       24 * sum(c for q, c in enumerate(counts) if q != r))
@@ -393,25 +418,42 @@ class GpuBackend:
 
         return D.pack_order(ds, order, list(counts))
 
-    def unpack(self, rbytes: torch.Tensor):
+    def recv_arena(self, nbytes: int) -> torch.Tensor:
+        """A padded arena for nbytes of received strings; the all-to-all
+        writes into the returned view and `unpack` adopts it without a copy."""
+        from . import device as D
+
+        self._recv = D.alloc_arena(nbytes, self.comm_device)
+        return self._recv[:nbytes]
+
+    def unpack(self, rbytes: torch.Tensor, n_strings: int | None = None):
         """Received zero-terminated strings -> arena + string starts
-        (s5g_load_delimited with delimiter 0)."""
+        (s5g_load_delimited_n with delimiter 0).  n_strings: how many strings
+        arrived (known from the index exchange), so the starts need
+        n_strings + 1 entries instead of one per byte."""
         from . import _lib
         from . import device as D
 
         alen = int(rbytes.numel())
         dev = rbytes.device
-        arena = D.alloc_arena(alen, dev)
+        own = getattr(self, "_recv", None)
+        if own is not None and alen and own.data_ptr() == rbytes.data_ptr():
+            arena = own  # received in place
+        else:
+            arena = D.alloc_arena(alen, dev)
+            if alen:
+                arena[:alen] = rbytes
+        self._recv = None
         if alen == 0:
             starts = torch.zeros(0, dtype=torch.int64, device=dev)
             return D.DeviceStrings(arena, 0, starts), starts
-        arena[:alen] = rbytes
-        handles = torch.empty(alen + 1, dtype=torch.int64, device=dev)
+        cap = (alen if n_strings is None else int(n_strings)) + 1
+        handles = torch.empty(cap, dtype=torch.int64, device=dev)
         ws = torch.empty(16 + 4 * ((alen + 16383) // 16384), dtype=torch.uint8, device=dev)
         n = C.c_int64()
-        _lib.check(_lib.lib().s5g_load_delimited(arena.data_ptr(), alen, 0, handles.data_ptr(),
-                                                 C.byref(n), ws.data_ptr(), ws.numel(),
-                                                 torch.cuda.current_stream(dev).cuda_stream))
+        _lib.check(_lib.lib().s5g_load_delimited_n(arena.data_ptr(), alen, 0, handles.data_ptr(), cap,
+                                                   C.byref(n), ws.data_ptr(), ws.numel(),
+                                                   torch.cuda.current_stream(dev).cuda_stream))
         starts = handles[: n.value]
         return D.DeviceStrings(arena, alen, starts), starts
 
