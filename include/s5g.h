@@ -197,6 +197,18 @@ int s5g_load_delimited(uint8_t *data, int64_t len, int32_t delimiter, int64_t *o
 int s5g_load_delimited_n(uint8_t *data, int64_t len, int32_t delimiter, int64_t *out_handles,
                          int64_t capacity, int64_t *out_n, void *workspace,
                          size_t workspace_bytes, void *stream);
+/* ... and with a rank directory: out_rank64 (device, ceil(len / 64) entries)
+ * receives the number of terminators before each 64-byte block of the arena.
+ * s5g_rank_positions then maps string starts of this arena (query, device, m
+ * entries, each one of out_handles[0 .. n)) to their index in out_handles:
+ * out_pos[j] = i with out_handles[i] == query[j] -- one directory entry plus
+ * the block's bytes before the handle per query, no search.  The multi-GPU
+ * path uses it to carry global indices through the local sort. */
+int s5g_load_delimited_rank(uint8_t *data, int64_t len, int32_t delimiter, int64_t *out_handles,
+                            int64_t capacity, int64_t *out_n, uint32_t *out_rank64,
+                            void *workspace, size_t workspace_bytes, void *stream);
+int s5g_rank_positions(const uint8_t *arena, int64_t arena_len, const uint32_t *rank64,
+                       const int64_t *query, int64_t m, int64_t *out_pos, void *stream);
 
 /* Stable grouping by destination rank for the all-to-all send buffer
  * (device): out_order[k] = index of the k-th string when strings are ordered

@@ -76,6 +76,8 @@ SIGNATURES = {
     "s5g_lengths": (C.c_int, [_p, _i64, _p, _i64, _p, _p]),
     "s5g_load_delimited": (C.c_int, [_p, _i64, _i32, _p, C.POINTER(_i64), _p, C.c_size_t, _p]),
     "s5g_load_delimited_n": (C.c_int, [_p, _i64, _i32, _p, _i64, C.POINTER(_i64), _p, C.c_size_t, _p]),
+    "s5g_load_delimited_rank": (C.c_int, [_p, _i64, _i32, _p, _i64, C.POINTER(_i64), _p, _p, C.c_size_t, _p]),
+    "s5g_rank_positions": (C.c_int, [_p, _i64, _p, _p, _i64, _p, _p]),
     "s5g_dist_stats": (C.c_int, [_p, _i64, C.POINTER(_i64), C.POINTER(_i64), _p]),
     "s5g_pack": (C.c_int, [_p, _i64, _p, _p, _p, _i64, _p, _p]),
     "s5g_profile_enable": (None, [C.c_int]),

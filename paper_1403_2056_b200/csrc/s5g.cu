@@ -1232,8 +1232,12 @@ __global__ void k_ld_scan(uint32_t* __restrict__ chunk_cnt, int64_t nchunks, int
 }
 
 // string k starts right after terminator k-1 (string 0 at offset 0)
+// rank64 (optional): terminators before each 64-byte block, i.e. the index of
+// the first string starting after the block's first byte -- the rank
+// directory s5g_rank_positions reads.
 __global__ void k_ld_write(const uint8_t* __restrict__ data, int64_t len,
-                           const uint32_t* __restrict__ chunk_off, int64_t* __restrict__ handles) {
+                           const uint32_t* __restrict__ chunk_off, int64_t* __restrict__ handles,
+                           uint32_t* __restrict__ rank64) {
     __shared__ uint32_t wsum[32];
     const int64_t t0 = (int64_t)blockIdx.x * LD_CHUNK + (int64_t)threadIdx.x * 64;
     uint64_t z[8];  // zero-byte masks of the thread's 64 bytes, in order
@@ -1250,6 +1254,7 @@ __global__ void k_ld_write(const uint8_t* __restrict__ data, int64_t len,
         cntv += __popcll(z[2 * q]) + __popcll(z[2 * q + 1]);
     }
     uint32_t k = chunk_off[blockIdx.x] + block_excl_sum<LD_NT>(cntv, wsum, nullptr);
+    if (rank64 && t0 < len) rank64[t0 >> 6] = k;
     if (blockIdx.x == 0 && threadIdx.x == 0) handles[0] = 0;
 #pragma unroll
     for (int j = 0; j < 8; j++)
@@ -1391,6 +1396,34 @@ __global__ void k_pos_search(const int64_t* __restrict__ in_h, const int64_t* __
             out_pos[j] = pos[u];
         }
     }
+}
+// Index of the string starting at each query handle of an arena loaded by
+// s5g_load_delimited_rank: the terminators before the handle's 64-byte block
+// (rank64) plus those in the block before the handle -- one directory entry
+// and at most eight aligned words per query, all loads independent (the
+// binary search over the starts walked ~25 dependent levels).
+__global__ void k_rank_positions(const uint8_t* __restrict__ arena, int64_t alen,
+                                 const uint32_t* __restrict__ rank64,
+                                 const int64_t* __restrict__ query, int64_t m,
+                                 int64_t* __restrict__ out_pos) {
+    const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (j >= m) return;
+    const int64_t h = query[j];
+    S5G_CHECK(h >= 0 && h < alen);
+    const int64_t b0 = h & ~int64_t(63);
+    uint32_t r = rank64[h >> 6];
+    const int full = (int)((h - b0) >> 3), rest = (int)(h & 7);
+    uint64_t w[8];
+#pragma unroll
+    for (int q = 0; q < 8; q++)
+        w[q] = q <= full ? __ldg(reinterpret_cast<const unsigned long long*>(arena + b0 + 8 * q)) : ~0ull;
+#pragma unroll
+    for (int q = 0; q < 8; q++) {
+        uint64_t z = zero_bytes(w[q]);
+        if (q == full) z &= rest ? (~0ull >> (64 - 8 * rest)) : 0ull;  // bytes before h only
+        if (q <= full) r += __popcll(z);
+    }
+    out_pos[j] = r;
 }
 __global__ void k_pos_match(const int32_t* __restrict__ in_pos, const int32_t* __restrict__ out_idx,
                             int64_t n, int64_t* __restrict__ out_pos) {
@@ -2975,6 +3008,13 @@ int s5g_load_delimited(uint8_t* data, int64_t len, int32_t delimiter, int64_t* o
 int s5g_load_delimited_n(uint8_t* data, int64_t len, int32_t delimiter, int64_t* out_handles,
                          int64_t capacity, int64_t* out_n, void* workspace,
                          size_t workspace_bytes, void* stream) {
+    return s5g_load_delimited_rank(data, len, delimiter, out_handles, capacity, out_n, nullptr,
+                                   workspace, workspace_bytes, stream);
+}
+
+int s5g_load_delimited_rank(uint8_t* data, int64_t len, int32_t delimiter, int64_t* out_handles,
+                            int64_t capacity, int64_t* out_n, uint32_t* out_rank64,
+                            void* workspace, size_t workspace_bytes, void* stream) {
     if (len < 0 || delimiter < 0 || delimiter > 255) return fail(S5G_E_INVALID, "delimiter must be a byte value");
     if (capacity < 0) return fail(S5G_E_INVALID, "negative capacity");
     cudaStream_t st = (cudaStream_t)stream;
@@ -3000,7 +3040,7 @@ int s5g_load_delimited_n(uint8_t* data, int64_t len, int32_t delimiter, int64_t*
     if (hbad) return fail(S5G_E_INVALID, "input contains byte 0, which is reserved as terminator");
     // (k_ld_write stores a start after every terminator: count + 1 entries)
     if (hn + 1 > capacity) return fail(S5G_E_INVALID, "more strings than out_handles has room for");
-    k_ld_write<<<(unsigned)nchunks, LD_NT, 0, st>>>(data, len, chunk, out_handles);
+    k_ld_write<<<(unsigned)nchunks, LD_NT, 0, st>>>(data, len, chunk, out_handles, out_rank64);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(st));
     *out_n = hn;
@@ -3109,6 +3149,18 @@ int s5g_input_positions(const int64_t* in_handles, const int64_t* out_handles, i
     CK(cub::DeviceRadixSort::SortPairs(tmp, tb, in_handles, k_in, iota, v_in, (int)n, 0, end_bit, st));
     CK(cub::DeviceRadixSort::SortPairs(tmp, tb, out_handles, k_out, iota, v_out, (int)n, 0, end_bit, st));
     k_pos_match<<<blocks_for(n, 256), 256, 0, st>>>(v_in, v_out, n, out_pos);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(st));
+    return 0;
+}
+
+int s5g_rank_positions(const uint8_t* arena, int64_t arena_len, const uint32_t* rank64,
+                       const int64_t* query, int64_t m, int64_t* out_pos, void* stream) {
+    if (m < 0 || arena_len < 0) return fail(S5G_E_INVALID, "negative size");
+    if (m == 0) return 0;
+    cudaStream_t st = (cudaStream_t)stream;
+    g_launches++;
+    k_rank_positions<<<blocks_for(m, 256), 256, 0, st>>>(arena, arena_len, rank64, query, m, out_pos);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(st));
     return 0;

@@ -31,6 +31,9 @@ class DeviceStrings:
     arena: torch.Tensor      # uint8, arena_len + pad bytes, pad zeroed
     arena_len: int
     handles: torch.Tensor    # int64[n]
+    # terminators before each 64-byte block (s5g_load_delimited_rank), when
+    # the handles are the arena's string starts: start -> index without a search
+    rank64: torch.Tensor | None = None
 
     @property
     def n(self) -> int:
@@ -333,6 +336,18 @@ def input_positions(in_handles: torch.Tensor, out_handles: torch.Tensor, max_han
     check(lib().s5g_input_positions(in_handles.data_ptr(), out_handles.data_ptr(), n,
                                     int(max(max_handle, 1)), out.data_ptr(), ws.data_ptr(),
                                     ws.numel(), torch.cuda.current_stream(dev).cuda_stream))
+    return out
+
+
+def rank_positions(ds: DeviceStrings, query: torch.Tensor) -> torch.Tensor:
+    """Index of the string starting at each query handle, for an arena loaded
+    with its rank directory (s5g_rank_positions)."""
+    m = query.numel()
+    out = torch.empty(m, dtype=torch.int64, device=query.device)
+    if m:
+        check(lib().s5g_rank_positions(ds.arena.data_ptr(), ds.arena_len, ds.rank64.data_ptr(),
+                                       query.contiguous().data_ptr(), m, out.data_ptr(),
+                                       torch.cuda.current_stream(query.device).cuda_stream))
     return out
 
 

@@ -210,7 +210,8 @@ def distributed_sort(shard: Shard, backend, group=None, samples_per_rank: int = 
         raise ValueError(f"unknown exchange mode: {mode}")
     # 4. local sort: received in global input order -> stable local sort
     perm, lcps = backend.local_sort(arena, handles, want_lcps, **sort_kw)
-    sorted_h = backend.take(handles, perm)
+    sorted_h = backend.sorted_handles(handles, perm) if hasattr(backend, "sorted_handles") else \
+        backend.take(handles, perm)
     sorted_g = backend.take(gidx, perm)
     # 5. LCP at the rank boundary
     if want_lcps:
@@ -450,12 +451,14 @@ class GpuBackend:
         cap = (alen if n_strings is None else int(n_strings)) + 1
         handles = torch.empty(cap, dtype=torch.int64, device=dev)
         ws = torch.empty(16 + 4 * ((alen + 16383) // 16384), dtype=torch.uint8, device=dev)
+        rank = torch.empty((alen + 63) // 64, dtype=torch.int32, device=dev)
         n = C.c_int64()
-        _lib.check(_lib.lib().s5g_load_delimited_n(arena.data_ptr(), alen, 0, handles.data_ptr(), cap,
-                                                   C.byref(n), ws.data_ptr(), ws.numel(),
-                                                   torch.cuda.current_stream(dev).cuda_stream))
+        _lib.check(_lib.lib().s5g_load_delimited_rank(arena.data_ptr(), alen, 0, handles.data_ptr(), cap,
+                                                      C.byref(n), rank.data_ptr(), ws.data_ptr(),
+                                                      ws.numel(),
+                                                      torch.cuda.current_stream(dev).cuda_stream))
         starts = handles[: n.value]
-        return D.DeviceStrings(arena, alen, starts), starts
+        return D.DeviceStrings(arena, alen, starts, rank), starts
 
     def local_sort(self, ds, handles, want_lcps, **kw):
         """Sorted permutation of `handles` and the LCPs: s5g_sort, then
@@ -465,7 +468,19 @@ class GpuBackend:
 
         local = D.DeviceStrings(ds.arena, ds.arena_len, handles)
         out_h, lcps, _ = D.sort(local, want_lcps=want_lcps, **kw)
+        self._sorted_h = out_h
+        if ds.rank64 is not None and handles.data_ptr() == ds.handles.data_ptr():
+            # the handles are the received arena's string starts: index by
+            # the rank directory (s5g_rank_positions), no search and no sort
+            return D.rank_positions(ds, out_h), lcps
         return D.input_positions(handles, out_h, ds.arena_len), lcps
+
+    def sorted_handles(self, handles, perm):
+        """handles[perm] -- the last local sort's own output when it is at hand."""
+        out_h, self._sorted_h = getattr(self, "_sorted_h", None), None
+        if out_h is not None and out_h.numel() == perm.numel():
+            return out_h
+        return self.take(handles, perm)
 
     def string_bytes(self, ds, h1: torch.Tensor) -> bytes:
         from . import device as D
