@@ -722,10 +722,11 @@ __global__ void __launch_bounds__(STEP_NT, STEP_MINB) k_step_cta(
     Rec* X = (in_b ? recB : recA) + lo;
     Rec* Y = (in_b ? recA : recB) + lo;
     int nvalid = sg.flags & SEG_NV_MASK;
-    const int v = (int)med_tree_capacity(n, vcap), L = levels_of(v), nb = 2 * v + 1;
-    const int count = med_sample_count(v);
+    const MedPlan mp = med_plan(n, vcap);
+    const int v = mp.v, L = levels_of(v), nb = 2 * v + 1;
+    const int count = mp.count;  // real sample keys; the rest of [0, P) is ~0 padding
     int P = 1;
-    while (P < count) P <<= 1;
+    while (P < mp.countp) P <<= 1;
     // cached words consumed in place: X[i].w[wo] is the word at `depth`,
     // nvalid words from wo on are valid
     int wo = 0;
@@ -829,7 +830,7 @@ __global__ void __launch_bounds__(STEP_NT, STEP_MINB) k_step_cta(
         }
         // ---- select_splitters (ssss.py:85-146) ------------------------------
         bitonic_u64<STEP_NT>(S.s, P);
-        select_tree<STEP_NT>(S.s, count, v, L, S.sa, S.sb, S.sp, S.tree, S.inorder, S.tpos, S.eqb);
+        select_tree<STEP_NT>(S.s, mp.countp, v, L, S.sa, S.sb, S.sp, S.tree, S.inorder, S.tpos, S.eqb);
         __syncthreads();
         // ---- classify + bucket counts (ssss.py:149-181, 292) -------------
         constexpr int CU = 4;  // keys in flight per thread

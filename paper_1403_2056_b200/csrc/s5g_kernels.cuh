@@ -120,8 +120,11 @@ constexpr int MED_MAX = MED_MAX_CFG;
 #ifndef MED_VMAX_CFG
 #define MED_VMAX_CFG 31
 #endif
+#ifndef MED_FREE_V
+#define MED_FREE_V 1  // 0: splitter counts 2^L - 1 only, 4-fold oversampling (the earlier plan)
+#endif
 #ifndef MED_TARGET_CFG
-#define MED_TARGET_CFG 1024
+#define MED_TARGET_CFG (MED_FREE_V ? 745 : 1024)
 #endif
 constexpr int MED_VMAX = MED_VMAX_CFG;  // <= 2*MED_VMAX+1 <= 255 buckets (uint8 ids)
 constexpr int MED_NB = 2 * MED_VMAX + 1;
@@ -141,6 +144,46 @@ __host__ __device__ inline int med_sample_count(int64_t v) {
     const int a = sample_count(v);
     const int cap = 4 * (int)(v + 1) - 1;
     return a < cap ? a : cap;
+}
+
+// Why: a fused step's children should FIT a finisher class, not straddle
+// one.  With 2^L - 1 splitters and 4-fold oversampling C5's 4096-string
+// segments split into 4 pieces of 1024 +- 50 %: half of them overflowed the
+// 1024-slot class into the 2048-slot one at ~60 % fill.  Six pieces of
+// 683 +- 25 % (MED_TARGET 745, 16-fold oversampling) nearly all fit it:
+// C5 36.5 -> 35.9 ms, C4 7.20 -> 7.05 ms, C2 / C3 unchanged.  Measured
+// alternatives: target 820 / 32-fold 35.9 (C2 +0.6 %), 820 / 64-fold 36.6,
+// 380 / 32-fold 36.1 (C3 +7 %, C4 +4 %), 640 / 16 36.0 (C3 +6 %), 900 / 16
+// 36.0, 745 / 8 36.1, 1024 / 16 36.6.
+// Fused steps with a free number of splitters (MED_FREE_V): `veff` real
+// splitters -- buckets of about MED_TARGET strings, not rounded to 2^L - 1 --
+// in the complete tree of v = 2^L - 1 >= veff nodes, its last v - veff
+// splitters the sample's ~0 padding (empty buckets at the top end).  With
+// a-fold oversampling the sample has a (veff + 1) - 1 keys and select_tree is
+// given a (v + 1) - 1: its equidistant picks at k a - 1 land on real keys for
+// k <= veff and in the padding above.
+#ifndef MED_OVERSAMPLE
+#define MED_OVERSAMPLE 16
+#endif
+struct MedPlan { int v, veff, count, countp; };
+__host__ __device__ inline MedPlan med_plan(int64_t n, int64_t vcap) {
+    MedPlan p;
+#if MED_FREE_V
+    int64_t want = (n + MED_TARGET - 1) / MED_TARGET - 1;
+    want = want < 1 ? 1 : want > MED_VMAX ? MED_VMAX : want;
+    const int64_t t = tree_capacity(n, vcap);
+    p.veff = (int)(want < t ? want : t);
+    p.v = 1;
+    while (p.v < p.veff) p.v = 2 * p.v + 1;
+    int a = MED_OVERSAMPLE;
+    while (a > 2 && a * (p.v + 1) > 16 * (MED_VMAX + 1)) a >>= 1;  // StepCtaSmem::s
+    p.count = a * (p.veff + 1) - 1;
+    p.countp = a * (p.v + 1) - 1;
+#else
+    p.v = p.veff = (int)med_tree_capacity(n, vcap);
+    p.count = p.countp = med_sample_count(p.v);
+#endif
+    return p;
 }
 
 __host__ __device__ inline int size_class(int64_t n) {
