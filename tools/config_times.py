@@ -14,6 +14,8 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--configs", default="c1_random,c2_dna,c3_urls,c4_suffixes,c5_nodup")
 ap.add_argument("--reps", type=int, default=7)
 ap.add_argument("--v", type=int, default=8191, help="splitter cap (tuning only)")
+ap.add_argument("--t-medium", type=int, default=1 << 20,
+                help="segments below it go to the finishers (tuning only; the library caps it at 2049)")
 a = ap.parse_args()
 for spec in a.configs.split(","):
     name, _, sc = spec.partition(":")
@@ -28,12 +30,12 @@ for spec in a.configs.split(","):
     out = (torch.empty(len(hnd), dtype=torch.int64, device="cuda"),
            torch.empty(len(hnd), dtype=torch.int64, device="cuda"))
     for _ in range(2):
-        D.sort(ds, want_lcps=True, out=out, workspace=ws, v=a.v)
+        D.sort(ds, want_lcps=True, out=out, workspace=ws, v=a.v, t_medium=a.t_medium)
     ts = []
     for _ in range(a.reps):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        D.sort(ds, want_lcps=True, out=out, workspace=ws, v=a.v)
+        D.sort(ds, want_lcps=True, out=out, workspace=ws, v=a.v, t_medium=a.t_medium)
         e1.record()
         torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1))
