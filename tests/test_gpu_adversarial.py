@@ -102,3 +102,28 @@ def test_full_width_tiles_with_one_bucket():
     odd = rng.integers(0, n, size=5000)
     buf[odd, :3] = rng.integers(97, 123, size=(5000, 3), dtype=np.uint8)
     _check(buf.reshape(-1), np.arange(n, dtype=np.int64) * 4)
+
+
+@pytest.mark.parametrize("n", [3000, 20000, 30000, 200000])
+def test_keys_equal_to_the_tree_padding(n):
+    """Words of eight 0xFF bytes equal the ~0 padding that fills a fused
+    step's splitter tree above its real splitters (med_plan): they must land
+    in one all-equal bucket a word deeper, next to smaller and terminated
+    keys, at fused-step sizes (the first step of an input <= 32768 strings is
+    a fused one) and below a device-wide root."""
+    rng = np.random.default_rng(n)
+    kinds = rng.integers(0, 4, size=n)
+    strs = []
+    for k in kinds:
+        tail = bytes(rng.integers(250, 256, size=int(rng.integers(0, 12)), dtype=np.uint8))
+        if k == 0:
+            strs.append(b"\xff" * 8 + tail)              # word 0 == ~0
+        elif k == 1:
+            strs.append(b"\xff" * 16 + tail)             # words 0 and 1 == ~0
+        elif k == 2:
+            strs.append(b"\xff" * int(rng.integers(0, 8)))  # terminated inside word 0
+        else:
+            strs.append(bytes(rng.integers(1, 256, size=8, dtype=np.uint8)) + tail)
+    buf = np.frombuffer(b"".join(s + b"\0" for s in strs), dtype=np.uint8).copy()
+    hnd = np.concatenate(([0], np.cumsum([len(s) + 1 for s in strs])[:-1])).astype(np.int64)
+    _check(buf, hnd)
