@@ -66,7 +66,10 @@ struct SegDev {
 // warps of 256 slots for <= 512, 1024, 2048
 constexpr int NCLS = 7;
 constexpr int SMALL_MAX = 2048;
-constexpr int SEG_TARGET = 1024;   // device-wide steps aim at buckets of this size
+#ifndef SEG_TARGET_CFG
+#define SEG_TARGET_CFG 1024
+#endif
+constexpr int SEG_TARGET = SEG_TARGET_CFG;   // device-wide steps aim at buckets of this size
 
 struct Counters {
     unsigned long long n_large, n_bound, fetches, seg_fetches, small_elems;
