@@ -1101,17 +1101,31 @@ __global__ void k_lengths(const uint8_t* __restrict__ arena, int64_t alen,
 // thread per string walked its ~15 words alone: 1 TB/s on C5's strings; a
 // warp per string with byte stores was a chain of dependent round trips.)
 constexpr int PACK_G = 8;
-constexpr int PACK_S = 4;  // strings per lane group: their loads are issued together
-__global__ void k_pack(const uint8_t* __restrict__ arena, int64_t alen,
+#ifndef PACK_S_CFG
+#define PACK_S_CFG 2
+#endif
+#ifndef PLAN_MINB
+#define PLAN_MINB 8  // k_plan_sizes: 2 strings, <= 32 registers: 2.66 ms on 2^25 C5 strings (4 strings at 47 registers: 2.71)
+#endif
+constexpr int PACK_S = PACK_S_CFG;  // strings per lane group: their loads are issued together
+#ifndef PACK_SP_CFG
+#define PACK_SP_CFG 2
+#endif
+#ifndef PACK_MINB
+#define PACK_MINB 6
+#endif
+constexpr int PACK_SP = PACK_SP_CFG;  // ... in k_pack: 2 strings and <= 42 registers (6 CTAs per SM) --
+// 2.66 ms on 2^25 C5 strings against 3.27 with 4 strings at 64 registers, 2.86 with 1 string at 32
+__global__ void __launch_bounds__(256, PACK_MINB) k_pack(const uint8_t* __restrict__ arena, int64_t alen,
                        const int64_t* __restrict__ handles, const int64_t* __restrict__ lens,
                        const int64_t* __restrict__ dst_off, int64_t n, uint8_t* __restrict__ dst) {
     const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t grp = t / PACK_G;
     const int sub = (int)(t % PACK_G);
-    int64_t h[PACK_S], o[PACK_S], e[PACK_S], a[PACK_S], z[PACK_S];
+    int64_t h[PACK_SP], o[PACK_SP], e[PACK_SP], a[PACK_SP], z[PACK_SP];
 #pragma unroll
-    for (int u = 0; u < PACK_S; u++) {
-        const int64_t i = grp * PACK_S + u;
+    for (int u = 0; u < PACK_SP; u++) {
+        const int64_t i = grp * PACK_SP + u;
         h[u] = o[u] = e[u] = 0;  // (an empty copy)
         if (i < n) {
             h[u] = handles[i];
@@ -1121,7 +1135,7 @@ __global__ void k_pack(const uint8_t* __restrict__ arena, int64_t alen,
         }
     }
 #pragma unroll
-    for (int u = 0; u < PACK_S; u++) {
+    for (int u = 0; u < PACK_SP; u++) {
         a[u] = min((o[u] + 7) & ~int64_t(7), e[u]);
         z[u] = max(e[u] & ~int64_t(7), a[u]);
     }
@@ -1139,20 +1153,20 @@ __global__ void k_pack(const uint8_t* __restrict__ arena, int64_t alen,
     // two rounds of 64 bytes per string with all the group's loads in flight
 #pragma unroll
     for (int r = 0; r < 2; r++) {
-        uint64_t w[PACK_S];
+        uint64_t w[PACK_SP];
 #pragma unroll
-        for (int u = 0; u < PACK_S; u++) {
+        for (int u = 0; u < PACK_SP; u++) {
             const int64_t q = a[u] + 8 * (sub + PACK_G * r);
             w[u] = q < z[u] ? word_at(u, q) : 0;
         }
 #pragma unroll
-        for (int u = 0; u < PACK_S; u++) {
+        for (int u = 0; u < PACK_SP; u++) {
             const int64_t q = a[u] + 8 * (sub + PACK_G * r);
             if (q < z[u]) *reinterpret_cast<uint64_t*>(dst + q) = w[u];
         }
     }
 #pragma unroll
-    for (int u = 0; u < PACK_S; u++) {
+    for (int u = 0; u < PACK_SP; u++) {
         for (int64_t q = a[u] + 8 * (sub + PACK_G * 2); q < z[u]; q += 8 * PACK_G)
             *reinterpret_cast<uint64_t*>(dst + q) = word_at(u, q);
         if (o[u] + sub < a[u]) dst[o[u] + sub] = byte_at(u, o[u] + sub);  // < 8 head bytes
@@ -1435,7 +1449,7 @@ __global__ void k_pos_match(const int32_t* __restrict__ in_pos, const int32_t* _
 // send order.  Eight lanes per string look at eight consecutive aligned words
 // per round and vote for the first terminator (one thread per string walked
 // its words alone, a chain of dependent loads per string).
-__global__ void k_plan_sizes(const uint8_t* __restrict__ arena, int64_t alen,
+__global__ void __launch_bounds__(256, PLAN_MINB) k_plan_sizes(const uint8_t* __restrict__ arena, int64_t alen,
                              const int64_t* __restrict__ handles, const int64_t* __restrict__ order,
                              int64_t n, int64_t* __restrict__ out_h, int64_t* __restrict__ size) {
     const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -2993,7 +3007,7 @@ int s5g_pack(const uint8_t* arena, int64_t arena_len, const int64_t* handles,
     if (n <= 0) return n < 0 ? fail(S5G_E_INVALID, "negative n") : 0;
     cudaStream_t st = (cudaStream_t)stream;
     g_launches++;
-    k_pack<<<blocks_for((n + PACK_S - 1) / PACK_S * PACK_G, 256), 256, 0, st>>>(arena, arena_len, handles, lengths, dst_off, n,
+    k_pack<<<blocks_for((n + PACK_SP - 1) / PACK_SP * PACK_G, 256), 256, 0, st>>>(arena, arena_len, handles, lengths, dst_off, n,
                                                 dst);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(st));
